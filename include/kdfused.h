@@ -1,0 +1,131 @@
+/* kdfused.h — C ABI of the B200-native (sm_100a) fused knowledge-distillation hot path.
+ *
+ * What it computes (§3.2): the student receives only the teacher's final hidden
+ * states H_t and "locally recomputes the full logit distributions using the teacher's language model
+ * head", which "preserv[es] the mathematical equivalence to standard logit-based KD" (P:136,
+ * P:266).  One call computes, for every token n with mask_n = 1,
+ *
+ *     Z_t = H_t · W_tᵀ ,  Z_s = H_s · W_sᵀ                       (both LM heads, fused; never stored)
+ *     p = softmax(Z_t / T) , q = softmax(Z_s / T)
+ *     ℓ_n = FKL Σ p ln(p/q) | RKL Σ q ln(q/p) | JSD_β β KL(p‖m)+(1−β) KL(q‖m), m = βp+(1−β)q
+ *           | TVD ½ Σ |p − q|                                     (P:153 names all four)
+ *     G   = loss_scale · mask_n · ∂ℓ_n/∂Z_s                          (teacher constant)
+ *     dL/dh_s = G · W_s ,   dL/dW_s (+)= Gᵀ · H_s                    ("backward passes")
+ *
+ * The vocabulary is swept in 128-column tiles with an online log-sum-exp, so no [tokens × V] logit
+ * tensor exists in HBM (BASELINE.json north_star).  Definitions and the readings of points the paper
+ * leaves open (no T² factor, β convention, reduction, masking) are in DESIGN.md "Readings" R1-R12.
+ *
+ * Conventions for every entry point
+ *  - All tensor pointers are DEVICE pointers (cudaMalloc / PyTorch CUDA memory), row-major, owned by
+ *    the caller; the library never allocates device memory and never frees caller memory.
+ *  - Every call is asynchronous on `stream` (no host synchronisation; the caller keeps inputs alive
+ *    until the stream passes the call).  Invalid arguments are rejected BEFORE any launch with a
+ *    non-zero kd_status; kd_last_error() then returns a thread-local message.
+ *  - bf16 matrices need 16-byte aligned base pointers; hidden widths d_t, d_s must be multiples of 64.
+ *  - Rows with mask = 0 are never read (NaN garbage there cannot affect any output).
+ *  - Results are deterministic (fixed reduction orders, no atomics in any floating-point sum).
+ */
+#ifndef KDFUSED_H_
+#define KDFUSED_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KDFUSED_ABI_VERSION 1
+
+typedef enum {
+  KD_FKL = 0, /* forward KL  Σ p ln(p/q) */
+  KD_RKL = 1, /* reverse KL  Σ q ln(q/p) */
+  KD_JSD = 2, /* β-JSD, m = βp + (1−β)q, β ∈ (0,1)            (reading R4) */
+  KD_TVD = 3  /* total variation ½ Σ |p − q| */
+} kd_div_kind;
+
+typedef enum {
+  KD_OK = 0,
+  KD_ERR_INVALID_ARG = 1,         /* T <= 0 or non-finite, β ∉ (0,1), unknown kind, NULL required ptr */
+  KD_ERR_SHAPE = 2,               /* inconsistent / unsupported sizes (d % 64 != 0, empty vocab range) */
+  KD_ERR_ALIGNMENT = 3,           /* a pointer is not 16-byte aligned */
+  KD_ERR_UNSUPPORTED = 4,         /* valid request this build does not implement */
+  KD_ERR_WORKSPACE_TOO_SMALL = 5, /* workspace_bytes < kd_workspace_size(p) or misaligned workspace */
+  KD_ERR_CUDA = 6                 /* a CUDA runtime/driver call failed (message in kd_last_error) */
+} kd_status;
+
+/* Problem description (plain data, no pointers). */
+typedef struct {
+  int64_t n_tokens;      /* N: packed token rows (ragged sequences concatenated by the caller), >= 0 */
+  int32_t d_t;           /* teacher hidden width, multiple of 64 */
+  int32_t d_s;           /* student hidden width, multiple of 64 */
+  int64_t vocab;         /* global V (151936 for Qwen3) */
+  int64_t v_begin;       /* this caller's vocabulary rows [v_begin, v_end); [0, V) on one GPU */
+  int64_t v_end;
+  float temperature;     /* T > 0, applied to teacher and student logits (reading R2: no T² factor) */
+  int32_t kind;          /* kd_div_kind */
+  float jsd_beta;        /* JSD only; in (0,1); BASELINE.json pins 0.5 */
+  float loss_scale;      /* L = loss_scale · Σ_n mask_n ℓ_n; 1/max(1,Σmask) gives SPEC's mean */
+  int32_t want_dW;       /* 0: skip dL/dW_s */
+  int32_t accumulate_dW; /* 1: dW_s += (gradient accumulation, P:210 GA=8); 0: dW_s = */
+  int32_t chunk_tokens;  /* token chunk Nc bounding the G scratch (0 = default 4096; rounded to 128) */
+  int32_t reserved[5];   /* must be zero */
+} kd_problem;
+
+/* Bytes of device workspace kd_fused_fwd_bwd needs for `p` (a pure function of p and the current
+ * device's SM count).  Returns 0 if p is invalid (see kd_last_error). */
+size_t kd_workspace_size(const kd_problem* p);
+
+/* The whole hot path in one call (single GPU, or one token shard of a token-sharded job).
+ *   h_t  [N, d_t]   bf16  teacher final (post-norm) hidden states
+ *   W_t  [V_r, d_t] bf16  teacher LM-head rows v_begin..v_end (nn.Linear layout, reading R7)
+ *   h_s  [N, d_s]   bf16  student final hidden states
+ *   W_s  [V_r, d_s] bf16  student LM-head rows
+ *   mask [N]        u8    1 = loss-bearing token, 0 = masked; NULL = all ones
+ *   loss [N]        f32   out: per-token divergence ℓ_n in nats (0 where mask = 0)
+ *   dh_s [N, d_s]   f32   out: loss_scale · mask_n · ∂ℓ_n/∂h_s[n]
+ *   dW_s [V_r, d_s] f32   out (want_dW): ∂L/∂W_s (accumulated if accumulate_dW), else may be NULL
+ *   n_nonfinite [1] i64   out (device): number of tokens whose ℓ_n is non-finite; may be NULL
+ *   workspace            device scratch of >= kd_workspace_size(p) bytes, 256-byte aligned
+ * Requires v_begin == 0 and v_end == vocab (use the kd_vocab_* entry points for vocab shards). */
+kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                           const void* W_s, const uint8_t* mask, float* loss, float* dh_s, float* dW_s,
+                           int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- vocabulary-sharded execution (north_star: "vocabulary sharding of W_t/W_s, with a tiny
+ * all-reduce of per-token stats").  Rank r owns rows [v_begin, v_end) of both heads.  FKL/RKL only.
+ *   1) kd_vocab_stats      -> rec [5][N] f32: this shard's per-token record (base-2 running maxima,
+ *                              sums and cross term; R10), 0-filled for masked rows.
+ *   2) caller all-gathers the P records into recs [P][5][N] (any transport; 20 B/token/rank).
+ *   3) kd_vocab_backward   merges the P records in rank order (deterministic), writes the loss, this
+ *                              shard's PARTIAL dh_s (caller all-reduces SUM over ranks) and the local
+ *                              dW_s rows.  */
+kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                         const void* W_s, const uint8_t* mask, float* rec, void* workspace,
+                         size_t workspace_bytes, void* stream);
+kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                            const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
+                            float* loss, float* dh_s_partial, float* dW_s, int64_t* n_nonfinite,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* Building block exposed for verification: D[M, N] = A · Bᵀ with bf16 operands and fp32 tcgen05
+ * accumulation.  A is [M, K] (a_mn_major = 0) or stored transposed as [K, M] (a_mn_major = 1); B is
+ * [N, K] (b_mn_major = 0) or [K, N] (b_mn_major = 1).  D is [M, N] fp32 row-major.  M, N, K >= 1,
+ * N % 32 == 0, K % 8 == 0 (K-major) / M, N % 8 == 0 (MN-major). */
+kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
+                           int32_t a_mn_major, int32_t b_mn_major, void* stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued (bench bookkeeping). */
+int32_t kd_last_launch_count(void);
+
+/* Thread-local message describing the last non-OK status (never NULL). */
+const char* kd_last_error(void);
+
+/* KDFUSED_ABI_VERSION of the loaded library. */
+int32_t kd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KDFUSED_H_ */

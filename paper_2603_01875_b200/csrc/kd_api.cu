@@ -1,0 +1,536 @@
+// kd_api.cu — host side of the C ABI declared in include/kdfused.h.
+//
+// Validation, the execution plan (token chunking, vocab-split and split-K choices sized to the SM
+// count), workspace carving, TMA tensor-map encoding and the launch sequence on the caller's stream.
+// Everything here is plain host C++; every floating-point step of the method runs in the kernels of
+// kd_pass.cu / kd_gemm.cu / kd_aux.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/kdfused.h"
+#include "kd_params.cuh"
+
+namespace kd {
+cudaError_t launch_pass(int pass, int kind, const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t s);
+cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, const CUtensorMap* a0, const CUtensorMap* a1,
+                        const CUtensorMap* b, const GemmParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_compact(const uint8_t* mask, int N, int* idx, int* n_eff, cudaStream_t s);
+cudaError_t launch_gather(const __nv_bfloat16* src, long long src_ld, __nv_bfloat16* dst, int d, int N,
+                          const int* idx, const int* n_eff, cudaStream_t s);
+cudaError_t launch_zero_masked(const uint8_t* mask, int N, float* loss, float* dh, int d_s, cudaStream_t s);
+cudaError_t launch_merge(const float* part, long long plane, long long split_stride, int n_split, int n_rows,
+                         int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
+                         long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, cudaStream_t s);
+cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, int kind, float beta,
+                        float* kfin, float* loss, const int* idx, long long* nonfinite, const float* ga,
+                        const float* gb, int g_ld, float scale, __nv_bfloat16* ghi, __nv_bfloat16* glo,
+                        int num_sms, cudaStream_t s);
+cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
+                             const int* n_eff, const int* idx, float* dh, int num_sms, cudaStream_t s);
+cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
+}  // namespace kd
+
+using namespace kd;
+
+// ------------------------------------------------------------------------------------ errors
+static thread_local std::string g_err = "ok";
+static thread_local int g_launches = 0;
+
+static kd_status fail(kd_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define KD_CUDA(expr)                                                                              \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return fail(KD_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+#define KD_LAUNCH(expr)  \
+  do {                   \
+    KD_CUDA(expr);       \
+    ++g_launches;        \
+  } while (0)
+
+// ------------------------------------------------------------------------------------ TMA maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static bool tma_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// bf16 2-D map: `inner` contiguous elements per row, `outer` rows of `row_bytes`; 128B-swizzled boxes.
+static kd_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                          uint32_t box_inner, uint32_t box_outer) {
+  if (!tma_encoder()) return fail(KD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (outer == 0) outer = 1;  // never addressed when the extent is empty (kernels skip all tiles)
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(KD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu", (int)r,
+                (unsigned long long)inner, (unsigned long long)outer);
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------------------------ plan
+static int device_sms() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Plan {
+  int N, d_t, d_s, V_r, kind;
+  int Nc, n_chunks, m_tiles_c, v_tiles, n_split, g_ld, k_split, num_sms;
+  bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
+  size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
+      off_glo, off_ga, off_gb, off_dhp, total;
+};
+
+// Static round-robin of units over a persistent grid: makespan in tiles (+ per-unit refill cost).
+static double pass_makespan(int m_tiles, int s, int v_tiles, int sms) {
+  const int units = m_tiles * s;
+  const int grid = units < sms ? units : sms;
+  double worst = 0;
+  for (int c = 0; c < grid; ++c) {
+    double t = 0;
+    for (int u = c; u < units; u += grid) {
+      const int sp = u / m_tiles;
+      t += (double)((long long)(sp + 1) * v_tiles / s - (long long)sp * v_tiles / s) + 0.1;
+    }
+    if (t > worst) worst = t;
+  }
+  return worst;
+}
+
+static int choose_n_split(int m_tiles, int v_tiles, int sms) {
+  int best = 1;
+  double best_cost = 1e300;
+  const int smax = v_tiles < 160 ? v_tiles : 160;
+  for (int s = 1; s <= smax; ++s) {
+    const double c = pass_makespan(m_tiles, s, v_tiles, sms);
+    if (c < best_cost * 0.999) { best_cost = c; best = s; }
+  }
+  return best;
+}
+
+static int choose_k_split(int m_tiles, int n_tiles, int kbs, int sms) {
+  int best = 1;
+  double best_cost = 1e300;
+  for (int k = 1; k <= 16 && k <= kbs; ++k) {
+    const int units = m_tiles * n_tiles * k;
+    const int grid = units < sms ? units : sms;
+    const double per = (double)((kbs + k - 1) / k) + 2.0;  // k-blocks per unit + epilogue/refill
+    const double waves = (double)((units + grid - 1) / grid);
+    const double c = waves * per + 0.02 * kbs * (k - 1);   // + reduction traffic
+    if (c < best_cost * 0.999) { best_cost = c; best = k; }
+  }
+  return best;
+}
+
+static kd_status validate(const kd_problem* p, bool require_full_vocab) {
+  if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
+  for (int i = 0; i < 5; ++i)
+    if (p->reserved[i] != 0) return fail(KD_ERR_INVALID_ARG, "reserved fields must be zero");
+  if (!(p->temperature > 0.f) || !std::isfinite(p->temperature))
+    return fail(KD_ERR_INVALID_ARG, "temperature must be finite and > 0 (got %g)", (double)p->temperature);
+  if (p->kind < KD_FKL || p->kind > KD_TVD) return fail(KD_ERR_INVALID_ARG, "unknown divergence kind %d", p->kind);
+  if (p->kind == KD_JSD && !(p->jsd_beta > 0.f && p->jsd_beta < 1.f))
+    return fail(KD_ERR_INVALID_ARG, "jsd_beta must lie in (0,1) (got %g)", (double)p->jsd_beta);
+  if (!std::isfinite(p->loss_scale)) return fail(KD_ERR_INVALID_ARG, "loss_scale must be finite");
+  if (p->n_tokens < 0 || p->n_tokens > (1ll << 30)) return fail(KD_ERR_SHAPE, "n_tokens out of range");
+  if (p->d_t < 64 || p->d_s < 64 || p->d_t % 64 || p->d_s % 64 || p->d_t > 65536 || p->d_s > 65536)
+    return fail(KD_ERR_SHAPE, "d_t and d_s must be positive multiples of 64 (got %d, %d)", p->d_t, p->d_s);
+  if (p->vocab < 1 || p->v_begin < 0 || p->v_end > p->vocab || p->v_end <= p->v_begin)
+    return fail(KD_ERR_SHAPE, "bad vocabulary range [%lld, %lld) of %lld", (long long)p->v_begin,
+                (long long)p->v_end, (long long)p->vocab);
+  if (p->v_end - p->v_begin > (1ll << 26)) return fail(KD_ERR_SHAPE, "vocabulary shard too large");
+  if (require_full_vocab && (p->v_begin != 0 || p->v_end != p->vocab))
+    return fail(KD_ERR_SHAPE, "kd_fused_fwd_bwd needs the full vocabulary; use kd_vocab_* for shards");
+  if (p->chunk_tokens < 0) return fail(KD_ERR_SHAPE, "chunk_tokens must be >= 0");
+  return KD_OK;
+}
+
+static Plan make_plan(const kd_problem* p) {
+  Plan P{};
+  P.N = (int)p->n_tokens;
+  P.d_t = p->d_t;
+  P.d_s = p->d_s;
+  P.V_r = (int)(p->v_end - p->v_begin);
+  P.kind = p->kind;
+  P.fix = (p->kind == KD_JSD || p->kind == KD_TVD);
+  P.num_sms = device_sms();
+  int nc = p->chunk_tokens > 0 ? p->chunk_tokens : 4096;
+  const int n_pad = ((P.N + kBM - 1) / kBM) * kBM;
+  if (nc > n_pad) nc = n_pad;
+  nc = ((nc + kBM - 1) / kBM) * kBM;
+  if (nc < kBM) nc = kBM;
+  P.Nc = nc;
+  P.n_chunks = (P.N + nc - 1) / nc;
+  P.m_tiles_c = nc / kBM;
+  P.v_tiles = (P.V_r + kBN - 1) / kBN;
+  P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, P.num_sms);
+  P.g_ld = ((P.V_r + 63) / 64) * 64;
+  P.k_split = choose_k_split(P.m_tiles_c, (P.d_s + kGemmBN - 1) / kGemmBN, (P.V_r + kBK - 1) / kBK, P.num_sms);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+  P.off_neff = take(8);
+  P.off_nonfinite = take(8);
+  P.off_idx = take((size_t)P.N * 4);
+  P.off_ht = take((size_t)P.N * P.d_t * 2);
+  P.off_hs = take((size_t)P.N * P.d_s * 2);
+  P.off_part = take((size_t)5 * P.n_split * P.Nc * 4);
+  P.off_fstats = take((size_t)3 * P.Nc * 4);
+  P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * P.Nc * 4 : 0);
+  P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
+  P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
+  P.off_glo = take((size_t)P.Nc * P.g_ld * 2);
+  P.off_ga = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
+  P.off_gb = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
+  P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
+  P.total = o;
+  return P;
+}
+
+static bool aligned16(const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; }
+
+template <typename T>
+static T* ws_at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+// ------------------------------------------------------------------------------------ the call sequence
+namespace {
+struct Ctx {
+  const kd_problem* p;
+  Plan P;
+  cudaStream_t s;
+  void* ws;
+  const __nv_bfloat16 *ht, *hs, *Wt, *Ws;  // possibly packed H
+  const int* idx;                          // NULL = identity (no mask)
+  int* n_eff;
+  long long* nonfinite;
+  CUtensorMap maps[4];
+};
+}  // namespace
+
+static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                          const uint8_t* mask, int64_t* n_nonfinite) {
+  const Plan& P = c.P;
+  c.n_eff = ws_at<int>(c.ws, P.off_neff);
+  c.nonfinite = n_nonfinite ? reinterpret_cast<long long*>(n_nonfinite) : ws_at<long long>(c.ws, P.off_nonfinite);
+  KD_CUDA(cudaMemsetAsync(c.nonfinite, 0, sizeof(long long), c.s));
+  c.Wt = static_cast<const __nv_bfloat16*>(W_t);
+  c.Ws = static_cast<const __nv_bfloat16*>(W_s);
+  if (mask) {
+    int* idx = ws_at<int>(c.ws, P.off_idx);
+    KD_LAUNCH(launch_compact(mask, P.N, idx, c.n_eff, c.s));
+    auto* pt = ws_at<__nv_bfloat16>(c.ws, P.off_ht);
+    auto* ps = ws_at<__nv_bfloat16>(c.ws, P.off_hs);
+    KD_LAUNCH(launch_gather(static_cast<const __nv_bfloat16*>(h_t), P.d_t, pt, P.d_t, P.N, idx, c.n_eff, c.s));
+    KD_LAUNCH(launch_gather(static_cast<const __nv_bfloat16*>(h_s), P.d_s, ps, P.d_s, P.N, idx, c.n_eff, c.s));
+    c.ht = pt;
+    c.hs = ps;
+    c.idx = idx;
+  } else {
+    KD_LAUNCH(launch_compact(nullptr, P.N, nullptr, c.n_eff, c.s));
+    c.ht = static_cast<const __nv_bfloat16*>(h_t);
+    c.hs = static_cast<const __nv_bfloat16*>(h_s);
+    c.idx = nullptr;
+  }
+  kd_status st;
+  if ((st = make_map(&c.maps[0], c.ht, P.d_t, P.N, (uint64_t)P.d_t * 2, kBK, kBM)) != KD_OK) return st;
+  if ((st = make_map(&c.maps[1], c.Wt, P.d_t, P.V_r, (uint64_t)P.d_t * 2, kBK, kBN)) != KD_OK) return st;
+  if ((st = make_map(&c.maps[2], c.hs, P.d_s, P.N, (uint64_t)P.d_s * 2, kBK, kBM)) != KD_OK) return st;
+  if ((st = make_map(&c.maps[3], c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, kBK, kBN)) != KD_OK) return st;
+  return KD_OK;
+}
+
+static PassParams pass_params(const Ctx& c, int row0) {
+  const Plan& P = c.P;
+  const kd_problem* p = c.p;
+  PassParams pp{};
+  pp.n_eff = c.n_eff;
+  pp.row0 = row0;
+  pp.n_rows = P.Nc;
+  pp.kb_t = P.d_t / kBK;
+  pp.kb_s = P.d_s / kBK;
+  pp.v_tiles = P.v_tiles;
+  pp.V_r = P.V_r;
+  pp.n_split = P.n_split;
+  pp.alpha = (float)(1.4426950408889634 / (double)p->temperature);
+  pp.part = ws_at<float>(c.ws, P.off_part);
+  pp.part_plane = (long long)P.n_split * P.Nc;
+  pp.fstats = ws_at<float>(c.ws, P.off_fstats);
+  const double cscale = (double)p->loss_scale / (double)p->temperature;
+  pp.gscale = (float)(p->kind == KD_RKL ? cscale * 0.6931471805599453 : cscale);
+  pp.beta = p->jsd_beta;
+  pp.g_hi = ws_at<__nv_bfloat16>(c.ws, P.off_ghi);
+  pp.g_lo = ws_at<__nv_bfloat16>(c.ws, P.off_glo);
+  pp.g_a = P.fix ? ws_at<float>(c.ws, P.off_ga) : nullptr;
+  pp.g_b = P.fix ? ws_at<float>(c.ws, P.off_gb) : nullptr;
+  pp.g_ld = P.g_ld;
+  pp.kpart = P.fix ? ws_at<float>(c.ws, P.off_kpart) : nullptr;
+  return pp;
+}
+
+static int pass_grid(const Plan& P) {
+  const int units = P.m_tiles_c * P.n_split;
+  return units < P.num_sms ? units : P.num_sms;
+}
+
+// pass 2 (+ JSD/TVD fix-up) + dh GEMM (+ split-K reduce) + dW GEMM for one chunk whose final per-token
+// statistics are already in fstats.
+static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW) {
+  const Plan& P = c.P;
+  const kd_problem* p = c.p;
+  PassParams pp = pass_params(c, row0);
+  const int grid = pass_grid(P);
+  KD_LAUNCH(launch_pass(2, P.kind, c.maps, pp, grid, c.s));
+  if (P.fix) {
+    const double cscale = (double)p->loss_scale / (double)p->temperature;
+    const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
+                                                 : 0.5 * cscale);
+    KD_LAUNCH(launch_kfix(pp.kpart, P.n_split, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
+                          ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
+                          pp.g_hi, pp.g_lo, P.num_sms, c.s));
+  }
+  // dh_s rows of this chunk: [G_hi | G_lo] · W_s  (K = V_r), split-K partial slabs, then reduce + scatter
+  CUtensorMap mg_hi, mg_lo, mw;
+  kd_status st;
+  if ((st = make_map(&mg_hi, pp.g_hi, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, kBK, kBM)) != KD_OK) return st;
+  if ((st = make_map(&mg_lo, pp.g_lo, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, kBK, kBM)) != KD_OK) return st;
+  if ((st = make_map(&mw, c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK) return st;
+  GemmParams gp{};
+  gp.M = P.Nc;
+  gp.N = P.d_s;
+  gp.K = P.V_r;
+  gp.dyn_dim = DYN_M;
+  gp.dyn = c.n_eff;
+  gp.dyn_base = row0;
+  gp.k_split = P.k_split;
+  gp.out = ws_at<float>(c.ws, P.off_dhp);
+  gp.out_ld = P.d_s;
+  gp.out_split_stride = (long long)P.Nc * P.d_s;
+  {
+    const int units = P.m_tiles_c * ((P.d_s + kGemmBN - 1) / kGemmBN) * P.k_split;
+    KD_LAUNCH(launch_gemm(false, true, 2, EPI_STORE, &mg_hi, &mg_lo, &mw, gp, units < P.num_sms ? units : P.num_sms,
+                          c.s));
+  }
+  KD_LAUNCH(launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
+                             P.num_sms, c.s));
+  if (dW) {
+    CUtensorMap ma_hi, ma_lo, mh;
+    if ((st = make_map(&ma_hi, pp.g_hi, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, 64, kBK)) != KD_OK) return st;
+    if ((st = make_map(&ma_lo, pp.g_lo, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, 64, kBK)) != KD_OK) return st;
+    const int rows_left = P.N - row0;
+    if ((st = make_map(&mh, c.hs + (size_t)row0 * P.d_s, P.d_s, rows_left, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK)
+      return st;
+    GemmParams wp{};
+    wp.M = P.V_r;
+    wp.N = P.d_s;
+    wp.K = P.Nc;
+    wp.dyn_dim = DYN_K;
+    wp.dyn = c.n_eff;
+    wp.dyn_base = row0;
+    wp.k_split = 1;
+    wp.out = dW;
+    wp.out_ld = P.d_s;
+    wp.out_split_stride = 0;
+    const int units = ((P.V_r + kBM - 1) / kBM) * ((P.d_s + kGemmBN - 1) / kGemmBN);
+    KD_LAUNCH(launch_gemm(true, true, 2, EPI_ACCUM, &ma_hi, &ma_lo, &mh, wp, units < P.num_sms ? units : P.num_sms,
+                          c.s));
+  }
+  return KD_OK;
+}
+
+static kd_status check_common(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                              const void* W_s, float* loss, float* dh, float* dW, void* ws, size_t ws_bytes,
+                              const Plan& P) {
+  if (P.N > 0 && (!h_t || !h_s || !loss || !dh)) return fail(KD_ERR_INVALID_ARG, "NULL input/output pointer");
+  if (!W_t || !W_s) return fail(KD_ERR_INVALID_ARG, "NULL LM-head pointer");
+  if (p->want_dW && !dW) return fail(KD_ERR_INVALID_ARG, "want_dW set but dW_s is NULL");
+  const void* ptrs[] = {h_t, W_t, h_s, W_s, loss, dh, dW};
+  for (const void* x : ptrs)
+    if (x && !aligned16(x)) return fail(KD_ERR_ALIGNMENT, "pointers must be 16-byte aligned");
+  if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace must be non-NULL and 256-byte aligned");
+  if (ws_bytes < P.total)
+    return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace %zu bytes < required %zu", ws_bytes, P.total);
+  return KD_OK;
+}
+
+extern "C" {
+
+size_t kd_workspace_size(const kd_problem* p) {
+  if (validate(p, false) != KD_OK) return 0;
+  return make_plan(p).total;
+}
+
+kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                           const void* W_s, const uint8_t* mask, float* loss, float* dh_s, float* dW_s,
+                           int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  kd_status st = validate(p, true);
+  if (st != KD_OK) return st;
+  Ctx c{};
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  float* dW = p->want_dW ? dW_s : nullptr;
+  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s, dW, workspace, workspace_bytes, c.P)) != KD_OK)
+    return st;
+  const Plan& P = c.P;
+  if (dW && !p->accumulate_dW) KD_CUDA(cudaMemsetAsync(dW, 0, (size_t)P.V_r * P.d_s * 4, c.s));
+  if (P.N == 0) {
+    if (n_nonfinite) KD_CUDA(cudaMemsetAsync(n_nonfinite, 0, 8, c.s));
+    return KD_OK;
+  }
+  if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
+  if (mask) KD_LAUNCH(launch_zero_masked(mask, P.N, loss, dh_s, P.d_s, c.s));
+  for (int ch = 0; ch < P.n_chunks; ++ch) {
+    const int row0 = ch * P.Nc;
+    PassParams pp = pass_params(c, row0);
+    KD_LAUNCH(launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 0,
+                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, c.s));
+    if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
+  }
+  return KD_OK;
+}
+
+kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                         const uint8_t* mask, float* rec, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  kd_status st = validate(p, false);
+  if (st != KD_OK) return st;
+  if (p->kind != KD_FKL && p->kind != KD_RKL)
+    return fail(KD_ERR_UNSUPPORTED, "vocab-sharded mode supports FKL/RKL (JSD/TVD need a K exchange: NEXT)");
+  Ctx c{};
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  float dummy_loss_ptr_guard = 0.f;
+  (void)dummy_loss_ptr_guard;
+  if (c.P.N > 0 && !rec) return fail(KD_ERR_INVALID_ARG, "rec is NULL");
+  if (rec && !aligned16(rec)) return fail(KD_ERR_ALIGNMENT, "rec must be 16-byte aligned");
+  if ((st = check_common(p, h_t, W_t, h_s, W_s, rec, rec, nullptr, workspace, workspace_bytes, c.P)) != KD_OK)
+    return st;
+  const Plan& P = c.P;
+  if (P.N == 0) return KD_OK;
+  if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
+  if (mask) KD_LAUNCH(launch_zero_records(mask, P.N, rec, (long long)P.N, c.s));
+  for (int ch = 0; ch < P.n_chunks; ++ch) {
+    const int row0 = ch * P.Nc;
+    PassParams pp = pass_params(c, row0);
+    KD_LAUNCH(launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
+                           nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, c.s));
+  }
+  return KD_OK;
+}
+
+kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                            const uint8_t* mask, const float* recs, int32_t n_ranks, float* loss,
+                            float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  kd_status st = validate(p, false);
+  if (st != KD_OK) return st;
+  if (p->kind != KD_FKL && p->kind != KD_RKL)
+    return fail(KD_ERR_UNSUPPORTED, "vocab-sharded mode supports FKL/RKL (JSD/TVD need a K exchange: NEXT)");
+  if (n_ranks < 1) return fail(KD_ERR_INVALID_ARG, "n_ranks must be >= 1");
+  Ctx c{};
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  float* dW = p->want_dW ? dW_s : nullptr;
+  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s_partial, dW, workspace, workspace_bytes, c.P)) != KD_OK)
+    return st;
+  if (c.P.N > 0 && !recs) return fail(KD_ERR_INVALID_ARG, "recs is NULL");
+  const Plan& P = c.P;
+  if (dW && !p->accumulate_dW) KD_CUDA(cudaMemsetAsync(dW, 0, (size_t)P.V_r * P.d_s * 4, c.s));
+  if (P.N == 0) {
+    if (n_nonfinite) KD_CUDA(cudaMemsetAsync(n_nonfinite, 0, 8, c.s));
+    return KD_OK;
+  }
+  if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
+  if (mask) KD_LAUNCH(launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
+  for (int ch = 0; ch < P.n_chunks; ++ch) {
+    const int row0 = ch * P.Nc;
+    // rank records [n_ranks][5][N] indexed by ORIGINAL row, merged in rank order
+    KD_LAUNCH(launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
+                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite, c.s));
+    if ((st = backward_chunk(c, row0, loss, dh_s_partial, dW)) != KD_OK) return st;
+  }
+  return KD_OK;
+}
+
+kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
+                           int32_t a_mn_major, int32_t b_mn_major, void* stream) {
+  g_launches = 0;
+  if (!A || !B || !D) return fail(KD_ERR_INVALID_ARG, "NULL pointer");
+  if (M < 1 || N < 1 || K < 1) return fail(KD_ERR_SHAPE, "M, N, K must be >= 1");
+  if (N % 32) return fail(KD_ERR_SHAPE, "N must be a multiple of 32");
+  if ((!a_mn_major && K % 8) || (a_mn_major && M % 8) || (!b_mn_major && K % 8) || (b_mn_major && N % 8))
+    return fail(KD_ERR_SHAPE, "contiguous extents must be multiples of 8 (16-byte rows)");
+  if (!aligned16(A) || !aligned16(B) || !aligned16(D)) return fail(KD_ERR_ALIGNMENT, "pointers must be 16B aligned");
+  CUtensorMap ma, mb;
+  kd_status st;
+  if (a_mn_major) st = make_map(&ma, A, M, K, (uint64_t)M * 2, 64, kBK);
+  else st = make_map(&ma, A, K, M, (uint64_t)K * 2, kBK, kBM);
+  if (st != KD_OK) return st;
+  if (b_mn_major) st = make_map(&mb, B, N, K, (uint64_t)N * 2, 64, kBK);
+  else st = make_map(&mb, B, K, N, (uint64_t)K * 2, kBK, kGemmBN);
+  if (st != KD_OK) return st;
+  GemmParams gp{};
+  gp.M = M;
+  gp.N = N;
+  gp.K = K;
+  gp.dyn_dim = DYN_NONE;
+  gp.k_split = 1;
+  gp.out = D;
+  gp.out_ld = N;
+  const int sms = device_sms();
+  const int units = ((M + kBM - 1) / kBM) * ((N + kGemmBN - 1) / kGemmBN);
+  KD_LAUNCH(launch_gemm(a_mn_major != 0, b_mn_major != 0, 1, EPI_STORE, &ma, nullptr, &mb, gp,
+                        units < sms ? units : sms, static_cast<cudaStream_t>(stream)));
+  return KD_OK;
+}
+
+int32_t kd_last_launch_count(void) { return g_launches; }
+const char* kd_last_error(void) { return g_err.c_str(); }
+int32_t kd_abi_version(void) { return KDFUSED_ABI_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+// kd_params.cuh — parameter blocks shared by the kernels and the host plan (kd_api.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+
+namespace kd {
+
+enum Kind : int { KIND_FKL = 0, KIND_RKL = 1, KIND_JSD = 2, KIND_TVD = 3 };
+
+constexpr int kBM = 128;        // token rows per tile (UMMA M, one TMEM lane per token)
+constexpr int kBN = 128;        // vocab columns per tile in the fused passes
+constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
+constexpr int kPassStages = 6;  // smem ring depth of the fused passes (6 x 32 KB)
+constexpr int kPassThreads = 256;
+
+// Fused dual-GEMM pass over one token chunk (rows [row0, row0 + n_rows) of the packed token list).
+// Work unit = (m_tile, vocab split); split s covers vocab tiles [s*v_tiles/n_split, (s+1)*v_tiles/n_split).
+struct PassParams {
+  const int* n_eff;   // device: number of valid packed rows (whole call)
+  int row0;           // first packed row of the chunk
+  int n_rows;         // chunk capacity (multiple of kBM)
+  int kb_t, kb_s;     // K blocks of the teacher / student GEMM (d/64)
+  int v_tiles;        // ceil(V_r / kBN)
+  int V_r;            // local vocabulary rows
+  int n_split;
+  float alpha;        // log2(e) / T
+  // pass 1 output: partial records, plane f at part + f*part_plane, index split*n_rows + r
+  float* part;
+  long long part_plane;
+  // pass 2 inputs/outputs
+  const float* fstats;  // [3][n_rows]: L2_t, L2_s (base-2 LSEs of z/T), ell2 (RKL loss in bits)
+  float gscale;         // c = loss_scale / T (FKL/RKL already folded with ln2 where needed)
+  float beta;           // JSD beta
+  __nv_bfloat16* g_hi;  // [n_rows][g_ld]
+  __nv_bfloat16* g_lo;
+  float* g_a;           // JSD/TVD: [n_rows][g_ld] fp32 planes
+  float* g_b;
+  int g_ld;             // multiple of 64, >= V_r
+  float* kpart;         // JSD/TVD: [2][n_split][n_rows] per-unit partial (K, J)
+};
+
+// Generic bf16 GEMM with fp32 TMEM accumulation: D[M, N] = sum_{a < NUM_A} A_a[M, K] * B[N, K]^T.
+enum GemmEpi : int { EPI_STORE = 0, EPI_ACCUM = 1 };
+enum DynDim : int { DYN_NONE = 0, DYN_M = 1, DYN_K = 2 };
+
+constexpr int kGemmBN = 256;
+constexpr int kGemmThreads = 256;
+
+struct GemmParams {
+  int M, N, K;         // static extents (the dynamic one is an upper bound)
+  int dyn_dim;         // DynDim: which extent is min(cap, *dyn - dyn_base)
+  const int* dyn;      // device counter (n_eff)
+  int dyn_base;
+  int k_split;         // split-K factor (EPI_STORE writes partial slabs)
+  float* out;          // fp32
+  long long out_ld;    // row stride (elements)
+  long long out_split_stride;  // elements between split-K slabs
+};
+
+}  // namespace kd

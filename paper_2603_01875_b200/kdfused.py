@@ -1,0 +1,217 @@
+"""Thin ctypes binding of ``include/kdfused.h`` (argument marshalling only).
+
+Every step of the KD hot path runs in the CUDA kernels of ``libkdfused.so``; this module only turns
+torch tensors into device pointers + sizes, allocates outputs / workspace with PyTorch (plumbing), and
+raises on a non-OK status.  There is no CPU fallback: if the library or a GPU is missing, calls fail
+loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkdfused.so")
+
+KINDS = {"fkl": 0, "rkl": 1, "jsd": 2, "tvd": 3}
+STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALIGNMENT", 4: "KD_ERR_UNSUPPORTED",
+          5: "KD_ERR_WORKSPACE_TOO_SMALL", 6: "KD_ERR_CUDA"}
+EXPORTED = ("kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward", "kd_gemm_bf16_f32",
+            "kd_last_launch_count", "kd_last_error", "kd_abi_version")
+
+
+class KDError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class KDProblem(ctypes.Structure):
+    _fields_ = [("n_tokens", ctypes.c_int64), ("d_t", ctypes.c_int32), ("d_s", ctypes.c_int32),
+                ("vocab", ctypes.c_int64), ("v_begin", ctypes.c_int64), ("v_end", ctypes.c_int64),
+                ("temperature", ctypes.c_float), ("kind", ctypes.c_int32), ("jsd_beta", ctypes.c_float),
+                ("loss_scale", ctypes.c_float), ("want_dW", ctypes.c_int32), ("accumulate_dW", ctypes.c_int32),
+                ("chunk_tokens", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libkdfused.so (built in-tree by ``paper_2603_01875_b200.build``); fail loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2603_01875_b200.build` "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, sz, i32, i64p = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p
+    P = ctypes.POINTER(KDProblem)
+    L.kd_workspace_size.argtypes = [P]
+    L.kd_workspace_size.restype = sz
+    L.kd_fused_fwd_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, i64p, vp, sz, vp]
+    L.kd_fused_fwd_bwd.restype = ctypes.c_int
+    L.kd_vocab_stats.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.kd_vocab_stats.restype = ctypes.c_int
+    L.kd_vocab_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
+    L.kd_vocab_backward.restype = ctypes.c_int
+    L.kd_gemm_bf16_f32.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
+    L.kd_gemm_bf16_f32.restype = ctypes.c_int
+    L.kd_last_launch_count.restype = ctypes.c_int32
+    L.kd_last_error.restype = ctypes.c_char_p
+    L.kd_abi_version.restype = ctypes.c_int32
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise KDError(status, lib().kd_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_problem(n_tokens, d_t, d_s, vocab, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False,
+                 accumulate_dW=False, v_begin=0, v_end=None, chunk_tokens=0) -> KDProblem:
+    p = KDProblem()
+    p.n_tokens, p.d_t, p.d_s, p.vocab = int(n_tokens), int(d_t), int(d_s), int(vocab)
+    p.v_begin = int(v_begin)
+    p.v_end = int(vocab if v_end is None else v_end)
+    p.temperature = float(T)
+    p.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
+    p.jsd_beta = float(beta)
+    p.loss_scale = float(loss_scale)
+    p.want_dW = int(bool(want_dW))
+    p.accumulate_dW = int(bool(accumulate_dW))
+    p.chunk_tokens = int(chunk_tokens)
+    return p
+
+
+def workspace_size(p: KDProblem) -> int:
+    n = lib().kd_workspace_size(ctypes.byref(p))
+    if n == 0:
+        raise KDError(1, lib().kd_last_error().decode())
+    return n
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = torch.device(device)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=key)
+        _ws_cache[key] = buf
+    return buf
+
+
+def last_launch_count() -> int:
+    return int(lib().kd_last_launch_count())
+
+
+def _as_bf16(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.bfloat16:
+        raise ValueError(f"{name} must be bfloat16")
+    return t.contiguous()
+
+
+@dataclass
+class KDResult:
+    loss: torch.Tensor          # [N] f32
+    dh_s: torch.Tensor          # [N, d_s] f32
+    dW_s: torch.Tensor | None   # [V_r, d_s] f32
+    n_nonfinite: torch.Tensor   # [1] i64 (device)
+
+
+def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False,
+                  accumulate_dW=False, dW_s=None, chunk_tokens=0, out=None, stream=None) -> KDResult:
+    """kd_fused_fwd_bwd: per-token loss, dL/dh_s and (optionally) dL/dW_s for device tensors."""
+    h_t, W_t, h_s, W_s = (_as_bf16(x, n) for x, n in ((h_t, "h_t"), (W_t, "W_t"), (h_s, "h_s"), (W_s, "W_s")))
+    N, d_t = h_t.shape
+    V, d_s = W_s.shape
+    dev = h_t.device
+    p = make_problem(N, d_t, d_s, V, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    if out is None:
+        loss = torch.empty(N, dtype=torch.float32, device=dev)
+        dh = torch.empty(N, d_s, dtype=torch.float32, device=dev)
+        nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        loss, dh, nnf = out.loss, out.dh_s, out.n_nonfinite
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if accumulate_dW else torch.empty)(V, d_s, dtype=torch.float32, device=dev)
+    ws = _workspace(workspace_size(p), dev)
+    _check(lib().kd_fused_fwd_bwd(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(h_s), _ptr(W_s), _ptr(mask),
+                                  _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws),
+                                  ws.numel(), _stream_handle(stream)))
+    return KDResult(loss, dh, dW_s if want_dW else None, nnf)
+
+
+def vocab_stats(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab, v_begin, T=1.0, kind="fkl",
+                chunk_tokens=0, stream=None) -> torch.Tensor:
+    """kd_vocab_stats: this vocab shard's per-token record [5, N] (to be all-gathered)."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(x, "input") for x in (h_t, W_t_shard, h_s, W_s_shard))
+    N, d_t = h_t.shape
+    V_r, d_s = W_s_shard.shape
+    p = make_problem(N, d_t, d_s, vocab, T=T, kind=kind, v_begin=v_begin, v_end=v_begin + V_r,
+                     chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
+    rec = torch.empty(5, N, dtype=torch.float32, device=h_t.device)
+    ws = _workspace(workspace_size(p), h_t.device)
+    _check(lib().kd_vocab_stats(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                _ptr(mask), _ptr(rec), _ptr(ws), ws.numel(), _stream_handle(stream)))
+    return rec
+
+
+def vocab_backward(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, vocab, v_begin, T=1.0, kind="fkl",
+                   loss_scale=1.0, want_dW=False, accumulate_dW=False, dW_s=None, chunk_tokens=0,
+                   stream=None) -> KDResult:
+    """kd_vocab_backward: merge the [P, 5, N] records; loss, PARTIAL dh_s (sum over ranks), local dW_s."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(x, "input") for x in (h_t, W_t_shard, h_s, W_s_shard))
+    N, d_t = h_t.shape
+    V_r, d_s = W_s_shard.shape
+    dev = h_t.device
+    p = make_problem(N, d_t, d_s, vocab, T=T, kind=kind, loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, v_begin=v_begin, v_end=v_begin + V_r, chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    recs = recs.to(device=dev, dtype=torch.float32).contiguous()
+    loss = torch.empty(N, dtype=torch.float32, device=dev)
+    dh = torch.empty(N, d_s, dtype=torch.float32, device=dev)
+    nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if accumulate_dW else torch.empty)(V_r, d_s, dtype=torch.float32, device=dev)
+    ws = _workspace(workspace_size(p), dev)
+    _check(lib().kd_vocab_backward(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                   _ptr(mask), _ptr(recs), int(recs.shape[0]), _ptr(loss), _ptr(dh),
+                                   _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),
+                                   _stream_handle(stream)))
+    return KDResult(loss, dh, dW_s if want_dW else None, nnf)
+
+
+def gemm_bf16_f32(A, B, *, M, N, K, a_mn_major=False, b_mn_major=False, stream=None) -> torch.Tensor:
+    """kd_gemm_bf16_f32: D[M, N] = A·Bᵀ (operands bf16, fp32 accumulate in TMEM)."""
+    A = _as_bf16(A, "A")
+    B = _as_bf16(B, "B")
+    D = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    _check(lib().kd_gemm_bf16_f32(_ptr(A), _ptr(B), _ptr(D), M, N, K, int(a_mn_major), int(b_mn_major),
+                                  _stream_handle(stream)))
+    return D
