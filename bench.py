@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py — KD tokens/s of the fused KD hot path (BASELINE.json metric) on N B200s.
+
+One step = one ``kd_fused_fwd_bwd`` call over one batch: recompute the teacher logits from H_t (V = 151936),
+the student logits, the divergence, the per-token loss and dL/dh_s (BASELINE.json configs[1] by default:
+Qwen3-8B d_t=4096 -> Qwen3-1.7B d_s=2048, 8 x 4096 tokens, FKL, T = 1).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c2|c3_rkl|c3_jsd|c4|c5] [--dW]
+    python bench.py --impl reference ...      # the fp64 CPU oracle on this box's host cores
+
+Multi-GPU (torchrun): token sharding with no data-path collective — every rank owns its own 32768 tokens
+and a full copy of both heads (weak scaling); the only collectives are the timing barrier / max.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import kd_inputs as KI  # noqa: E402
+
+METRIC = "KD tokens/s (fwd+bwd, V=151936)"
+UNIT = "tokens/s"
+L2_BYTES = 126 * 2 ** 20
+GUIDE_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kd", choices=["kd", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(KI.CONFIGS))
+    ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU (default: the config's)")
+    ap.add_argument("--dW", action="store_true", help="also compute dL/dW_s")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=128)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(GUIDE_FALLBACK)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int):
+    mask_desc = {"none": "all ones", "prompt_pad": "prompt L_p~U[64,512] + padding beyond L~U[2048,4096] masked",
+                 "ragged": "ragged L~U[256,8192], prompt L_p~U[32,min(512,L/2)] masked"}[cfg.mask]
+    heads_b = cfg.vocab * (cfg.d_t + cfg.d_s) * 2
+    return {
+        "workload": f"{cfg.name}: d_t={cfg.d_t} -> d_s={cfg.d_s}, V={cfg.vocab}, {n_tok} tokens/GPU, "
+                    f"{cfg.kind.upper()} T={cfg.temperature:g}" + (" +dW_s" if want_dW else ""),
+        "baseline_config": cfg.notes,
+        "tokens_per_gpu": n_tok, "d_t": cfg.d_t, "d_s": cfg.d_s, "vocab": cfg.vocab, "kind": cfg.kind,
+        "temperature": cfg.temperature, "jsd_beta": cfg.jsd_beta if cfg.kind == "jsd" else None,
+        "want_dW": want_dW, "mask": mask_desc,
+        "parallelism": f"token-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU",
+        "l2": f"no flush: resident inputs {heads_b / 1e9:.2f} GB heads + {n_tok * (cfg.d_t + cfg.d_s) * 2 / 1e9:.2f} GB "
+              f"hidden > {L2_BYTES / 2 ** 20:.0f} MiB L2",
+    }
+
+
+# ------------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(gpu_index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------------- oracle timing
+def oracle_tokens_per_s(cfg: KI.KDConfig, n_sample: int, want_dW: bool, seed: int = 0):
+    """Time the fp64 CPU oracle (as it stands) on a bounded token sample at the full config shapes."""
+    from oracle.kd_oracle import kd_fused_fwd_bwd
+    W_t, W_s = KI.make_heads(cfg.vocab, cfg.d_t, cfg.d_s, seed=1000 + seed)
+    H_t, H_s = KI.make_hidden(n_sample, W_t, W_s, seed=1001 + seed, head_seed=1000 + seed)
+    Wt, Ws = KI.bf16_to_f64(W_t), KI.bf16_to_f64(W_s)
+    ht, hs = KI.bf16_to_f64(H_t), KI.bf16_to_f64(H_s)
+    del W_t, W_s
+    t0 = time.perf_counter()
+    kd_fused_fwd_bwd(ht, Wt, hs, Ws, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, want_dW=want_dW)
+    dt = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    return n_sample / dt, dt, cores
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, rank 0 only (other ranks exit 0 without work)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    cfg = KI.CONFIGS[args.config]
+    n_sample = max(1, args.cpu_sample_tokens // 2)
+    from oracle.kd_oracle import kd_fused_fwd_bwd
+    W_t, W_s = KI.make_heads(cfg.vocab, cfg.d_t, cfg.d_s, seed=1000)
+    Wt, Ws = KI.bf16_to_f64(W_t), KI.bf16_to_f64(W_s)
+    times = []
+    for step in range(args.warmup + args.steps):
+        H_t, H_s = KI.make_hidden(n_sample, W_t, W_s, seed=1001 + step, head_seed=1000)
+        ht, hs = KI.bf16_to_f64(H_t), KI.bf16_to_f64(H_s)
+        t0 = time.perf_counter()
+        kd_fused_fwd_bwd(ht, Wt, hs, Ws, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, want_dW=args.dW)
+        if step >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = n_sample * len(times) / total
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"{n_sample} tokens per step at full {cfg.name} shapes (V={cfg.vocab}, d_t={cfg.d_t}, d_s={cfg.d_s}), "
+              f"fp64 numpy, heads pre-converted to fp64 outside the timed call")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (kd_inputs recipe, seeded)",
+            "config": workload_desc(cfg, n_sample, args.dW, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_01875_b200 as kd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    kd.lib()
+    cfg = KI.CONFIGS[args.config]
+    want_dW = args.dW or cfg.want_dW
+    n_tok = args.tokens or cfg.n_tokens
+
+    # ---- inputs: heads replicated (seed 1000), each rank its own tokens (seed 1001 + rank)
+    W_t, W_s = KI.make_heads(cfg.vocab, cfg.d_t, cfg.d_s, seed=1000)
+    H_t, H_s = KI.make_hidden(n_tok, W_t, W_s, seed=1001 + rank, head_seed=1000)
+    mask_np = KI.make_mask(KI.KDConfig(**{**cfg.__dict__, "n_seq": max(1, n_tok // cfg.seq_len)}),
+                           seed=1002 + rank) if cfg.mask != "none" else None
+    if mask_np is not None:
+        mask_np = np.resize(mask_np, n_tok)
+
+    def up(b):
+        return torch.from_numpy(b.view(np.int16)).to(dev).view(torch.bfloat16)
+
+    Wt, Ws, Ht, Hs = up(W_t), up(W_s), up(H_t), up(H_s)
+    mask = torch.from_numpy(mask_np).to(dev) if mask_np is not None else None
+    n_eff = int(mask_np.sum()) if mask_np is not None else n_tok
+    del W_t, W_s
+    kw = dict(T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0, want_dW=want_dW,
+              accumulate_dW=False)
+    out = kd.KDResult(torch.empty(n_tok, dtype=torch.float32, device=dev),
+                      torch.empty(n_tok, cfg.d_s, dtype=torch.float32, device=dev), None,
+                      torch.zeros(1, dtype=torch.int64, device=dev))
+    dW = torch.empty(cfg.vocab, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return kd.fused_fwd_bwd(Ht, Wt, Hs, Ws, mask, dW_s=dW, out=out, **kw)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = kd.last_launch_count()
+
+    # ---- timed region (device events on the launching stream; live per-kernel events inside the library)
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    kd.profile_read()
+    kd.profile_enable(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    kd.profile_enable(False)
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    prof = kd.profile_read()
+    ms_max = max_over_ranks(ms)
+    value = world * n_eff * args.steps / (ms_max / 1000.0)
+    nonfinite = int(out.n_nonfinite.item())
+
+    # ---- roofline of the dominant kernel (live CUDA events)
+    pk = peaks()
+    flops_pass = 2.0 * n_eff * cfg.vocab * (cfg.d_t + cfg.d_s)  # both LM-head GEMMs, one vocab sweep
+    flops_g = 2.0 * n_eff * cfg.vocab * cfg.d_s                   # G · W_s  (or Gᵀ · H_s)
+    algo = {"pass1": flops_pass, "pass2": flops_pass, "gemm_dh": flops_g, "gemm_dW": flops_g}
+    exec_mult = {"pass1": 1.0, "pass2": 1.0, "gemm_dh": 2.0, "gemm_dW": 2.0}   # split-bf16 G: 2 MMAs
+    kernels = {}
+    total_ms = sum(t for _, t in prof.values()) or 1.0
+    for name, (n, t) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        e = {"launches": n, "ms_per_step": t / args.steps, "share": t / total_ms}
+        if name in algo:
+            e["algorithmic_tflops"] = algo[name] * args.steps / (t / 1e3) / 1e12
+            e["tensor_pipe_tflops_executed"] = e["algorithmic_tflops"] * exec_mult[name]
+        kernels[name] = e
+    dom = max((k for k in kernels if k in algo), key=lambda k: kernels[k]["ms_per_step"])
+    peak_sust = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom, {}).get("dram_bytes_per_launch")
+    n_l, t_l = prof[dom]
+    achieved = algo[dom] * args.steps / n_l / (t_l / n_l / 1e3) / 1e12
+    roofline = {"bound": "tensor", "kernel": f"kd_pass_kernel ({dom})" if dom.startswith("pass") else dom,
+                "achieved": achieved, "peak": peak_sust, "unit": "TFLOP/s", "frac": achieved / peak_sust,
+                "traffic": traffic,
+                "peak_note": f"bf16 dense, {pk['source']}, sustained (kernel timed inside a long step); "
+                             f"burst {pk['bf16_tflops']}",
+                "algorithmic_per_launch": f"2*tokens*V*(d_t+d_s) flop = {algo[dom] * args.steps / n_l:.4g}"}
+    step_useful = 2.0 * n_eff * cfg.vocab * (cfg.d_t + 2 * cfg.d_s + (cfg.d_s if want_dW else 0))
+    useful_frac = step_useful * args.steps / (ms_max / 1e3) / 1e12 / peak_sust
+
+    # ---- e2e: same metric through the C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hHt = Ht.cpu().pin_memory()
+        hHs = Hs.cpu().pin_memory()
+        hmask = mask.cpu().pin_memory() if mask is not None else None
+        hloss = torch.empty(n_tok, dtype=torch.float32).pin_memory()
+        hdh = torch.empty(n_tok, cfg.d_s, dtype=torch.float32).pin_memory()
+        dHt, dHs = torch.empty_like(Ht), torch.empty_like(Hs)
+        dmask = torch.empty_like(mask) if mask is not None else None
+
+        def e2e_step():
+            dHt.copy_(hHt, non_blocking=True)
+            dHs.copy_(hHs, non_blocking=True)
+            if dmask is not None:
+                dmask.copy_(hmask, non_blocking=True)
+            r = kd.fused_fwd_bwd(dHt, Wt, dHs, Ws, dmask, dW_s=dW, out=out, **kw)
+            hloss.copy_(r.loss, non_blocking=True)
+            hdh.copy_(r.dh_s, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+        h2d = n_tok * (cfg.d_t + cfg.d_s) * 2 + (n_tok if mask is not None else 0)
+        d2h = n_tok * 4 + n_tok * cfg.d_s * 4
+        e2e = {"value": world * n_eff * args.steps / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "note": "heads resident in HBM (weights); per-step H_t/H_s in, loss/dh out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, cores = oracle_tokens_per_s(cfg, args.cpu_sample_tokens, want_dW)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{args.cpu_sample_tokens} tokens at full {cfg.name} shapes, fp64 numpy "
+                         f"({dt:.1f} s; BLAS threads = all {cores} affinity cores)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kd_inputs recipe, seeded)",
+                "config": workload_desc(cfg, n_tok, want_dW, world), "clocks": clocks, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps, "roofline": roofline, "cpu_baseline": cpu,
+                "useful_flop_frac": useful_frac, "kernels": kernels, "nonfinite_tokens": nonfinite,
+                "tokens_loss_bearing_per_gpu": n_eff}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

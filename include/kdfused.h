@@ -119,6 +119,15 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
 /* Number of kernel launches the last successful call on this thread enqueued (bench bookkeeping). */
 int32_t kd_last_launch_count(void);
 
+/* Live per-kernel timing (used by bench.py for the roofline figure).  While enabled, every kernel the
+ * library launches is bracketed by two CUDA events on the call's stream (negligible GPU cost).
+ * kd_profile_read synchronises those events, fills launches[i] / total_ms[i] for kernel id i
+ * (0 <= i < min(max_kernels, count)), clears the record and returns the number of kernel ids (or -1 if
+ * an event failed).  kd_profile_kernel_name(i) names id i ("pass1", "pass2", "gemm_dh", ...). */
+int32_t kd_profile_enable(int32_t on);
+int32_t kd_profile_read(int32_t* launches, double* total_ms, int32_t max_kernels);
+const char* kd_profile_kernel_name(int32_t id);
+
 /* Thread-local message describing the last non-OK status (never NULL). */
 const char* kd_last_error(void);
 

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/kdfused.h"
 #include "kd_params.cuh"
@@ -59,10 +60,39 @@ static kd_status fail(kd_status st, const char* fmt, ...) {
     cudaError_t e_ = (expr);                                                                       \
     if (e_ != cudaSuccess) return fail(KD_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
   } while (0)
-#define KD_LAUNCH(expr)  \
-  do {                   \
-    KD_CUDA(expr);       \
-    ++g_launches;        \
+// ------------------------------------------------------------------------------------ live profiling
+// When enabled, every launch is bracketed by two CUDA events on the launch stream; kd_profile_read()
+// resolves them into per-kernel totals (bench.py uses this for the live roofline figure).
+enum KernelId : int { K_COMPACT, K_GATHER, K_ZERO, K_PASS1, K_MERGE, K_PASS2, K_KFIX, K_GEMM_DH, K_REDUCE_DH,
+                      K_GEMM_DW, K_GEMM, K_NUM };
+static const char* kKernelNames[K_NUM] = {"compact", "gather", "zero_masked", "pass1", "merge", "pass2",
+                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm"};
+struct ProfRec { int id; cudaEvent_t a, b; };
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_ev_pool;
+static thread_local cudaStream_t g_cur_stream = nullptr;
+
+static cudaEvent_t prof_event() {
+  if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+#define KD_LAUNCH(id, expr)                                                  \
+  do {                                                                       \
+    cudaEvent_t ea_ = nullptr, eb_ = nullptr;                                \
+    if (g_prof_on) { ea_ = prof_event(); cudaEventRecord(ea_, g_cur_stream); } \
+    KD_CUDA(expr);                                                           \
+    ++g_launches;                                                            \
+    if (g_prof_on) {                                                         \
+      eb_ = prof_event();                                                    \
+      cudaEventRecord(eb_, g_cur_stream);                                    \
+      std::lock_guard<std::mutex> lk_(g_prof_mu);                            \
+      g_prof.push_back({(id), ea_, eb_});                       \
+    }                                                                        \
   } while (0)
 
 // ------------------------------------------------------------------------------------ TMA maps
@@ -252,16 +282,16 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
   c.Ws = static_cast<const __nv_bfloat16*>(W_s);
   if (mask) {
     int* idx = ws_at<int>(c.ws, P.off_idx);
-    KD_LAUNCH(launch_compact(mask, P.N, idx, c.n_eff, c.s));
+    KD_LAUNCH(K_COMPACT, launch_compact(mask, P.N, idx, c.n_eff, c.s));
     auto* pt = ws_at<__nv_bfloat16>(c.ws, P.off_ht);
     auto* ps = ws_at<__nv_bfloat16>(c.ws, P.off_hs);
-    KD_LAUNCH(launch_gather(static_cast<const __nv_bfloat16*>(h_t), P.d_t, pt, P.d_t, P.N, idx, c.n_eff, c.s));
-    KD_LAUNCH(launch_gather(static_cast<const __nv_bfloat16*>(h_s), P.d_s, ps, P.d_s, P.N, idx, c.n_eff, c.s));
+    KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_t), P.d_t, pt, P.d_t, P.N, idx, c.n_eff, c.s));
+    KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_s), P.d_s, ps, P.d_s, P.N, idx, c.n_eff, c.s));
     c.ht = pt;
     c.hs = ps;
     c.idx = idx;
   } else {
-    KD_LAUNCH(launch_compact(nullptr, P.N, nullptr, c.n_eff, c.s));
+    KD_LAUNCH(K_COMPACT, launch_compact(nullptr, P.N, nullptr, c.n_eff, c.s));
     c.ht = static_cast<const __nv_bfloat16*>(h_t);
     c.hs = static_cast<const __nv_bfloat16*>(h_s);
     c.idx = nullptr;
@@ -314,12 +344,12 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
   const int grid = pass_grid(P);
-  KD_LAUNCH(launch_pass(2, P.kind, c.maps, pp, grid, c.s));
+  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, c.maps, pp, grid, c.s));
   if (P.fix) {
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
                                                  : 0.5 * cscale);
-    KD_LAUNCH(launch_kfix(pp.kpart, P.n_split, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
+    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
                           pp.g_hi, pp.g_lo, P.num_sms, c.s));
   }
@@ -342,10 +372,10 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   gp.out_split_stride = (long long)P.Nc * P.d_s;
   {
     const int units = P.m_tiles_c * ((P.d_s + kGemmBN - 1) / kGemmBN) * P.k_split;
-    KD_LAUNCH(launch_gemm(false, true, 2, EPI_STORE, &mg_hi, &mg_lo, &mw, gp, units < P.num_sms ? units : P.num_sms,
+    KD_LAUNCH(K_GEMM_DH, launch_gemm(false, true, 2, EPI_STORE, &mg_hi, &mg_lo, &mw, gp, units < P.num_sms ? units : P.num_sms,
                           c.s));
   }
-  KD_LAUNCH(launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
+  KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                              P.num_sms, c.s));
   if (dW) {
     CUtensorMap ma_hi, ma_lo, mh;
@@ -366,7 +396,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
     wp.out_ld = P.d_s;
     wp.out_split_stride = 0;
     const int units = ((P.V_r + kBM - 1) / kBM) * ((P.d_s + kGemmBN - 1) / kGemmBN);
-    KD_LAUNCH(launch_gemm(true, true, 2, EPI_ACCUM, &ma_hi, &ma_lo, &mh, wp, units < P.num_sms ? units : P.num_sms,
+    KD_LAUNCH(K_GEMM_DW, launch_gemm(true, true, 2, EPI_ACCUM, &ma_hi, &ma_lo, &mh, wp, units < P.num_sms ? units : P.num_sms,
                           c.s));
   }
   return KD_OK;
@@ -399,6 +429,7 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
                            const void* W_s, const uint8_t* mask, float* loss, float* dh_s, float* dW_s,
                            int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = validate(p, true);
   if (st != KD_OK) return st;
   Ctx c{};
@@ -416,12 +447,12 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
     return KD_OK;
   }
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
-  if (mask) KD_LAUNCH(launch_zero_masked(mask, P.N, loss, dh_s, P.d_s, c.s));
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s, P.d_s, c.s));
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    KD_LAUNCH(launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
-    KD_LAUNCH(launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 0,
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
   }
@@ -431,6 +462,7 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
 kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
                          const uint8_t* mask, float* rec, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = validate(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL && p->kind != KD_RKL)
@@ -449,12 +481,12 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   const Plan& P = c.P;
   if (P.N == 0) return KD_OK;
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
-  if (mask) KD_LAUNCH(launch_zero_records(mask, P.N, rec, (long long)P.N, c.s));
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_records(mask, P.N, rec, (long long)P.N, c.s));
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    KD_LAUNCH(launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
-    KD_LAUNCH(launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
                            nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, c.s));
   }
   return KD_OK;
@@ -465,6 +497,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
                             float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
                             size_t workspace_bytes, void* stream) {
   g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = validate(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL && p->kind != KD_RKL)
@@ -486,11 +519,11 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
     return KD_OK;
   }
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
-  if (mask) KD_LAUNCH(launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     // rank records [n_ranks][5][N] indexed by ORIGINAL row, merged in rank order
-    KD_LAUNCH(launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
+    KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s_partial, dW)) != KD_OK) return st;
   }
@@ -500,6 +533,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
 kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
                            int32_t a_mn_major, int32_t b_mn_major, void* stream) {
   g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
   if (!A || !B || !D) return fail(KD_ERR_INVALID_ARG, "NULL pointer");
   if (M < 1 || N < 1 || K < 1) return fail(KD_ERR_SHAPE, "M, N, K must be >= 1");
   if (N % 32) return fail(KD_ERR_SHAPE, "N must be a multiple of 32");
@@ -524,12 +558,37 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
   gp.out_ld = N;
   const int sms = device_sms();
   const int units = ((M + kBM - 1) / kBM) * ((N + kGemmBN - 1) / kGemmBN);
-  KD_LAUNCH(launch_gemm(a_mn_major != 0, b_mn_major != 0, 1, EPI_STORE, &ma, nullptr, &mb, gp,
+  KD_LAUNCH(K_GEMM, launch_gemm(a_mn_major != 0, b_mn_major != 0, 1, EPI_STORE, &ma, nullptr, &mb, gp,
                         units < sms ? units : sms, static_cast<cudaStream_t>(stream)));
   return KD_OK;
 }
 
 int32_t kd_last_launch_count(void) { return g_launches; }
+
+int32_t kd_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int32_t prev = g_prof_on ? 1 : 0;
+  g_prof_on = on != 0;
+  return prev;
+}
+
+int32_t kd_profile_read(int32_t* launches, double* total_ms, int32_t max_kernels) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int n = max_kernels < K_NUM ? max_kernels : K_NUM;
+  for (int i = 0; i < n; ++i) { launches[i] = 0; total_ms[i] = 0.0; }
+  int32_t rc = K_NUM;
+  for (const ProfRec& r : g_prof) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) rc = -1;
+    if (r.id < n) { launches[r.id] += 1; total_ms[r.id] += ms; }
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  return rc;
+}
+
+const char* kd_profile_kernel_name(int32_t id) { return (id >= 0 && id < K_NUM) ? kKernelNames[id] : "?"; }
 const char* kd_last_error(void) { return g_err.c_str(); }
 int32_t kd_abi_version(void) { return KDFUSED_ABI_VERSION; }
 

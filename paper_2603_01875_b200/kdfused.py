@@ -20,7 +20,8 @@ KINDS = {"fkl": 0, "rkl": 1, "jsd": 2, "tvd": 3}
 STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALIGNMENT", 4: "KD_ERR_UNSUPPORTED",
           5: "KD_ERR_WORKSPACE_TOO_SMALL", 6: "KD_ERR_CUDA"}
 EXPORTED = ("kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward", "kd_gemm_bf16_f32",
-            "kd_last_launch_count", "kd_last_error", "kd_abi_version")
+            "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
+            "kd_last_error", "kd_abi_version")
 
 
 class KDError(RuntimeError):
@@ -62,6 +63,12 @@ def lib() -> ctypes.CDLL:
     L.kd_gemm_bf16_f32.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     L.kd_gemm_bf16_f32.restype = ctypes.c_int
     L.kd_last_launch_count.restype = ctypes.c_int32
+    L.kd_profile_enable.argtypes = [i32]
+    L.kd_profile_enable.restype = i32
+    L.kd_profile_read.argtypes = [vp, vp, i32]
+    L.kd_profile_read.restype = i32
+    L.kd_profile_kernel_name.argtypes = [i32]
+    L.kd_profile_kernel_name.restype = ctypes.c_char_p
     L.kd_last_error.restype = ctypes.c_char_p
     L.kd_abi_version.restype = ctypes.c_int32
     _lib = L
@@ -120,6 +127,24 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 
 def last_launch_count() -> int:
     return int(lib().kd_last_launch_count())
+
+
+def profile_enable(on: bool) -> bool:
+    """Bracket every library launch with CUDA events (live per-kernel timing)."""
+    return bool(lib().kd_profile_enable(int(bool(on))))
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total_ms)} since the last read (synchronises the recorded events)."""
+    L = lib()
+    n = 32
+    launches = (ctypes.c_int32 * n)()
+    total = (ctypes.c_double * n)()
+    k = L.kd_profile_read(launches, total, n)
+    if k < 0:
+        raise RuntimeError("kd_profile_read: an event failed")
+    return {L.kd_profile_kernel_name(i).decode(): (int(launches[i]), float(total[i]))
+            for i in range(min(k, n)) if launches[i] > 0}
 
 
 def _as_bf16(t: torch.Tensor, name: str) -> torch.Tensor:
