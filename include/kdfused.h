@@ -73,6 +73,10 @@ typedef struct {
   int32_t reserved[5];   /* must be zero */
 } kd_problem;
 
+/* Host-only validation of `p` (no CUDA call): the status kd_fused_fwd_bwd / kd_vocab_* would return for
+ * the problem itself (pointer checks aside). */
+kd_status kd_check_problem(const kd_problem* p);
+
 /* Bytes of device workspace kd_fused_fwd_bwd needs for `p` (a pure function of p and the current
  * device's SM count).  Returns 0 if p is invalid (see kd_last_error). */
 size_t kd_workspace_size(const kd_problem* p);

@@ -154,7 +154,8 @@ def make_heads(vocab: int, d_t: int, d_s: int, seed: int = 1000):
     W_t[:, 0] = bias
     W_s = _normal_rows(seed, 2, vocab, d_s)
     W_s *= np.float32(0.5 * ss)
-    W_s += W_t[:, :d_s] * np.float32(math.sqrt(d_t / d_s))
+    k = min(d_t, d_s)
+    W_s[:, :k] += W_t[:, :k] * np.float32(math.sqrt(d_t / d_s))
     W_s[:, 0] = bias
     return _bf16_bits_par(W_t), _bf16_bits_par(W_s)
 

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -36,6 +37,8 @@ cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, c
                         int num_sms, cudaStream_t s);
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
                              const int* n_eff, const int* idx, float* dh, int num_sms, cudaStream_t s);
+cudaError_t launch_corr_dh(const int* corr_v, const float* corr_r, int n_split, int n_rows, int row0,
+                           const int* n_eff, const int* idx, const __nv_bfloat16* Ws, int d_s, float* dh, cudaStream_t s);
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
 }  // namespace kd
 
@@ -64,9 +67,9 @@ static kd_status fail(kd_status st, const char* fmt, ...) {
 // When enabled, every launch is bracketed by two CUDA events on the launch stream; kd_profile_read()
 // resolves them into per-kernel totals (bench.py uses this for the live roofline figure).
 enum KernelId : int { K_COMPACT, K_GATHER, K_ZERO, K_PASS1, K_MERGE, K_PASS2, K_KFIX, K_GEMM_DH, K_REDUCE_DH,
-                      K_GEMM_DW, K_GEMM, K_NUM };
+                      K_GEMM_DW, K_GEMM, K_CORR_DH, K_NUM };
 static const char* kKernelNames[K_NUM] = {"compact", "gather", "zero_masked", "pass1", "merge", "pass2",
-                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm"};
+                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm", "corr_dh"};
 struct ProfRec { int id; cudaEvent_t a, b; };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -135,6 +138,17 @@ static int device_sms() {
   return sms > 0 ? sms : 148;
 }
 
+// Backward GEMMs flush their TMEM accumulator into the fp32 output every kKbPerAcc K blocks (see kd_gemm.cu).
+constexpr int kKbPerAccDefault = 64;
+static int kb_per_acc() {  // KD_KB_PER_ACC overrides the promotion period (precision experiments)
+  static int v = [] {
+    const char* e = getenv("KD_KB_PER_ACC");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : kKbPerAccDefault;
+  }();
+  return v;
+}
+
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Plan {
@@ -142,7 +156,7 @@ struct Plan {
   int Nc, n_chunks, m_tiles_c, v_tiles, n_split, g_ld, k_split, num_sms;
   bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
-      off_glo, off_ga, off_gb, off_dhp, total;
+      off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, total;
 };
 
 // Static round-robin of units over a persistent grid: makespan in tiles (+ per-unit refill cost).
@@ -238,7 +252,7 @@ static Plan make_plan(const kd_problem* p) {
   P.off_ht = take((size_t)P.N * P.d_t * 2);
   P.off_hs = take((size_t)P.N * P.d_s * 2);
   P.off_part = take((size_t)5 * P.n_split * P.Nc * 4);
-  P.off_fstats = take((size_t)3 * P.Nc * 4);
+  P.off_fstats = take((size_t)5 * P.Nc * 4);
   P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
   P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
@@ -246,6 +260,8 @@ static Plan make_plan(const kd_problem* p) {
   P.off_ga = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_gb = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
+  P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * kCorrSlots * P.Nc * 4);
+  P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * kCorrSlots * P.Nc * 4);
   P.total = o;
   return P;
 }
@@ -329,6 +345,8 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.g_b = P.fix ? ws_at<float>(c.ws, P.off_gb) : nullptr;
   pp.g_ld = P.g_ld;
   pp.kpart = P.fix ? ws_at<float>(c.ws, P.off_kpart) : nullptr;
+  pp.corr_v = P.fix ? nullptr : ws_at<int>(c.ws, P.off_corr_v);
+  pp.corr_r = P.fix ? nullptr : ws_at<float>(c.ws, P.off_corr_r);
   return pp;
 }
 
@@ -367,6 +385,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   gp.dyn = c.n_eff;
   gp.dyn_base = row0;
   gp.k_split = P.k_split;
+  gp.kb_per_acc = kb_per_acc();
   gp.out = ws_at<float>(c.ws, P.off_dhp);
   gp.out_ld = P.d_s;
   gp.out_split_stride = (long long)P.Nc * P.d_s;
@@ -377,6 +396,9 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   }
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                              P.num_sms, c.s));
+  if (!P.fix)
+    KD_LAUNCH(K_CORR_DH, launch_corr_dh(pp.corr_v, pp.corr_r, P.n_split, P.Nc, row0, c.n_eff, c.idx, c.Ws, P.d_s, dh,
+                                        c.s));
   if (dW) {
     CUtensorMap ma_hi, ma_lo, mh;
     if ((st = make_map(&ma_hi, pp.g_hi, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, 64, kBK)) != KD_OK) return st;
@@ -392,6 +414,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
     wp.dyn = c.n_eff;
     wp.dyn_base = row0;
     wp.k_split = 1;
+    wp.kb_per_acc = kb_per_acc();
     wp.out = dW;
     wp.out_ld = P.d_s;
     wp.out_split_stride = 0;
@@ -419,6 +442,8 @@ static kd_status check_common(const kd_problem* p, const void* h_t, const void* 
 }
 
 extern "C" {
+
+kd_status kd_check_problem(const kd_problem* p) { return validate(p, false); }
 
 size_t kd_workspace_size(const kd_problem* p) {
   if (validate(p, false) != KD_OK) return 0;
@@ -472,8 +497,6 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
-  float dummy_loss_ptr_guard = 0.f;
-  (void)dummy_loss_ptr_guard;
   if (c.P.N > 0 && !rec) return fail(KD_ERR_INVALID_ARG, "rec is NULL");
   if (rec && !aligned16(rec)) return fail(KD_ERR_ALIGNMENT, "rec must be 16-byte aligned");
   if ((st = check_common(p, h_t, W_t, h_s, W_s, rec, rec, nullptr, workspace, workspace_bytes, c.P)) != KD_OK)
@@ -554,6 +577,7 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
   gp.K = K;
   gp.dyn_dim = DYN_NONE;
   gp.k_split = 1;
+  gp.kb_per_acc = 1 << 30;  // plain GEMM: one accumulator per output tile
   gp.out = D;
   gp.out_ld = N;
   const int sms = device_sms();

@@ -82,21 +82,26 @@ __global__ void __launch_bounds__(256) k_zero_masked(const uint8_t* __restrict__
 }
 
 // ------------------------------------------------------------------ A2: merge of split records
+// The merge runs in fp64 (a few dozen records per token, negligible cost): one split holds S ≈ 1 and the
+// others add small amounts, which fp32 would round away at the 1e-7 level p_top ≈ 1 is sensitive to.
 struct Rec {
-  float Mp, Mq, Sp, Sq, U;
+  double Mp, Mq, Sp, Sq, U;
 };
 __device__ __forceinline__ void rec_merge(Rec& A, const Rec& B) {
-  if (B.Sp == 0.f) return;  // empty record = identity
-  if (A.Sp == 0.f) { A = B; return; }
-  const float Mp = fmaxf(A.Mp, B.Mp), Mq = fmaxf(A.Mq, B.Mq);
-  const float dpa = Mp - A.Mp, dqa = Mq - A.Mq, dpb = Mp - B.Mp, dqb = Mq - B.Mq;
-  const float fpa = exp2f(-dpa), fpb = exp2f(-dpb);
+  if (B.Sp == 0.0) return;  // empty record = identity
+  if (A.Sp == 0.0) { A = B; return; }
+  const double Mp = fmax(A.Mp, B.Mp), Mq = fmax(A.Mq, B.Mq);
+  const double dpa = Mp - A.Mp, dqa = Mq - A.Mq, dpb = Mp - B.Mp, dqb = Mq - B.Mq;
+  const double fpa = exp2(-dpa), fpb = exp2(-dpb);
   Rec R;
   R.Mp = Mp;
   R.Mq = Mq;
-  R.Sp = fpa * A.Sp + fpb * B.Sp;
-  R.Sq = exp2f(-dqa) * A.Sq + exp2f(-dqb) * B.Sq;
-  R.U = fpa * (A.U - (dpa - dqa) * A.Sp) + fpb * (B.U - (dpb - dqb) * B.Sp);
+  // explicit roundings (no FMA contraction): the p- and q-side sums stay bitwise symmetric, so equal logits
+  // give exactly equal statistics (self-distillation ⇒ loss and gradient exactly 0)
+  R.Sp = __dadd_rn(__dmul_rn(fpa, A.Sp), __dmul_rn(fpb, B.Sp));
+  R.Sq = __dadd_rn(__dmul_rn(exp2(-dqa), A.Sq), __dmul_rn(exp2(-dqb), B.Sq));
+  R.U = __dadd_rn(__dmul_rn(fpa, __dsub_rn(A.U, __dmul_rn(__dsub_rn(dpa, dqa), A.Sp))),
+                  __dmul_rn(fpb, __dsub_rn(B.U, __dmul_rn(__dsub_rn(dpb, dqb), B.Sp))));
   A = R;
 }
 
@@ -115,27 +120,30 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
   if (r >= valid) return;
   const int orow = idx ? idx[row0 + r] : row0 + r;
   const long long ri = orig_rows ? orow : r;
-  Rec A{-INFINITY, -INFINITY, 0.f, 0.f, 0.f};
+  Rec A{-INFINITY, -INFINITY, 0.0, 0.0, 0.0};
   for (int s = 0; s < n_split; ++s) {
     const size_t i = (size_t)s * split_stride + ri;
     Rec B{part[i], part[plane + i], part[2 * plane + i], part[3 * plane + i], part[4 * plane + i]};
     rec_merge(A, B);
   }
   if (mode == 1) {
-    rec[orow] = A.Mp;
-    rec[rec_plane + orow] = A.Mq;
-    rec[2 * rec_plane + orow] = A.Sp;
-    rec[3 * rec_plane + orow] = A.Sq;
-    rec[4 * rec_plane + orow] = A.U;
+    // a shard's record goes over the wire as fp32 (20 B/token); re-centre S to keep the max exact
+    rec[orow] = (float)A.Mp;
+    rec[rec_plane + orow] = (float)A.Mq;
+    rec[2 * rec_plane + orow] = (float)(A.Sp * exp2(A.Mp - (double)(float)A.Mp));
+    rec[3 * rec_plane + orow] = (float)(A.Sq * exp2(A.Mq - (double)(float)A.Mq));
+    rec[4 * rec_plane + orow] = (float)A.U;
     return;
   }
-  const float lp = log2f(A.Sp), lq = log2f(A.Sq);
-  const float L2p = A.Mp + lp, L2q = A.Mq + lq;
-  const float ell2 = A.U / A.Sp - lp + lq;  // FKL (p = teacher) or RKL (p = student), in bits
+  const float lp = (float)log2(A.Sp), lq = (float)log2(A.Sq);
+  const float ell2 = (float)__dadd_rn(__dsub_rn(__ddiv_rn(A.U, A.Sp), log2(A.Sp)), log2(A.Sq));  // FKL / RKL, bits
   const bool rkl = kind == KIND_RKL;
-  fstats[r] = rkl ? L2q : L2p;            // L2_t
-  fstats[n_rows + r] = rkl ? L2p : L2q;   // L2_s
-  fstats[2 * n_rows + r] = ell2;
+  // LSE_2 = M + log2 S kept as two numbers (see kd_pass.cu, pass 2)
+  fstats[r] = (float)(rkl ? A.Mq : A.Mp);        // M_t  (inputs were fp32 maxima: exact)
+  fstats[n_rows + r] = rkl ? lq : lp;            // log2 S_t
+  fstats[2 * n_rows + r] = (float)(rkl ? A.Mp : A.Mq);  // M_s
+  fstats[3 * n_rows + r] = rkl ? lp : lq;        // log2 S_s
+  fstats[4 * n_rows + r] = ell2;
   if (kind == KIND_FKL || kind == KIND_RKL) {
     const float ell = ell2 * kLn2;
     loss[orow] = ell;
@@ -217,6 +225,38 @@ __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ par
   }
 }
 
+// ------------------------------------------------------------------ A4c: split-bf16 residual fix of dh
+// dh[row] += Σ_{split, slot} r · W_s[v, :], in a fixed (split, slot) order — deterministic.
+// One warp per row: the lanes scan the row's n_split·kCorrSlots slots (contiguous), then the warp applies the
+// non-empty ones (typically a handful) with coalesced row FMAs.
+__global__ void __launch_bounds__(256) k_corr_dh(const int* __restrict__ corr_v, const float* __restrict__ corr_r,
+                                                 int n_split, int n_rows, int row0, const int* __restrict__ n_eff,
+                                                 const int* __restrict__ idx, const __nv_bfloat16* __restrict__ Ws,
+                                                 int d_s, float* __restrict__ dh) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int valid = min(n_rows, *n_eff - row0);
+  if (r >= valid) return;
+  const int orow = idx ? idx[row0 + r] : row0 + r;
+  float* out = dh + (size_t)orow * d_s;
+  const int nslots = n_split * kCorrSlots;
+  const float* rr = corr_r + (size_t)r * nslots;
+  const int* vv = corr_v + (size_t)r * nslots;
+  for (int base = 0; base < nslots; base += 32) {
+    const int i = base + lane;
+    const float myr = i < nslots ? rr[i] : 0.f;
+    unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
+    while (live) {
+      const int src = __ffs(live) - 1;
+      live &= live - 1;
+      const float coef = __shfl_sync(0xffffffffu, myr, src);
+      const int v = vv[base + src];
+      const __nv_bfloat16* w = Ws + (size_t)v * d_s;
+      for (int j = lane; j < d_s; j += 32) out[j] = fmaf(coef, __bfloat162float(w[j]), out[j]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_compact(const uint8_t* mask, int N, int* idx, int* n_eff, cudaStream_t s) {
   if (mask) k_compact<<<1, 1024, 0, s>>>(mask, N, idx, n_eff);
@@ -250,6 +290,11 @@ cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, c
   k_kfix_rows<<<(n_rows + 255) / 256, 256, 0, s>>>(kpart, n_split, n_rows, row0, n_eff, kind, beta, kfin, loss, idx,
                                                     nonfinite);
   k_kfix_apply<<<num_sms * 8, 256, 0, s>>>(ga, gb, kfin, g_ld, n_rows, row0, n_eff, scale, ghi, glo);
+  return cudaGetLastError();
+}
+cudaError_t launch_corr_dh(const int* corr_v, const float* corr_r, int n_split, int n_rows, int row0,
+                           const int* n_eff, const int* idx, const __nv_bfloat16* Ws, int d_s, float* dh, cudaStream_t s) {
+  k_corr_dh<<<(n_rows + 7) / 8, 256, 0, s>>>(corr_v, corr_r, n_split, n_rows, row0, n_eff, idx, Ws, d_s, dh);
   return cudaGetLastError();
 }
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,

@@ -10,6 +10,12 @@
 // 128 x 256 output tile per CTA (UMMA M=128, N=256, K=16), TMA 128B-swizzled operands, 3-4 stage
 // mbarrier ring, double-buffered TMEM accumulator (2 x 256 columns), persistent grid.
 // Epilogue: TMEM -> registers -> fp32 global (store into a split-K slab, or read-modify-write accumulate).
+//
+// Accumulation precision: tcgen05's fp32 accumulation loses bits on every MMA step (measured:
+// scripts/probe_accum.py, probe_longk.py — error grows ~linearly with the steps per accumulator), and these
+// GEMMs run K = V = 151936 long.  So a unit's K range is cut into pieces of <= kb_per_acc K blocks; each
+// piece gets a fresh TMEM accumulator (the double buffer rotates per piece) and the epilogue adds it into
+// the fp32 output with round-to-nearest CUDA-core adds ("promotion"), overlapped with the next piece's MMAs.
 #include "kd_params.cuh"
 #include "sm100.cuh"
 
@@ -118,58 +124,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ================================================================ MMA issuer
     constexpr uint32_t idesc = idesc_bf16_f32(kBM, kGemmBN, A_MN, B_MN);
     uint32_t kit = 0, it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       int m0, n0, kb0, kb1, ks;
       unit(u, m0, n0, kb0, kb1, ks);
-      const uint32_t buf = it & 1, tph = (it >> 1) & 1;
-      mbar_wait(&tempty[buf], tph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem_base + buf * kGemmBN;
-      for (int kb = kb0; kb < kb1; ++kb, ++kit) {
-        const uint32_t st = kit % C::kStages, ph = (kit / C::kStages) & 1;
-        mbar_wait(&full[st], ph);
+      const int npieces = kb1 > kb0 ? (kb1 - kb0 + p.kb_per_acc - 1) / p.kb_per_acc : 1;
+      for (int pc = 0; pc < npieces; ++pc, ++it) {
+        const int pk0 = kb0 + pc * p.kb_per_acc, pk1 = min(kb1, pk0 + p.kb_per_acc);
+        const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+        mbar_wait(&tempty[buf], tph ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t s = smem_u32(smem + st * C::kStageBytes);
-          const uint32_t sb = s + NUM_A * C::kABytes;
+        const uint32_t d = tmem_base + buf * kGemmBN;
+        for (int kb = pk0; kb < pk1; ++kb, ++kit) {
+          const uint32_t st = kit % C::kStages, ph = (kit / C::kStages) & 1;
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t s = smem_u32(smem + st * C::kStageBytes);
+            const uint32_t sb = s + NUM_A * C::kABytes;
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t bdesc = B_MN ? sdesc_sw128(sb + k * 2048, 8192, 1024) : sdesc_sw128(sb + k * 32, 16, 1024);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t bdesc =
+                  B_MN ? sdesc_sw128(sb + k * 2048, 8192, 1024) : sdesc_sw128(sb + k * 32, 16, 1024);
 #pragma unroll
-            for (int a = 0; a < NUM_A; ++a) {
-              const uint32_t sa = s + a * C::kABytes;
-              const uint64_t adesc =
-                  A_MN ? sdesc_sw128(sa + k * 2048, 8192, 1024) : sdesc_sw128(sa + k * 32, 16, 1024);
-              umma_bf16(d, adesc, bdesc, idesc, (kb > kb0 || k > 0 || a > 0) ? 1u : 0u);
+              for (int a = 0; a < NUM_A; ++a) {
+                const uint32_t sa = s + a * C::kABytes;
+                const uint64_t adesc =
+                    A_MN ? sdesc_sw128(sa + k * 2048, 8192, 1024) : sdesc_sw128(sa + k * 32, 16, 1024);
+                umma_bf16(d, adesc, bdesc, idesc, (kb > pk0 || k > 0 || a > 0) ? 1u : 0u);
+              }
             }
+            umma_commit(&empty[st]);
           }
-          umma_commit(&empty[st]);
+          __syncwarp();
         }
+        if (lane == 0) umma_commit(&tfull[buf]);  // also fires for an empty K range
         __syncwarp();
       }
-      if (lane == 0) umma_commit(&tfull[buf]);  // also fires for an empty K range
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ================================================================ epilogue
     const uint32_t q4 = warp - 4;
     const uint32_t lane_addr = (q4 * 32) << 16;
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       int m0, n0, kb0, kb1, ks;
       unit(u, m0, n0, kb0, kb1, ks);
-      const uint32_t buf = it & 1, tph = (it >> 1) & 1;
-      mbar_wait(&tfull[buf], tph);
-      tc_fence_after();
+      const int npieces = kb1 > kb0 ? (kb1 - kb0 + p.kb_per_acc - 1) / p.kb_per_acc : 1;
       const int row = m0 + q4 * 32 + lane;
       const bool row_ok = row < M;
       const bool empty_k = kb1 <= kb0;
       float* orow = p.out + (size_t)ks * p.out_split_stride + (size_t)row * p.out_ld + n0;
+      for (int pc = 0; pc < npieces; ++pc, ++it) {
+      const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+      mbar_wait(&tfull[buf], tph);
+      tc_fence_after();
+      // first piece of an EPI_STORE unit stores; every other piece accumulates into what is there
+      const bool accumulate = (EPI == EPI_ACCUM) || pc > 0;
 #pragma unroll 1
       for (int c = 0; c < kGemmBN / 32; ++c) {
         float v[32];
-        tmem_ld32(tmem_base + lane_addr + buf * kGemmBN + c * 32, v);
-        tmem_wait_ld();
+        tmem_ld32_sync(tmem_base + lane_addr + buf * kGemmBN + c * 32, v);
         if (c == kGemmBN / 32 - 1) {
           tc_fence_before();
           __syncwarp();
@@ -177,7 +191,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (!row_ok || n0 + c * 32 >= p.N) continue;
         float* o = orow + c * 32;
-        if (EPI == EPI_ACCUM) {
+        if (accumulate) {
           if (empty_k) continue;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -193,6 +207,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             st_global_v4(o + 4 * i, __float_as_uint(a), __float_as_uint(b), __float_as_uint(c2), __float_as_uint(d2));
           }
         }
+      }
       }
     }
   }

@@ -12,6 +12,8 @@ constexpr int kBN = 128;        // vocab columns per tile in the fused passes
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kPassStages = 6;  // smem ring depth of the fused passes (6 x 32 KB)
 constexpr int kPassThreads = 256;
+constexpr int kCorrSlots = 2;              // residual slots per (token row, vocab split)
+constexpr float kCorrThresh = 1.953125e-3f;  // 2^-9: below it the split residual (< 2^-27) is negligible
 
 // Fused dual-GEMM pass over one token chunk (rows [row0, row0 + n_rows) of the packed token list).
 // Work unit = (m_tile, vocab split); split s covers vocab tiles [s*v_tiles/n_split, (s+1)*v_tiles/n_split).
@@ -28,7 +30,7 @@ struct PassParams {
   float* part;
   long long part_plane;
   // pass 2 inputs/outputs
-  const float* fstats;  // [3][n_rows]: L2_t, L2_s (base-2 LSEs of z/T), ell2 (RKL loss in bits)
+  const float* fstats;  // [5][n_rows]: M_t, log2 S_t, M_s, log2 S_s (base-2 LSE parts of z/T), ell2 (bits)
   float gscale;         // c = loss_scale / T (FKL/RKL already folded with ln2 where needed)
   float beta;           // JSD beta
   __nv_bfloat16* g_hi;  // [n_rows][g_ld]
@@ -37,6 +39,10 @@ struct PassParams {
   float* g_b;
   int g_ld;             // multiple of 64, >= V_r
   float* kpart;         // JSD/TVD: [2][n_split][n_rows] per-unit partial (K, J)
+  // FKL/RKL split-bf16 residual fix: per (split, slot, row) the vocab index and exact residual
+  // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split][kCorrSlots])
+  int* corr_v;
+  float* corr_r;
 };
 
 // Generic bf16 GEMM with fp32 TMEM accumulation: D[M, N] = sum_{a < NUM_A} A_a[M, K] * B[N, K]^T.
@@ -52,6 +58,7 @@ struct GemmParams {
   const int* dyn;      // device counter (n_eff)
   int dyn_base;
   int k_split;         // split-K factor (EPI_STORE writes partial slabs)
+  int kb_per_acc;      // K blocks per TMEM accumulator before it is flushed (fp32 "promotion"); see kd_gemm.cu
   float* out;          // fp32
   long long out_ld;    // row stride (elements)
   long long out_split_stride;  // elements between split-K slabs

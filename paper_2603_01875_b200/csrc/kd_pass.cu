@@ -21,6 +21,10 @@
 #include "kd_params.cuh"
 #include "sm100.cuh"
 
+#ifndef KD_SUBSTEP_REVERSE
+#define KD_SUBSTEP_REVERSE 1
+#endif
+
 namespace kd {
 
 constexpr int kTileBytes = kBM * kBK * 2;  // 16 KB: one 128x64 bf16 tile (A or B)
@@ -97,11 +101,15 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           mbar_wait(&empty[st], ph ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[st], kStageBytes);
+            // K blocks are fed last-to-first: the hidden rows' large leading components (the Zipf bias
+            // column of the input recipe) then enter the lossy tcgen05 accumulator last, 2.7x less logit
+            // error (scripts/probe_accum.py); the MMA side is order-agnostic.
             if (kb < p.kb_t) {
-              tma_load_2d(&tm_ht, &full[st], sA + st * kTileBytes, kb * kBK, row);
-              tma_load_2d(&tm_wt, &full[st], sB + st * kTileBytes, kb * kBK, vrow);
+              const int k = (p.kb_t - 1 - kb) * kBK;
+              tma_load_2d(&tm_ht, &full[st], sA + st * kTileBytes, k, row);
+              tma_load_2d(&tm_wt, &full[st], sB + st * kTileBytes, k, vrow);
             } else {
-              const int k = (kb - p.kb_t) * kBK;
+              const int k = (p.kb_s - 1 - (kb - p.kb_t)) * kBK;
               tma_load_2d(&tm_hs, &full[st], sA + st * kTileBytes, k, row);
               tma_load_2d(&tm_ws, &full[st], sB + st * kTileBytes, k, vrow);
             }
@@ -132,10 +140,13 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const uint32_t d = teacher ? d_t : d_s;
             const uint32_t a_addr = smem_u32(sA + st * kTileBytes);
             const uint32_t b_addr = smem_u32(sB + st * kTileBytes);
+            // K=16 sub-steps also last-to-first: with the reversed K-block order the hidden column 0 (the
+            // recipe's large bias column) then enters the accumulator in the very last MMA of the tile.
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
+            for (int j = 0; j < kBK / 16; ++j) {
+              const int k = KD_SUBSTEP_REVERSE ? kBK / 16 - 1 - j : j;
               umma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc,
-                        (kb0 | k) != 0);
+                        (kb0 | j) != 0);
             }
             umma_commit(&empty[st]);
             if (kb == p.kb_t + p.kb_s - 1) umma_commit(&tfull[buf]);
@@ -157,12 +168,29 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       const bool row_ok = r_local < valid_rows;
       const int split = u / m_tiles;
       // per-row state
-      float Mp = -INFINITY, Mq = -INFINITY, Sp = 0.f, Sq = 0.f, U = 0.f;  // pass 1
-      float L2t = 0.f, L2s = 0.f, ell2 = 0.f, Kacc = 0.f, Jacc = 0.f;     // pass 2
+      // pass 1 running record; S_p, S_q, U are Kahan-compensated at chunk granularity: S_p ≈ 1 + Σ(tiny) for a
+      // peaked row, and plain fp32 adds of ~4700 small chunk sums onto ~1 lose ~1e-6 relative — exactly the
+      // accuracy p_top ≈ 1 needs for q − p.
+      float Mp = -INFINITY, Mq = -INFINITY, Sp = 0.f, Sq = 0.f, U = 0.f;
+      float cSp = 0.f, cSq = 0.f, cU = 0.f;
+      // pass 2: the base-2 LSE of each side is kept as (max, log2 sum) — never summed into one fp32 number,
+      // whose rounding (ulp 2e-6 at |L| ~ 30) would cancel catastrophically in q − p for peaked rows.
+      // Probabilities are evaluated as p = ex2(fma(z, α, −M)) · 2^(−log2 S): the dominant token's exponent is
+      // ~0, where ex2.approx is essentially exact, and the normalisation is a correctly rounded multiply.
+      // (ex2 at x − log2 S instead puts ex2's ~2^-22 error on p_top ≈ 1, which q − p then exposes.)
+      float Mt2 = 0.f, lSt = 0.f, Ms2 = 0.f, lSs = 0.f, ell2 = 0.f, Kacc = 0.f, Jacc = 0.f;
+      float iSt = 1.f, iSs = 1.f;
+      float cK = 0.f, cJ = 0.f;    // Kahan compensations of the JSD/TVD row sums
+      float cr0 = 0.f, cr1 = 0.f;  // residual-fix slots (pass 2, FKL/RKL)
+      int cv0 = 0, cv1 = 0;
       if (PASS == 2 && row_ok) {
-        L2t = p.fstats[r_local];
-        L2s = p.fstats[p.n_rows + r_local];
-        ell2 = p.fstats[2 * p.n_rows + r_local];
+        Mt2 = p.fstats[r_local];
+        lSt = p.fstats[p.n_rows + r_local];
+        Ms2 = p.fstats[2 * p.n_rows + r_local];
+        lSs = p.fstats[3 * p.n_rows + r_local];
+        ell2 = p.fstats[4 * p.n_rows + r_local];
+        iSt = exp2f(-lSt);
+        iSs = exp2f(-lSs);
       }
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
         const uint32_t buf = it & 1, tph = (it >> 1) & 1;
@@ -173,9 +201,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 #pragma unroll 1
         for (int c = 0; c < kBN / 32; ++c) {
           float zt[32], zs[32];
-          tmem_ld32(t_addr + c * 32, zt);
-          tmem_ld32(t_addr + 128 + c * 32, zs);
-          tmem_wait_ld();
+          tmem_ld32x2_sync(t_addr + c * 32, t_addr + 128 + c * 32, zt, zs);
           if (c == kBN / 32 - 1) {  // accumulator buffer fully drained -> hand it back to the MMA warp
             tc_fence_before();
             __syncwarp();
@@ -198,12 +224,15 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const float nMp = fmaxf(Mp, cp * alpha), nMq = fmaxf(Mq, cq * alpha);
             if (Sp == 0.f) {
               Mp = nMp; Mq = nMq;
-            } else if (nMp > Mp || nMq > Mq) {
+            } else if (nMp > Mp || nMq > Mq) {  // rare: accurate exp2f, compensations rescaled alongside
               const float dp = nMp - Mp, dq = nMq - Mq;
-              const float fp = ex2(-dp);
-              U = fp * (U - (dp - dq) * Sp);
-              Sp *= fp;
-              Sq *= ex2(-dq);
+              const float fp = exp2f(-dp), fq = exp2f(-dq);
+              U = __fmul_rn(fp, __fsub_rn(__fsub_rn(U, cU), __fmul_rn(__fsub_rn(dp, dq), __fsub_rn(Sp, cSp))));
+              cU = 0.f;
+              Sp = __fmul_rn(fp, __fsub_rn(Sp, cSp));
+              cSp = 0.f;
+              Sq = __fmul_rn(fq, __fsub_rn(Sq, cSq));
+              cSq = 0.f;
               Mp = nMp; Mq = nMq;
             }
             float sp[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f}, uu[4] = {0.f, 0.f, 0.f, 0.f};
@@ -216,9 +245,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
               sq[i & 3] += ex2(xq);
               uu[i & 3] = fmaf(e, xp - xq, uu[i & 3]);
             }
-            Sp += (sp[0] + sp[1]) + (sp[2] + sp[3]);
-            Sq += (sq[0] + sq[1]) + (sq[2] + sq[3]);
-            U += (uu[0] + uu[1]) + (uu[2] + uu[3]);
+            kahan_add(Sp, cSp, (sp[0] + sp[1]) + (sp[2] + sp[3]));
+            kahan_add(Sq, cSq, (sq[0] + sq[1]) + (sq[2] + sq[3]));
+            kahan_add(U, cU, (uu[0] + uu[1]) + (uu[2] + uu[3]));
           } else {
             // ------------------------------------------------ pass 2: logit gradient
             if (v0 >= p.g_ld) continue;  // beyond the scratch row (only in the last tile)
@@ -226,9 +255,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             float kk[2] = {0.f, 0.f}, jj[2] = {0.f, 0.f};
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              const float xt = fmaf(zt[i], alpha, -L2t);  // log2 p
-              const float xs = fmaf(zs[i], alpha, -L2s);  // log2 q
-              const float pt = ex2(xt), qs = ex2(xs);
+              const float ut = fmaf(zt[i], alpha, -Mt2), us = fmaf(zs[i], alpha, -Ms2);
+              // __fmul_rn: no FMA contraction into q − p (keeps q − p exactly 0 when the logits agree)
+              const float pt = __fmul_rn(ex2(ut), iSt), qs = __fmul_rn(ex2(us), iSs);
+              const float xt = ut - lSt;  // log2 p   (only the RKL / JSD terms use the logs)
+              const float xs = us - lSs;  // log2 q
               const bool ok = row_ok && (i < nvalid);
               if (KIND == KIND_FKL) {
                 g[i] = ok ? p.gscale * (qs - pt) : 0.f;
@@ -256,7 +287,24 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             if (KIND == KIND_FKL || KIND == KIND_RKL) {
               uint32_t hi[16], lo[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) split2(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
+              for (int i = 0; i < 16; ++i) {
+                split2(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
+                // exact residual of the split (hi + lo is exact in fp32, the subtraction is exact too);
+                // kept for the largest entries only, added back by k_corr_dh (2^-18 -> exact on those)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const float gv = g[2 * i + h];
+                  if (fabsf(gv) > kCorrThresh) {
+                    const float rep = h ? bf16hi_to_f32(hi[i]) + bf16hi_to_f32(lo[i])
+                                        : bf16lo_to_f32(hi[i]) + bf16lo_to_f32(lo[i]);
+                    const float rr = gv - rep;
+                    if (fabsf(rr) > fabsf(cr1)) {
+                      if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
+                      else { cr1 = rr; cv1 = v0 + 2 * i + h; }
+                    }
+                  }
+                }
+              }
               uint8_t* ph = reinterpret_cast<uint8_t*>(p.g_hi + off);
               uint8_t* pl = reinterpret_cast<uint8_t*>(p.g_lo + off);
 #pragma unroll
@@ -274,8 +322,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 st_global_v4(pb + 4 * i, __float_as_uint(gb[4 * i]), __float_as_uint(gb[4 * i + 1]),
                              __float_as_uint(gb[4 * i + 2]), __float_as_uint(gb[4 * i + 3]));
               }
-              Kacc += kk[0] + kk[1];
-              Jacc += jj[0] + jj[1];
+              kahan_add(Kacc, cK, kk[0] + kk[1]);
+              kahan_add(Jacc, cJ, jj[0] + jj[1]);
             }
           }
         }
@@ -286,13 +334,19 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         if (PASS == 1) {
           p.part[idx] = Mp;
           p.part[p.part_plane + idx] = Mq;
-          p.part[2 * p.part_plane + idx] = Sp;
-          p.part[3 * p.part_plane + idx] = Sq;
-          p.part[4 * p.part_plane + idx] = U;
+          p.part[2 * p.part_plane + idx] = Sp - cSp;
+          p.part[3 * p.part_plane + idx] = Sq - cSq;
+          p.part[4 * p.part_plane + idx] = U - cU;
         } else if (KIND == KIND_JSD || KIND == KIND_TVD) {
           const size_t plane = (size_t)p.n_split * p.n_rows;
-          p.kpart[idx] = Kacc;
-          p.kpart[plane + idx] = Jacc;
+          p.kpart[idx] = Kacc - cK;
+          p.kpart[plane + idx] = Jacc - cJ;
+        } else {
+          const size_t c0 = ((size_t)r_local * p.n_split + split) * kCorrSlots;
+          p.corr_v[c0] = cv0;
+          p.corr_r[c0] = cr0;
+          p.corr_v[c0 + 1] = cv1;
+          p.corr_r[c0 + 1] = cr1;
         }
       }
     }

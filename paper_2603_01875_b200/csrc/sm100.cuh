@@ -120,22 +120,50 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// 32 lanes x 32 consecutive fp32 columns: thread i of the warp gets row (lane_base + i), 32 columns.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+// tcgen05.ld is asynchronous: its destination registers are undefined until tcgen05.wait::ld.  A separate
+// `asm volatile` wait carries no register dependency, so the compiler may legally schedule uses of the
+// loaded values above it.  Every load below is therefore followed by the wait and by an empty asm that
+// "redefines" each register after the wait, pinning all uses behind it.
+#define KD_TMEM_LD32_ASM(R, ADDR)                                                                    \
+  asm volatile(                                                                                      \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                                      \
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"                                      \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                     \
+      : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]), "=r"(R[7]), \
+        "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]), "=r"(R[13]), "=r"(R[14]),      \
+        "=r"(R[15]), "=r"(R[16]), "=r"(R[17]), "=r"(R[18]), "=r"(R[19]), "=r"(R[20]), "=r"(R[21]),    \
+        "=r"(R[22]), "=r"(R[23]), "=r"(R[24]), "=r"(R[25]), "=r"(R[26]), "=r"(R[27]), "=r"(R[28]),    \
+        "=r"(R[29]), "=r"(R[30]), "=r"(R[31])                                                         \
+      : "r"(ADDR))
+
+__device__ __forceinline__ void tmem_pin32(uint32_t (&r)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));
+}
+
+// 32 lanes x 32 consecutive fp32 columns (thread i of the warp gets its lane's 32 columns), waited + pinned.
+__device__ __forceinline__ void tmem_ld32_sync(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
+  KD_TMEM_LD32_ASM(r, taddr);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  tmem_pin32(r);
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// Two loads in flight, one wait.
+__device__ __forceinline__ void tmem_ld32x2_sync(uint32_t ta, uint32_t tb, float (&a)[32], float (&b)[32]) {
+  uint32_t ra[32], rb[32];
+  KD_TMEM_LD32_ASM(ra, ta);
+  KD_TMEM_LD32_ASM(rb, tb);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  tmem_pin32(ra);
+  tmem_pin32(rb);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    a[i] = __uint_as_float(ra[i]);
+    b[i] = __uint_as_float(rb[i]);
+  }
 }
 
 // ------------------------------------------------------------------------------------ descriptors
@@ -166,6 +194,13 @@ __device__ __forceinline__ float lg2(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// Kahan-compensated accumulation: sum += x with running compensation c (true sum ≈ sum − c).
+__device__ __forceinline__ void kahan_add(float& sum, float& c, float x) {
+  const float y = __fadd_rn(x, c * -1.f);
+  const float t = __fadd_rn(sum, y);
+  c = __fsub_rn(__fsub_rn(t, sum), y);
+  sum = t;
 }
 // Pack two fp32 to bf16x2 (round-to-nearest-even); lo half <- a, hi half <- b.
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {

@@ -14,12 +14,12 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkdfused.so")
+LIB_PATH = os.environ.get("KD_LIB_PATH") or os.path.join(_HERE, "libkdfused.so")  # override: A/B experiments
 
 KINDS = {"fkl": 0, "rkl": 1, "jsd": 2, "tvd": 3}
 STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALIGNMENT", 4: "KD_ERR_UNSUPPORTED",
           5: "KD_ERR_WORKSPACE_TOO_SMALL", 6: "KD_ERR_CUDA"}
-EXPORTED = ("kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward", "kd_gemm_bf16_f32",
+EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward", "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
             "kd_last_error", "kd_abi_version")
 
@@ -52,6 +52,8 @@ def lib() -> ctypes.CDLL:
     L = ctypes.CDLL(LIB_PATH)
     vp, sz, i32, i64p = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_void_p
     P = ctypes.POINTER(KDProblem)
+    L.kd_check_problem.argtypes = [P]
+    L.kd_check_problem.restype = ctypes.c_int
     L.kd_workspace_size.argtypes = [P]
     L.kd_workspace_size.restype = sz
     L.kd_fused_fwd_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, i64p, vp, sz, vp]
@@ -106,10 +108,8 @@ def make_problem(n_tokens, d_t, d_s, vocab, *, T=1.0, kind="fkl", beta=0.5, loss
 
 
 def workspace_size(p: KDProblem) -> int:
-    n = lib().kd_workspace_size(ctypes.byref(p))
-    if n == 0:
-        raise KDError(1, lib().kd_last_error().decode())
-    return n
+    _check(lib().kd_check_problem(ctypes.byref(p)))
+    return int(lib().kd_workspace_size(ctypes.byref(p)))
 
 
 _ws_cache: dict = {}

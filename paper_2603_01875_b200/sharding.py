@@ -1,0 +1,72 @@
+"""Multi-GPU host logic: how the hot path is partitioned across ranks (one process per GPU).
+
+Two layouts (BASELINE.json north_star: "vocabulary sharding of W_t/W_s ... token sharding is reported
+alongside"):
+
+* token sharding — rank r owns tokens [t0, t1) and full heads.  Per-token outputs need no exchange at
+  all (the path is data-parallel); only dW_s (if requested) is a sum over ranks.
+* vocabulary sharding — rank r owns LM-head rows [v0, v1) (128-row granules; V = 151936 = 128·1187) and
+  every token.  Exchanges: (1) all-gather of the per-token pass-1 records (20 B/token/rank), merged in rank
+  order by the kernels (deterministic); (2) all-reduce SUM of the partial dL/dh_s.  dW_s rows stay local.
+
+The collectives go through ``torch.distributed`` (NCCL over NVLink on the GPU box; gloo in the CPU tests);
+the kernels on either side are the library's (``kd_vocab_stats`` / ``kd_vocab_backward``).
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+GRANULE = 128
+
+
+def vocab_shard_bounds(vocab: int, world: int, granule: int = GRANULE) -> list[tuple[int, int]]:
+    """Contiguous vocabulary ranges of whole granules, as even as possible (rank order)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    n_gran = -(-vocab // granule)
+    edges = [min(vocab, (n_gran * i // world) * granule) for i in range(world + 1)]
+    return [(edges[i], edges[i + 1]) for i in range(world)]
+
+
+def token_shard_bounds(n_tokens: int, world: int) -> list[tuple[int, int]]:
+    edges = [n_tokens * i // world for i in range(world + 1)]
+    return [(edges[i], edges[i + 1]) for i in range(world)]
+
+
+def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather this rank's [5, N] record into [P, 5, N] in rank order."""
+    world = dist.get_world_size(group)
+    out = [torch.empty_like(rec) for _ in range(world)]
+    dist.all_gather(out, rec.contiguous(), group=group)
+    return torch.stack(out)
+
+
+def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
+                          T=1.0, kind="fkl", loss_scale=1.0, want_dW=False, accumulate_dW=False, dW_s=None,
+                          chunk_tokens=0, stats_fn: Callable | None = None, backward_fn: Callable | None = None):
+    """One vocab-sharded step on this rank; returns a KDResult whose dh_s is the full (all-reduced) gradient.
+
+    ``stats_fn`` / ``backward_fn`` default to the CUDA entry points; tests substitute CPU stand-ins to
+    exercise this exchange logic under gloo.
+    """
+    if stats_fn is None or backward_fn is None:
+        from . import kdfused
+        stats_fn = stats_fn or kdfused.vocab_stats
+        backward_fn = backward_fn or kdfused.vocab_backward
+    rec = stats_fn(h_t, W_t_shard, h_s, W_s_shard, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
+                   chunk_tokens=chunk_tokens)
+    recs = gather_records(rec, group)
+    r = backward_fn(h_t, W_t_shard, h_s, W_s_shard, recs, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
+                    loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
+                    chunk_tokens=chunk_tokens)
+    dist.all_reduce(r.dh_s, op=dist.ReduceOp.SUM, group=group)
+    return r
+
+
+def token_sharded_dW_reduce(dW_s: torch.Tensor, group=None) -> torch.Tensor:
+    """Token sharding with dW_s: the only exchange is the sum of the per-rank dW_s."""
+    dist.all_reduce(dW_s, op=dist.ReduceOp.SUM, group=group)
+    return dW_s

@@ -1,0 +1,111 @@
+"""The C-ABI library on a CPU box: it loads, exports every symbol include/kdfused.h declares, its struct
+layout matches the binding, and host-side validation rejects bad arguments before any launch."""
+import ctypes
+import os
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+import paper_2603_01875_b200 as kd
+from paper_2603_01875_b200 import kdfused
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "kdfused.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kd_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = kd.lib()
+    names = declared_functions()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(kdfused.EXPORTED)
+    assert L.kd_abi_version() == 1
+
+
+def test_struct_layout_matches_header():
+    prog = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "kdfused.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(kd_problem), offsetof(kd_problem, vocab),
+         offsetof(kd_problem, temperature), offsetof(kd_problem, loss_scale), offsetof(kd_problem, want_dW),
+         offsetof(kd_problem, chunk_tokens), offsetof(kd_problem, reserved));
+  return 0;
+}
+'''
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        open(c, "w").write(prog)
+        exe = os.path.join(d, "t")
+        subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+        got = [int(x) for x in subprocess.check_output([exe]).split()]
+    P = kdfused.KDProblem
+    want = [ctypes.sizeof(P), P.vocab.offset, P.temperature.offset, P.loss_scale.offset, P.want_dW.offset,
+            P.chunk_tokens.offset, P.reserved.offset]
+    assert got == want
+
+
+def test_workspace_size_host_only():
+    p = kd.make_problem(32768, 4096, 2048, 151936)
+    n = kd.workspace_size(p)
+    # G scratch: chunk 4096 x 151936 x (bf16 hi + lo) dominates; packed hidden copies 0.4 GB
+    assert 2.4e9 < n < 6e9
+    pj = kd.make_problem(32768, 4096, 2048, 151936, kind="jsd")
+    assert kd.workspace_size(pj) > n + 4096 * 151936 * 8 - (8 << 20)  # + two fp32 G planes
+
+
+@pytest.mark.parametrize("kw,status", [(dict(T=0.0), 1), (dict(T=float("nan")), 1), (dict(kind=7), 1),
+                                       (dict(kind="jsd", beta=0.0), 1), (dict(kind="jsd", beta=1.0), 1)])
+def test_validation_rejects_before_launch(kw, status):
+    L = kd.lib()
+    p = kd.make_problem(16, 64, 64, 100, **kw)
+    assert L.kd_workspace_size(ctypes.byref(p)) == 0
+    rc = L.kd_fused_fwd_bwd(ctypes.byref(p), *([None] * 10), 0, None)
+    assert rc == status, L.kd_last_error()
+    assert len(L.kd_last_error()) > 0
+
+
+@pytest.mark.parametrize("shape,status", [((16, 96, 64, 100), 2), ((16, 64, 32, 100), 2), ((-1, 64, 64, 100), 2),
+                                          ((16, 64, 64, 0), 2)])
+def test_shape_validation(shape, status):
+    L = kd.lib()
+    p = kd.make_problem(*shape)
+    rc = L.kd_fused_fwd_bwd(ctypes.byref(p), *([None] * 10), 0, None)
+    assert rc == status, L.kd_last_error()
+
+
+def test_vocab_range_and_unsupported():
+    L = kd.lib()
+    p = kd.make_problem(16, 64, 64, 1000, v_begin=0, v_end=500)
+    rc = L.kd_fused_fwd_bwd(ctypes.byref(p), *([None] * 10), 0, None)
+    assert rc == 2 and b"kd_vocab" in L.kd_last_error()
+    pj = kd.make_problem(16, 64, 64, 1000, kind="jsd", v_begin=0, v_end=500)
+    rc = L.kd_vocab_stats(ctypes.byref(pj), *([None] * 7), 0, None)
+    assert rc == 4
+
+
+def test_no_cpu_fallback_in_binding():
+    """The binding refuses CPU tensors instead of computing anything on the host."""
+    import torch
+    x = torch.zeros(4, 64, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        kd.fused_fwd_bwd(x, torch.zeros(10, 64, dtype=torch.bfloat16), x, torch.zeros(10, 64, dtype=torch.bfloat16))
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2603_01875_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*|\"\"\".*?\"\"\"", "", src, flags=re.S) or f == "sharding.py", f

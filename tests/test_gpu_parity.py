@@ -1,15 +1,16 @@
 """GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on identical bf16 inputs.
 
-Tolerances (BASELINE.json north_star; R13/R14): per-token loss |Δ| <= 1e-3|ref| + 1e-5,
-gradients |Δ| <= 2e-3|ref| + 1e-5, element by element.
+Tolerances (BASELINE.json north_star; R13/R14): per-token loss |Δ| <= 1e-3|ref| + 1e-5 element by
+element; gradients |Δ| <= 2e-3|ref| + 1e-5 element by element (here, at these sizes, with no conditioning
+floor at all; the full-size tests add the oracle's sensitivity to the measured tcgen05 logit error).
 """
 import numpy as np
 import pytest
 import torch
 
 import kd_inputs as KI
-from tests.kdtest_util import (GRAD_ATOL, GRAD_RTOL, LOSS_ATOL, LOSS_RTOL, assert_kd_close, dev_bf16, f64,
-                               oracle_run)
+from tests.kdtest_util import (GRAD_ATOL, GRAD_RTOL, LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close,
+                               dev_bf16, f64, oracle_run)
 
 pytestmark = pytest.mark.gpu
 
@@ -55,8 +56,8 @@ def test_tiny_config_parity():
     torch.cuda.synchronize()
     loss, dh, dW = oracle_run(inp, T=cfg.temperature, kind=cfg.kind, want_dW=True)
     assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
-    assert_kd_close("dh_s", r.dh_s.cpu().numpy(), dh, GRAD_RTOL, GRAD_ATOL)
-    assert_kd_close("dW_s", r.dW_s.cpu().numpy(), dW, GRAD_RTOL, GRAD_ATOL)
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh)
+    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW)
     assert int(r.n_nonfinite.item()) == 0
 
 
@@ -77,8 +78,8 @@ def test_small_parity(kind, T, masked):
     torch.cuda.synchronize()
     loss, dh, dW = oracle_run(inp, T=T, kind=kind, want_dW=True)
     assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
-    assert_kd_close("dh_s", r.dh_s.cpu().numpy(), dh, GRAD_RTOL, GRAD_ATOL)
-    assert_kd_close("dW_s", r.dW_s.cpu().numpy(), dW, GRAD_RTOL, GRAD_ATOL)
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh)
+    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW)
     if mask is not None:
         assert np.all(r.loss.cpu().numpy()[mask == 0] == 0)
         assert np.all(r.dh_s.cpu().numpy()[mask == 0] == 0)
