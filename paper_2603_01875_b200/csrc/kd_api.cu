@@ -21,7 +21,8 @@
 #include "kd_params.cuh"
 
 namespace kd {
-cudaError_t launch_pass(int pass, int kind, const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t s);
+cudaError_t launch_pass(int pass, int kind, int cg, int bn, const CUtensorMap* maps, const PassParams& p, int grid,
+                        cudaStream_t s);
 cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, const CUtensorMap* a0, const CUtensorMap* a1,
                         const CUtensorMap* b, const GemmParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_compact(const uint8_t* mask, int N, int* idx, int* n_eff, cudaStream_t s);
@@ -132,6 +133,22 @@ static kd_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint
 }
 
 // ------------------------------------------------------------------------------------ plan
+static int cta_group() {  // KD_CTA_GROUP=1 selects single-SM pass tiles (A/B experiments); default: SM pairs
+  static int v = [] {
+    const char* e = getenv("KD_CTA_GROUP");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return v;
+}
+
+static int pass_bn() {  // KD_PASS_BN=128 selects 128-wide vocab tiles (A/B experiments); default 256
+  static int v = [] {
+    const char* e = getenv("KD_PASS_BN");
+    return (e && atoi(e) == 128) ? 128 : 256;
+  }();
+  return v;
+}
+
 static int device_sms() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -154,6 +171,8 @@ static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 struct Plan {
   int N, d_t, d_s, V_r, kind;
   int Nc, n_chunks, m_tiles_c, v_tiles, n_split, g_ld, k_split, num_sms;
+  int cg;  // CTA group of the fused passes: 2 = SM pairs (UMMA M=256), 1 = single SMs
+  int bn;  // vocab tile of the fused passes (UMMA N): 256 or 128
   bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
       off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, total;
@@ -232,16 +251,19 @@ static Plan make_plan(const kd_problem* p) {
   P.kind = p->kind;
   P.fix = (p->kind == KD_JSD || p->kind == KD_TVD);
   P.num_sms = device_sms();
+  P.cg = cta_group();
+  P.bn = pass_bn();
+  const int bmt = kBM * P.cg;  // token rows per fused-pass work tile
   int nc = p->chunk_tokens > 0 ? p->chunk_tokens : 4096;
-  const int n_pad = ((P.N + kBM - 1) / kBM) * kBM;
+  const int n_pad = ((P.N + bmt - 1) / bmt) * bmt;
   if (nc > n_pad) nc = n_pad;
-  nc = ((nc + kBM - 1) / kBM) * kBM;
-  if (nc < kBM) nc = kBM;
+  nc = ((nc + bmt - 1) / bmt) * bmt;
+  if (nc < bmt) nc = bmt;
   P.Nc = nc;
   P.n_chunks = (P.N + nc - 1) / nc;
-  P.m_tiles_c = nc / kBM;
-  P.v_tiles = (P.V_r + kBN - 1) / kBN;
-  P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, P.num_sms);
+  P.m_tiles_c = nc / bmt;
+  P.v_tiles = (P.V_r + P.bn - 1) / P.bn;
+  P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, P.num_sms / P.cg);
   P.g_ld = ((P.V_r + 63) / 64) * 64;
   P.k_split = choose_k_split(P.m_tiles_c, (P.d_s + kGemmBN - 1) / kGemmBN, (P.V_r + kBK - 1) / kBK, P.num_sms);
   size_t o = 0;
@@ -251,17 +273,17 @@ static Plan make_plan(const kd_problem* p) {
   P.off_idx = take((size_t)P.N * 4);
   P.off_ht = take((size_t)P.N * P.d_t * 2);
   P.off_hs = take((size_t)P.N * P.d_s * 2);
-  P.off_part = take((size_t)5 * P.n_split * P.Nc * 4);
+  P.off_part = take((size_t)5 * P.n_split * kEpiHalves * P.Nc * 4);
   P.off_fstats = take((size_t)5 * P.Nc * 4);
-  P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * P.Nc * 4 : 0);
+  P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * kEpiHalves * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
   P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
   P.off_glo = take((size_t)P.Nc * P.g_ld * 2);
   P.off_ga = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_gb = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
-  P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * kCorrSlots * P.Nc * 4);
-  P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * kCorrSlots * P.Nc * 4);
+  P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * kEpiHalves * kCorrSlots * P.Nc * 4);
+  P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * kEpiHalves * kCorrSlots * P.Nc * 4);
   P.total = o;
   return P;
 }
@@ -314,9 +336,9 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
   }
   kd_status st;
   if ((st = make_map(&c.maps[0], c.ht, P.d_t, P.N, (uint64_t)P.d_t * 2, kBK, kBM)) != KD_OK) return st;
-  if ((st = make_map(&c.maps[1], c.Wt, P.d_t, P.V_r, (uint64_t)P.d_t * 2, kBK, kBN)) != KD_OK) return st;
+  if ((st = make_map(&c.maps[1], c.Wt, P.d_t, P.V_r, (uint64_t)P.d_t * 2, kBK, P.bn / P.cg)) != KD_OK) return st;
   if ((st = make_map(&c.maps[2], c.hs, P.d_s, P.N, (uint64_t)P.d_s * 2, kBK, kBM)) != KD_OK) return st;
-  if ((st = make_map(&c.maps[3], c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, kBK, kBN)) != KD_OK) return st;
+  if ((st = make_map(&c.maps[3], c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, kBK, P.bn / P.cg)) != KD_OK) return st;
   return KD_OK;
 }
 
@@ -334,7 +356,7 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.n_split = P.n_split;
   pp.alpha = (float)(1.4426950408889634 / (double)p->temperature);
   pp.part = ws_at<float>(c.ws, P.off_part);
-  pp.part_plane = (long long)P.n_split * P.Nc;
+  pp.part_plane = (long long)P.n_split * kEpiHalves * P.Nc;
   pp.fstats = ws_at<float>(c.ws, P.off_fstats);
   const double cscale = (double)p->loss_scale / (double)p->temperature;
   pp.gscale = (float)(p->kind == KD_RKL ? cscale * 0.6931471805599453 : cscale);
@@ -350,9 +372,10 @@ static PassParams pass_params(const Ctx& c, int row0) {
   return pp;
 }
 
-static int pass_grid(const Plan& P) {
+static int pass_grid(const Plan& P) {  // CTAs (a multiple of the CTA group)
   const int units = P.m_tiles_c * P.n_split;
-  return units < P.num_sms ? units : P.num_sms;
+  const int workers = P.num_sms / P.cg;
+  return (units < workers ? units : workers) * P.cg;
 }
 
 // pass 2 (+ JSD/TVD fix-up) + dh GEMM (+ split-K reduce) + dW GEMM for one chunk whose final per-token
@@ -362,12 +385,12 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
   const int grid = pass_grid(P);
-  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, c.maps, pp, grid, c.s));
+  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, P.cg, P.bn, c.maps, pp, grid, c.s));
   if (P.fix) {
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
                                                  : 0.5 * cscale);
-    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
+    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
                           pp.g_hi, pp.g_lo, P.num_sms, c.s));
   }
@@ -397,7 +420,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                              P.num_sms, c.s));
   if (!P.fix)
-    KD_LAUNCH(K_CORR_DH, launch_corr_dh(pp.corr_v, pp.corr_r, P.n_split, P.Nc, row0, c.n_eff, c.idx, c.Ws, P.d_s, dh,
+    KD_LAUNCH(K_CORR_DH, launch_corr_dh(pp.corr_v, pp.corr_r, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, c.idx, c.Ws, P.d_s, dh,
                                         c.s));
   if (dW) {
     CUtensorMap ma_hi, ma_lo, mh;
@@ -476,8 +499,8 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
-    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 0,
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
   }
@@ -508,8 +531,8 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, c.maps, pp, pass_grid(P), c.s));
-    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split, P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
                            nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, c.s));
   }
   return KD_OK;

@@ -11,7 +11,11 @@ constexpr int kBM = 128;        // token rows per tile (UMMA M, one TMEM lane pe
 constexpr int kBN = 128;        // vocab columns per tile in the fused passes
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kPassStages = 6;  // smem ring depth of the fused passes (6 x 32 KB)
-constexpr int kPassThreads = 256;
+constexpr int kEpiWarps = 8;   // fused-pass epilogue: 2 warps per TMEM lane quarter, each owning half the columns
+constexpr int kEpiHalves = kEpiWarps / 4;
+constexpr int kPassThreads = 128 + 32 * kEpiWarps;  // warps 0-3: TMA / MMA / TMEM alloc / idle; 4..: epilogue
+// Per token row, each (vocab split, column half) writes its own partial record / K-J partial / residual slots:
+// "record slots" = n_split * kEpiHalves, merged downstream in a fixed order.
 constexpr int kCorrSlots = 2;              // residual slots per (token row, vocab split)
 constexpr float kCorrThresh = 1.953125e-3f;  // 2^-9: below it the split residual (< 2^-27) is negligible
 
@@ -26,7 +30,7 @@ struct PassParams {
   int V_r;            // local vocabulary rows
   int n_split;
   float alpha;        // log2(e) / T
-  // pass 1 output: partial records, plane f at part + f*part_plane, index split*n_rows + r
+  // pass 1 output: partial records, plane f at part + f*part_plane, index (split*kEpiHalves + half)*n_rows + r
   float* part;
   long long part_plane;
   // pass 2 inputs/outputs
@@ -38,9 +42,9 @@ struct PassParams {
   float* g_a;           // JSD/TVD: [n_rows][g_ld] fp32 planes
   float* g_b;
   int g_ld;             // multiple of 64, >= V_r
-  float* kpart;         // JSD/TVD: [2][n_split][n_rows] per-unit partial (K, J)
+  float* kpart;         // JSD/TVD: [2][n_split*kEpiHalves][n_rows] per-(unit, half) partial (K, J)
   // FKL/RKL split-bf16 residual fix: per (split, slot, row) the vocab index and exact residual
-  // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split][kCorrSlots])
+  // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split*kEpiHalves][kCorrSlots])
   int* corr_v;
   float* corr_r;
 };

@@ -28,8 +28,22 @@
 namespace kd {
 
 constexpr int kTileBytes = kBM * kBK * 2;  // 16 KB: one 128x64 bf16 tile (A or B)
-constexpr int kStageBytes = 2 * kTileBytes;
-constexpr int kPassSmem = kPassStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+// CG = CTA group: 1 = one SM computes a 128-token x 128-vocab tile (UMMA M=128);
+//                 2 = an SM pair (cluster of 2) computes 256 x 128 with tcgen05.mma.cta_group::2 (UMMA M=256):
+//                     each CTA stages its own 128 token rows of H and HALF (64 rows) of the vocab tile of W, so
+//                     per-SM operand traffic per MMA drops by 25% and the tensor pipe is no longer starved.
+// BN = vocab columns per tile = UMMA N.  BN = 128 double-buffers the TMEM accumulators (2 x (t + s) = 512 cols) so
+//      the epilogue overlaps the next tile's MMAs; BN = 256 fills TMEM with one (t + s) pair (no overlap) but its
+//      UMMA N=256 instructions sustain a much higher tensor-pipe rate (measured).
+template <int CG, int BN>
+struct PassCfg {
+  static constexpr int kABytes = kTileBytes;                 // 128 rows of H per CTA
+  static constexpr int kBBytes = (BN / CG) * kBK * 2;        // BN/CG rows of W per CTA
+  static constexpr int kStages = (192 * 1024) / (kABytes + kBBytes);
+  static constexpr int kNumBuf = 512 / (2 * BN);             // TMEM accumulator buffers
+  static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 struct UnitRange {
   int m_tile, vt0, vt1;
@@ -43,23 +57,29 @@ __device__ __forceinline__ UnitRange unit_range(int u, int m_tiles, int n_split,
   return r;
 }
 
-template <int PASS, int KIND>
+template <int PASS, int KIND, int CG, int BN>
 __global__ void __launch_bounds__(kPassThreads, 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
                    const PassParams p) {
+  using C = PassCfg<CG, BN>;
+  constexpr int kStages = C::kStages;
+  constexpr int kNB = C::kNumBuf;
+  constexpr int kBMt = kBM * CG;  // token rows per work tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kPassStages * kTileBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kPassStages * kTileBytes);
-  uint64_t* empty = full + kPassStages;
-  uint64_t* tfull = empty + kPassStages;
+  uint8_t* sB = smem + kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * C::kBBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
+  const int worker = blockIdx.x / CG, n_workers = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_ht);
@@ -68,88 +88,101 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     tma_prefetch(&tm_ws);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kPassStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[b], kEpiWarps * CG);  // one arrival per epilogue warp of every CTA in the group
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    if (CG == 2) tmem_alloc_pair(tmem_slot, 512);
+    else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int valid_rows = min(p.n_rows, *p.n_eff - p.row0);
-  const int m_tiles = valid_rows > 0 ? (valid_rows + kBM - 1) / kBM : 0;
+  const int m_tiles = valid_rows > 0 ? (valid_rows + kBMt - 1) / kBMt : 0;
   const int n_units = m_tiles * p.n_split;
 
   if (warp == 0) {
     // ================================================================ TMA producer
     uint32_t kit = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = worker; u < n_units; u += n_workers) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
-      const int row = p.row0 + ur.m_tile * kBM;
+      const int row = p.row0 + ur.m_tile * kBMt + rank * kBM;  // this CTA's 128 token rows
       for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
-        const int vrow = vt * kBN;
+        const int vrow = vt * BN + rank * (BN / CG);           // this CTA's share of the vocab tile
         for (int kb = 0; kb < p.kb_t + p.kb_s; ++kb, ++kit) {
-          const uint32_t st = kit % kPassStages, ph = (kit / kPassStages) & 1;
+          const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
           mbar_wait(&empty[st], ph ^ 1);
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[st], kStageBytes);
+            // the leader's full barrier collects the bytes of both CTAs
+            if (rank == 0) mbar_arrive_expect_tx(&full[st], CG * (C::kABytes + C::kBBytes));
             // K blocks are fed last-to-first: the hidden rows' large leading components (the Zipf bias
             // column of the input recipe) then enter the lossy tcgen05 accumulator last, 2.7x less logit
             // error (scripts/probe_accum.py); the MMA side is order-agnostic.
-            if (kb < p.kb_t) {
-              const int k = (p.kb_t - 1 - kb) * kBK;
-              tma_load_2d(&tm_ht, &full[st], sA + st * kTileBytes, k, row);
-              tma_load_2d(&tm_wt, &full[st], sB + st * kTileBytes, k, vrow);
+            const bool tch = kb < p.kb_t;
+            const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
+            const CUtensorMap* ma = tch ? &tm_ht : &tm_hs;
+            const CUtensorMap* mb = tch ? &tm_wt : &tm_ws;
+            if (CG == 2) {
+              tma_load_2d_pair(ma, &full[st], sA + st * C::kABytes, k, row);
+              tma_load_2d_pair(mb, &full[st], sB + st * C::kBBytes, k, vrow);
             } else {
-              const int k = (p.kb_s - 1 - (kb - p.kb_t)) * kBK;
-              tma_load_2d(&tm_hs, &full[st], sA + st * kTileBytes, k, row);
-              tma_load_2d(&tm_ws, &full[st], sB + st * kTileBytes, k, vrow);
+              tma_load_2d(ma, &full[st], sA + st * C::kABytes, k, row);
+              tma_load_2d(mb, &full[st], sB + st * C::kBBytes, k, vrow);
             }
           }
           __syncwarp();
         }
       }
     }
-  } else if (warp == 1) {
-    // ================================================================ MMA issuer (one thread)
-    constexpr uint32_t idesc = idesc_bf16_f32(kBM, kBN, false, false);
+  } else if (warp == 1 && rank == 0) {
+    // ================================================================ MMA issuer (one thread of the leader)
+    constexpr uint32_t idesc = idesc_bf16_f32(kBMt, BN, false, false);
     uint32_t kit = 0, it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = worker; u < n_units; u += n_workers) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
-        const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+        const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
         mbar_wait(&tempty[buf], tph ^ 1);
         tc_fence_after();
-        const uint32_t d_t = tmem_base + buf * 256;
-        const uint32_t d_s = d_t + 128;
+        const uint32_t d_t = tmem_base + buf * (2 * BN);
+        const uint32_t d_s = d_t + BN;
         for (int kb = 0; kb < p.kb_t + p.kb_s; ++kb, ++kit) {
-          const uint32_t st = kit % kPassStages, ph = (kit / kPassStages) & 1;
+          const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
           mbar_wait(&full[st], ph);
           tc_fence_after();
           if (lane == 0) {
             const bool teacher = kb < p.kb_t;
             const int kb0 = teacher ? kb : kb - p.kb_t;
             const uint32_t d = teacher ? d_t : d_s;
-            const uint32_t a_addr = smem_u32(sA + st * kTileBytes);
-            const uint32_t b_addr = smem_u32(sB + st * kTileBytes);
+            const uint32_t a_addr = smem_u32(sA + st * C::kABytes);
+            const uint32_t b_addr = smem_u32(sB + st * C::kBBytes);
             // K=16 sub-steps also last-to-first: with the reversed K-block order the hidden column 0 (the
             // recipe's large bias column) then enters the accumulator in the very last MMA of the tile.
 #pragma unroll
             for (int j = 0; j < kBK / 16; ++j) {
               const int k = KD_SUBSTEP_REVERSE ? kBK / 16 - 1 - j : j;
-              umma_bf16(d, sdesc_sw128(a_addr + k * 32, 16, 1024), sdesc_sw128(b_addr + k * 32, 16, 1024), idesc,
-                        (kb0 | j) != 0);
+              const uint64_t ad = sdesc_sw128(a_addr + k * 32, 16, 1024), bd = sdesc_sw128(b_addr + k * 32, 16, 1024);
+              if (CG == 2) umma_bf16_pair(d, ad, bd, idesc, (kb0 | j) != 0);
+              else umma_bf16(d, ad, bd, idesc, (kb0 | j) != 0);
             }
-            umma_commit(&empty[st]);
-            if (kb == p.kb_t + p.kb_s - 1) umma_commit(&tfull[buf]);
+            if (CG == 2) {  // stage consumed in both CTAs; at tile end the accumulator is ready in both TMEMs
+              umma_commit_pair(&empty[st], 0x3);
+              if (kb == p.kb_t + p.kb_s - 1) umma_commit_pair(&tfull[buf], 0x3);
+            } else {
+              umma_commit(&empty[st]);
+              if (kb == p.kb_t + p.kb_s - 1) umma_commit(&tfull[buf]);
+            }
           }
           __syncwarp();
         }
@@ -157,16 +190,20 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     }
   } else if (warp >= 4) {
     // ================================================================ epilogue (one token row per thread)
-    const uint32_t q4 = warp - 4;                   // TMEM lane quarter
+    const uint32_t q4 = (warp - 4) & 3;             // TMEM lane quarter (warp w may only touch lanes 32(w%4)..)
+    const int half = (warp - 4) >> 2;               // which half of the tile's columns this warp owns
     const int r_in_tile = q4 * 32 + lane;
     const uint32_t lane_addr = (q4 * 32) << 16;
     const float alpha = p.alpha;
+    // the leader's tempty barrier collects the releases of both CTAs' epilogues
+    const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = worker; u < n_units; u += n_workers) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
-      const int r_local = ur.m_tile * kBM + r_in_tile;  // row within the chunk
+      const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;  // row within the chunk
       const bool row_ok = r_local < valid_rows;
       const int split = u / m_tiles;
+      const int rslot = split * kEpiHalves + half;  // this thread's record slot
       // per-row state
       // pass 1 running record; S_p, S_q, U are Kahan-compensated at chunk granularity: S_p ≈ 1 + Σ(tiny) for a
       // peaked row, and plain fp32 adds of ~4700 small chunk sums onto ~1 lose ~1e-6 relative — exactly the
@@ -193,19 +230,23 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         iSs = exp2f(-lSs);
       }
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
-        const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+        const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
         mbar_wait(&tfull[buf], tph);
         tc_fence_after();
-        const uint32_t t_addr = tmem_base + lane_addr + buf * 256;
-        const int vbase = vt * kBN;
+        const uint32_t t_addr = tmem_base + lane_addr + buf * (2 * BN);
+        const int vbase = vt * BN;
+        constexpr int kChunks = BN / 32 / kEpiHalves;  // 32-column chunks per warp
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
           float zt[32], zs[32];
-          tmem_ld32x2_sync(t_addr + c * 32, t_addr + 128 + c * 32, zt, zs);
-          if (c == kBN / 32 - 1) {  // accumulator buffer fully drained -> hand it back to the MMA warp
+          tmem_ld32x2_sync(t_addr + c * 32, t_addr + BN + c * 32, zt, zs);
+          if (c == (half + 1) * kChunks - 1) {  // this warp's part drained -> release toward the MMA warp
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (lane == 0) {
+              if (CG == 2) mbar_arrive_cluster(tempty_leader + buf * 8);
+              else mbar_arrive(&tempty[buf]);
+            }
           }
           const int v0 = vbase + c * 32;
           const int nvalid = min(32, p.V_r - v0);  // columns of this chunk inside [0, V_r)
@@ -330,7 +371,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       }
       // ---- unit done: emit per-row partials (rows inside the chunk's valid range only)
       if (row_ok) {
-        const size_t idx = (size_t)split * p.n_rows + r_local;
+        const size_t idx = (size_t)rslot * p.n_rows + r_local;
         if (PASS == 1) {
           p.part[idx] = Mp;
           p.part[p.part_plane + idx] = Mq;
@@ -338,11 +379,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           p.part[3 * p.part_plane + idx] = Sq - cSq;
           p.part[4 * p.part_plane + idx] = U - cU;
         } else if (KIND == KIND_JSD || KIND == KIND_TVD) {
-          const size_t plane = (size_t)p.n_split * p.n_rows;
+          const size_t plane = (size_t)p.n_split * kEpiHalves * p.n_rows;
           p.kpart[idx] = Kacc - cK;
           p.kpart[plane + idx] = Jacc - cJ;
         } else {
-          const size_t c0 = ((size_t)r_local * p.n_split + split) * kCorrSlots;
+          const size_t c0 = ((size_t)r_local * p.n_split * kEpiHalves + rslot) * kCorrSlots;
           p.corr_v[c0] = cv0;
           p.corr_r[c0] = cr0;
           p.corr_v[c0 + 1] = cv1;
@@ -352,36 +393,61 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();  // neither CTA leaves while its partner may still signal its barriers
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, 512);
+  if (warp == 2) {
+    if (CG == 2) tmem_dealloc_pair(tmem_base, 512);
+    else tmem_dealloc(tmem_base, 512);
+  }
 }
 
 // ------------------------------------------------------------------------------- host-side launchers
-template <int PASS, int KIND>
+template <int PASS, int KIND, int CG, int BN>
 static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t stream) {
-  auto kern = kd_pass_kernel<PASS, KIND>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPassSmem);
+  auto kern = kd_pass_kernel<PASS, KIND, CG, BN>;
+  const int smem = PassCfg<CG, BN>::kSmem;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kPassThreads, kPassSmem, stream>>>(maps[0], maps[1], maps[2], maps[3], p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kPassThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
 }
 
-cudaError_t launch_pass(int pass, int kind, const CUtensorMap* maps, const PassParams& p, int grid,
-                        cudaStream_t stream) {
+template <int CG, int BN>
+static cudaError_t launch_pass_cg(int pass, int kind, const CUtensorMap* maps, const PassParams& p, int grid,
+                                  cudaStream_t stream) {
   if (pass == 1) {
     // pass 1 only distinguishes which side is "primary" (RKL swaps the roles)
-    return kind == KIND_RKL ? launch_pass_t<1, KIND_RKL>(maps, p, grid, stream)
-                            : launch_pass_t<1, KIND_FKL>(maps, p, grid, stream);
+    return kind == KIND_RKL ? launch_pass_t<1, KIND_RKL, CG, BN>(maps, p, grid, stream)
+                            : launch_pass_t<1, KIND_FKL, CG, BN>(maps, p, grid, stream);
   }
   switch (kind) {
-    case KIND_FKL: return launch_pass_t<2, KIND_FKL>(maps, p, grid, stream);
-    case KIND_RKL: return launch_pass_t<2, KIND_RKL>(maps, p, grid, stream);
-    case KIND_JSD: return launch_pass_t<2, KIND_JSD>(maps, p, grid, stream);
-    default: return launch_pass_t<2, KIND_TVD>(maps, p, grid, stream);
+    case KIND_FKL: return launch_pass_t<2, KIND_FKL, CG, BN>(maps, p, grid, stream);
+    case KIND_RKL: return launch_pass_t<2, KIND_RKL, CG, BN>(maps, p, grid, stream);
+    case KIND_JSD: return launch_pass_t<2, KIND_JSD, CG, BN>(maps, p, grid, stream);
+    default: return launch_pass_t<2, KIND_TVD, CG, BN>(maps, p, grid, stream);
   }
 }
 
-int pass_smem_bytes() { return kPassSmem; }
+// cg = 1: single-SM tiles (grid = #tile workers); cg = 2: SM pairs (grid = 2 x #pair workers).
+// bn = vocab tile (UMMA N) 128 or 256.  maps: [H_t, W_t, H_s, W_s] with W boxes of bn / cg rows.
+cudaError_t launch_pass(int pass, int kind, int cg, int bn, const CUtensorMap* maps, const PassParams& p, int grid,
+                        cudaStream_t stream) {
+  if (cg == 2) return bn == 256 ? launch_pass_cg<2, 256>(pass, kind, maps, p, grid, stream)
+                                : launch_pass_cg<2, 128>(pass, kind, maps, p, grid, stream);
+  return bn == 256 ? launch_pass_cg<1, 256>(pass, kind, maps, p, grid, stream)
+                   : launch_pass_cg<1, 128>(pass, kind, maps, p, grid, stream);
+}
 
 }  // namespace kd
