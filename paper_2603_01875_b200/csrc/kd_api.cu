@@ -37,9 +37,8 @@ cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, c
                         const float* gb, int g_ld, float scale, __nv_bfloat16* ghi, __nv_bfloat16* glo,
                         int num_sms, cudaStream_t s);
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
-                             const int* n_eff, const int* idx, float* dh, int num_sms, cudaStream_t s);
-cudaError_t launch_corr_dh(const int* corr_v, const float* corr_r, int n_split, int n_rows, int row0,
-                           const int* n_eff, const int* idx, const __nv_bfloat16* Ws, int d_s, float* dh, cudaStream_t s);
+                             const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
+                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s);
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
 }  // namespace kd
 
@@ -68,9 +67,9 @@ static kd_status fail(kd_status st, const char* fmt, ...) {
 // When enabled, every launch is bracketed by two CUDA events on the launch stream; kd_profile_read()
 // resolves them into per-kernel totals (bench.py uses this for the live roofline figure).
 enum KernelId : int { K_COMPACT, K_GATHER, K_ZERO, K_PASS1, K_MERGE, K_PASS2, K_KFIX, K_GEMM_DH, K_REDUCE_DH,
-                      K_GEMM_DW, K_GEMM, K_CORR_DH, K_NUM };
+                      K_GEMM_DW, K_GEMM, K_NUM };
 static const char* kKernelNames[K_NUM] = {"compact", "gather", "zero_masked", "pass1", "merge", "pass2",
-                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm", "corr_dh"};
+                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm"};
 struct ProfRec { int id; cudaEvent_t a, b; };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -394,11 +393,12 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
                           pp.g_hi, pp.g_lo, P.num_sms, c.s));
   }
-  // dh_s rows of this chunk: [G_hi | G_lo] · W_s  (K = V_r), split-K partial slabs, then reduce + scatter
+  // dh_s rows of this chunk: [G_hi | G_lo] · W_s  (K = V_r); the scratch holds Gᵀ [g_ld][Nc], i.e. the A operand
+  // [tokens, V] is MN-major; W_s [V_r, d_s] is the MN-major B operand.  Split-K slabs, then reduce + scatter.
   CUtensorMap mg_hi, mg_lo, mw;
   kd_status st;
-  if ((st = make_map(&mg_hi, pp.g_hi, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, kBK, kBM)) != KD_OK) return st;
-  if ((st = make_map(&mg_lo, pp.g_lo, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, kBK, kBM)) != KD_OK) return st;
+  if ((st = make_map(&mg_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK) return st;
+  if ((st = make_map(&mg_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK) return st;
   if ((st = make_map(&mw, c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK) return st;
   GemmParams gp{};
   gp.M = P.Nc;
@@ -414,18 +414,17 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   gp.out_split_stride = (long long)P.Nc * P.d_s;
   {
     const int units = P.m_tiles_c * ((P.d_s + kGemmBN - 1) / kGemmBN) * P.k_split;
-    KD_LAUNCH(K_GEMM_DH, launch_gemm(false, true, 2, EPI_STORE, &mg_hi, &mg_lo, &mw, gp, units < P.num_sms ? units : P.num_sms,
+    KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, 2, EPI_STORE, &mg_hi, &mg_lo, &mw, gp, units < P.num_sms ? units : P.num_sms,
                           c.s));
   }
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
-                             P.num_sms, c.s));
-  if (!P.fix)
-    KD_LAUNCH(K_CORR_DH, launch_corr_dh(pp.corr_v, pp.corr_r, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, c.idx, c.Ws, P.d_s, dh,
-                                        c.s));
+                                          P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
+                                          P.n_split * kEpiHalves * kCorrSlots, c.Ws, c.s));
   if (dW) {
     CUtensorMap ma_hi, ma_lo, mh;
-    if ((st = make_map(&ma_hi, pp.g_hi, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, 64, kBK)) != KD_OK) return st;
-    if ((st = make_map(&ma_lo, pp.g_lo, P.g_ld, P.Nc, (uint64_t)P.g_ld * 2, 64, kBK)) != KD_OK) return st;
+    // dW_s += Gᵀ · H_s: A = Gᵀ [g_ld][Nc] is K-major (K = tokens), B = H_s chunk MN-major
+    if ((st = make_map(&ma_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, kBK, kBM)) != KD_OK) return st;
+    if ((st = make_map(&ma_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, kBK, kBM)) != KD_OK) return st;
     const int rows_left = P.N - row0;
     if ((st = make_map(&mh, c.hs + (size_t)row0 * P.d_s, P.d_s, rows_left, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK)
       return st;
@@ -442,7 +441,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
     wp.out_ld = P.d_s;
     wp.out_split_stride = 0;
     const int units = ((P.V_r + kBM - 1) / kBM) * ((P.d_s + kGemmBN - 1) / kGemmBN);
-    KD_LAUNCH(K_GEMM_DW, launch_gemm(true, true, 2, EPI_ACCUM, &ma_hi, &ma_lo, &mh, wp, units < P.num_sms ? units : P.num_sms,
+    KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, 2, EPI_ACCUM, &ma_hi, &ma_lo, &mh, wp, units < P.num_sms ? units : P.num_sms,
                           c.s));
   }
   return KD_OK;

@@ -82,27 +82,51 @@ __global__ void __launch_bounds__(256) k_zero_masked(const uint8_t* __restrict__
 }
 
 // ------------------------------------------------------------------ A2: merge of split records
-// The merge runs in fp64 (a few dozen records per token, negligible cost): one split holds S ≈ 1 and the
-// others add small amounts, which fp32 would round away at the 1e-7 level p_top ≈ 1 is sensitive to.
+// Merge of R records of one row with the pairwise operator, in its closed form: with M = max_r m_r,
+//   S = Σ_r 2^{m_r − M} S_r ,   U = Σ_r 2^{m_p,r − M_p} (U_r − ((M_p − m_p,r) − (M_q − m_q,r)) S_p,r)
+// (identical to folding ⊕ in record order; the oracle's kd_blockwise pins that algebra).  Factors come from
+// fp32 exp2f of an exact fp32 difference — the dominant record's factor is exactly 1 — and the sums are
+// accumulated in fp64 with explicit roundings (no contraction), so the p- and q-side stay bitwise symmetric
+// and S ≈ 1 + Σ(small) keeps the 1e-7-level accuracy p_top ≈ 1 needs.
 struct Rec {
   double Mp, Mq, Sp, Sq, U;
 };
-__device__ __forceinline__ void rec_merge(Rec& A, const Rec& B) {
-  if (B.Sp == 0.0) return;  // empty record = identity
-  if (A.Sp == 0.0) { A = B; return; }
-  const double Mp = fmax(A.Mp, B.Mp), Mq = fmax(A.Mq, B.Mq);
-  const double dpa = Mp - A.Mp, dqa = Mq - A.Mq, dpb = Mp - B.Mp, dqb = Mq - B.Mq;
-  const double fpa = exp2(-dpa), fpb = exp2(-dpb);
-  Rec R;
-  R.Mp = Mp;
-  R.Mq = Mq;
-  // explicit roundings (no FMA contraction): the p- and q-side sums stay bitwise symmetric, so equal logits
-  // give exactly equal statistics (self-distillation ⇒ loss and gradient exactly 0)
-  R.Sp = __dadd_rn(__dmul_rn(fpa, A.Sp), __dmul_rn(fpb, B.Sp));
-  R.Sq = __dadd_rn(__dmul_rn(exp2(-dqa), A.Sq), __dmul_rn(exp2(-dqb), B.Sq));
-  R.U = __dadd_rn(__dmul_rn(fpa, __dsub_rn(A.U, __dmul_rn(__dsub_rn(dpa, dqa), A.Sp))),
-                  __dmul_rn(fpb, __dsub_rn(B.U, __dmul_rn(__dsub_rn(dpb, dqb), B.Sp))));
-  A = R;
+// One warp per row: lane l takes records l, l+32, ...; max and sums are combined with a fixed xor-shuffle tree
+// (deterministic, and the same tree for the p- and q-side).
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ __forceinline__ float warp_max_f(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ __forceinline__ Rec merge_records(const float* __restrict__ part, long long plane, long long split_stride,
+                                             int n, long long ri, int lane) {
+  float Mp = -INFINITY, Mq = -INFINITY;
+  for (int s = lane; s < n; s += 32) {
+    const size_t i = (size_t)s * split_stride + ri;
+    if (part[2 * plane + i] == 0.f) continue;  // empty record = identity
+    Mp = fmaxf(Mp, part[i]);
+    Mq = fmaxf(Mq, part[plane + i]);
+  }
+  Mp = warp_max_f(Mp);
+  Mq = warp_max_f(Mq);
+  double Sp = 0.0, Sq = 0.0, U = 0.0;
+  for (int s = lane; s < n; s += 32) {
+    const size_t i = (size_t)s * split_stride + ri;
+    const float sp = part[2 * plane + i];
+    if (sp == 0.f) continue;
+    const float dp = __fsub_rn(Mp, part[i]), dq = __fsub_rn(Mq, part[plane + i]);
+    const double fp = (double)exp2f(-dp), fq = (double)exp2f(-dq);
+    Sp = __dadd_rn(Sp, __dmul_rn(fp, (double)sp));
+    Sq = __dadd_rn(Sq, __dmul_rn(fq, (double)part[3 * plane + i]));
+    U = __dadd_rn(U, __dmul_rn(fp, __dsub_rn((double)part[4 * plane + i],
+                                             __dmul_rn(__dsub_rn((double)dp, (double)dq), (double)sp))));
+  }
+  return Rec{Mp, Mq, warp_sum_d(Sp), warp_sum_d(Sq), warp_sum_d(U)};
 }
 
 // mode 0: final statistics of the chunk's rows (fstats + FKL/RKL loss); mode 1: the merged record itself
@@ -115,17 +139,14 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
                                                      float* __restrict__ rec, long long rec_plane,
                                                      const int* __restrict__ idx, int orig_rows,
                                                      long long* __restrict__ nonfinite) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int valid = min(n_rows, *n_eff - row0);
   if (r >= valid) return;
   const int orow = idx ? idx[row0 + r] : row0 + r;
   const long long ri = orig_rows ? orow : r;
-  Rec A{-INFINITY, -INFINITY, 0.0, 0.0, 0.0};
-  for (int s = 0; s < n_split; ++s) {
-    const size_t i = (size_t)s * split_stride + ri;
-    Rec B{part[i], part[plane + i], part[2 * plane + i], part[3 * plane + i], part[4 * plane + i]};
-    rec_merge(A, B);
-  }
+  const Rec A = merge_records(part, plane, split_stride, n_split, ri, lane);
+  if (lane != 0) return;
   if (mode == 1) {
     // a shard's record goes over the wire as fp32 (20 B/token); re-centre S to keep the max exact
     rec[orow] = (float)A.Mp;
@@ -181,78 +202,104 @@ __global__ void __launch_bounds__(256) k_kfix_rows(const float* __restrict__ kpa
   if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
 }
 
-// G = scale·(G_a − K_r·G_b) -> split bf16, over rows [0, rows_pad) and columns [0, g_ld)
+// G = scale·(G_a − K_r·G_b) -> split bf16, over the transposed scratch [g_ld][n_rows]: element (v, r) at v*n_rows + r,
+// rows [0, rows_pad) (the rows pass 2 wrote).  n_rows % 4 == 0.
 __global__ void __launch_bounds__(256) k_kfix_apply(const float* __restrict__ ga, const float* __restrict__ gb,
                                                     const float* __restrict__ kfin, int g_ld, int n_rows, int row0,
                                                     const int* __restrict__ n_eff, float scale,
                                                     __nv_bfloat16* __restrict__ ghi, __nv_bfloat16* __restrict__ glo) {
-  const int per_row4 = g_ld / 4;
   const int valid = min(n_rows, *n_eff - row0);
-  const int rows_pad = valid > 0 ? min(n_rows, (valid + kBM - 1) / kBM * kBM) : 0;  // rows pass 2 wrote
-  const long long total4 = (long long)rows_pad * per_row4;
+  const int rows_pad = valid > 0 ? min(n_rows, (valid + 255) / 256 * 256) : 0;
+  const int per_v4 = rows_pad / 4;
+  const long long total4 = (long long)g_ld * per_v4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total4;
        i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / per_row4);
-    const float K = kfin[r];
-    const float4 a = reinterpret_cast<const float4*>(ga)[i];
-    const float4 b = reinterpret_cast<const float4*>(gb)[i];
+    const long long v = i / per_v4;
+    const int r = (int)(i % per_v4) * 4;
+    const size_t e = (size_t)v * n_rows + r;
+    const float4 a = *reinterpret_cast<const float4*>(ga + e);
+    const float4 b = *reinterpret_cast<const float4*>(gb + e);
+    const float4 K = *reinterpret_cast<const float4*>(kfin + r);
     uint32_t h0, l0, h1, l1;
-    split2(scale * (a.x - K * b.x), scale * (a.y - K * b.y), h0, l0);
-    split2(scale * (a.z - K * b.z), scale * (a.w - K * b.w), h1, l1);
-    reinterpret_cast<uint2*>(ghi)[i] = make_uint2(h0, h1);
-    reinterpret_cast<uint2*>(glo)[i] = make_uint2(l0, l1);
+    split2(scale * (a.x - K.x * b.x), scale * (a.y - K.y * b.y), h0, l0);
+    split2(scale * (a.z - K.z * b.z), scale * (a.w - K.w * b.w), h1, l1);
+    *reinterpret_cast<uint2*>(ghi + e) = make_uint2(h0, h1);
+    *reinterpret_cast<uint2*>(glo + e) = make_uint2(l0, l1);
   }
 }
 
-// ------------------------------------------------------------------ A4r: dh split-K reduce + scatter
+// ------------------------------------------------------------------ A4r: dh split-K reduce + residual fix + scatter
+// One warp per token row: lane j owns columns {8j..8j+7} + 256·i (coalesced 32-byte / 16-byte accesses).
+//   dh[orig(r), :] = Σ_ks part[ks][r, :]  +  Σ_{slot} r_slot · W_s[v_slot, :]
+// The second sum is the split-bf16 residual fix (kd_pass.cu): the exact residual g − (hi + lo) of the largest
+// entries of G, added back in a fixed (slot) order — deterministic.  d_s % 8 == 0, d_s <= 2048 * 4.
+constexpr int kRedVec = 8;  // 8-column groups per lane per column block: 32 lanes x 8 x 8 = 2048 columns
 __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ part, long long split_stride, int k_split,
                                                    int d_s, int n_rows, int row0, const int* __restrict__ n_eff,
-                                                   const int* __restrict__ idx, float* __restrict__ dh) {
-  const int valid = min(n_rows, *n_eff - row0);
-  const int per_row4 = d_s / 4;
-  const long long total4 = (long long)max(valid, 0) * per_row4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / per_row4);
-    const int j = (int)(i % per_row4);
-    float4 acc = reinterpret_cast<const float4*>(part)[i];
-    for (int s = 1; s < k_split; ++s) {
-      const float4 b = reinterpret_cast<const float4*>(part + s * split_stride)[i];
-      acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w;
-    }
-    const int orow = idx ? idx[row0 + r] : row0 + r;
-    reinterpret_cast<float4*>(dh + (size_t)orow * d_s)[j] = acc;
-  }
-}
-
-// ------------------------------------------------------------------ A4c: split-bf16 residual fix of dh
-// dh[row] += Σ_{split, slot} r · W_s[v, :], in a fixed (split, slot) order — deterministic.
-// One warp per row: the lanes scan the row's n_split·kCorrSlots slots (contiguous), then the warp applies the
-// non-empty ones (typically a handful) with coalesced row FMAs.
-__global__ void __launch_bounds__(256) k_corr_dh(const int* __restrict__ corr_v, const float* __restrict__ corr_r,
-                                                 int n_split, int n_rows, int row0, const int* __restrict__ n_eff,
-                                                 const int* __restrict__ idx, const __nv_bfloat16* __restrict__ Ws,
-                                                 int d_s, float* __restrict__ dh) {
+                                                   const int* __restrict__ idx, float* __restrict__ dh,
+                                                   const int* __restrict__ corr_v, const float* __restrict__ corr_r,
+                                                   int n_slots, const __nv_bfloat16* __restrict__ Ws) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int valid = min(n_rows, *n_eff - row0);
   if (r >= valid) return;
   const int orow = idx ? idx[row0 + r] : row0 + r;
   float* out = dh + (size_t)orow * d_s;
-  const int nslots = n_split * kCorrSlots;
-  const float* rr = corr_r + (size_t)r * nslots;
-  const int* vv = corr_v + (size_t)r * nslots;
-  for (int base = 0; base < nslots; base += 32) {
-    const int i = base + lane;
-    const float myr = i < nslots ? rr[i] : 0.f;
-    unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
-    while (live) {
-      const int src = __ffs(live) - 1;
-      live &= live - 1;
-      const float coef = __shfl_sync(0xffffffffu, myr, src);
-      const int v = vv[base + src];
-      const __nv_bfloat16* w = Ws + (size_t)v * d_s;
-      for (int j = lane; j < d_s; j += 32) out[j] = fmaf(coef, __bfloat162float(w[j]), out[j]);
+  const float* rr = corr_r ? corr_r + (size_t)r * n_slots : nullptr;
+  const int* vv = corr_v ? corr_v + (size_t)r * n_slots : nullptr;
+  for (int cb = 0; cb < d_s; cb += 32 * 8 * kRedVec) {  // column blocks of 2048
+    float acc[kRedVec][8];
+#pragma unroll
+    for (int g = 0; g < kRedVec; ++g)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
+    for (int ks = 0; ks < k_split; ++ks) {
+      const float* src = part + ks * split_stride + (size_t)r * d_s;
+#pragma unroll
+      for (int g = 0; g < kRedVec; ++g) {
+        const int col = cb + (g * 32 + lane) * 8;
+        if (col < d_s) {
+          const float4 a = *reinterpret_cast<const float4*>(src + col);
+          const float4 b = *reinterpret_cast<const float4*>(src + col + 4);
+          acc[g][0] += a.x; acc[g][1] += a.y; acc[g][2] += a.z; acc[g][3] += a.w;
+          acc[g][4] += b.x; acc[g][5] += b.y; acc[g][6] += b.z; acc[g][7] += b.w;
+        }
+      }
+    }
+    if (rr) {
+      for (int base = 0; base < n_slots; base += 32) {
+        const float myr = base + lane < n_slots ? rr[base + lane] : 0.f;
+        unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
+        while (live) {
+          const int src = __ffs(live) - 1;
+          live &= live - 1;
+          const float coef = __shfl_sync(0xffffffffu, myr, src);
+          const __nv_bfloat16* w = Ws + (size_t)vv[base + src] * d_s;
+#pragma unroll
+          for (int g = 0; g < kRedVec; ++g) {
+            const int col = cb + (g * 32 + lane) * 8;
+            if (col < d_s) {
+              const uint4 q = *reinterpret_cast<const uint4*>(w + col);
+              acc[g][0] = fmaf(coef, bf16lo_to_f32(q.x), acc[g][0]);
+              acc[g][1] = fmaf(coef, bf16hi_to_f32(q.x), acc[g][1]);
+              acc[g][2] = fmaf(coef, bf16lo_to_f32(q.y), acc[g][2]);
+              acc[g][3] = fmaf(coef, bf16hi_to_f32(q.y), acc[g][3]);
+              acc[g][4] = fmaf(coef, bf16lo_to_f32(q.z), acc[g][4]);
+              acc[g][5] = fmaf(coef, bf16hi_to_f32(q.z), acc[g][5]);
+              acc[g][6] = fmaf(coef, bf16lo_to_f32(q.w), acc[g][6]);
+              acc[g][7] = fmaf(coef, bf16hi_to_f32(q.w), acc[g][7]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kRedVec; ++g) {
+      const int col = cb + (g * 32 + lane) * 8;
+      if (col < d_s) {
+        *reinterpret_cast<float4*>(out + col) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+        *reinterpret_cast<float4*>(out + col + 4) = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
+      }
     }
   }
 }
@@ -275,7 +322,7 @@ cudaError_t launch_zero_masked(const uint8_t* mask, int N, float* loss, float* d
 cudaError_t launch_merge(const float* part, long long plane, long long split_stride, int n_split, int n_rows,
                          int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
                          long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, cudaStream_t s) {
-  k_merge_stats<<<(n_rows + 255) / 256, 256, 0, s>>>(part, plane, split_stride, n_split, n_rows, row0, n_eff, kind,
+  k_merge_stats<<<(n_rows + 7) / 8, 256, 0, s>>>(part, plane, split_stride, n_split, n_rows, row0, n_eff, kind,
                                                       mode, fstats, loss, rec, rec_plane, idx, orig_rows, nonfinite);
   return cudaGetLastError();
 }
@@ -292,14 +339,12 @@ cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, c
   k_kfix_apply<<<num_sms * 8, 256, 0, s>>>(ga, gb, kfin, g_ld, n_rows, row0, n_eff, scale, ghi, glo);
   return cudaGetLastError();
 }
-cudaError_t launch_corr_dh(const int* corr_v, const float* corr_r, int n_split, int n_rows, int row0,
-                           const int* n_eff, const int* idx, const __nv_bfloat16* Ws, int d_s, float* dh, cudaStream_t s) {
-  k_corr_dh<<<(n_rows + 7) / 8, 256, 0, s>>>(corr_v, corr_r, n_split, n_rows, row0, n_eff, idx, Ws, d_s, dh);
-  return cudaGetLastError();
-}
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
-                             const int* n_eff, const int* idx, float* dh, int num_sms, cudaStream_t s) {
-  k_reduce_dh<<<num_sms * 8, 256, 0, s>>>(part, split_stride, k_split, d_s, n_rows, row0, n_eff, idx, dh);
+                             const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
+                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s) {
+  if (d_s % 8 != 0) return cudaErrorInvalidValue;
+  k_reduce_dh<<<(n_rows + 7) / 8, 256, 0, s>>>(part, split_stride, k_split, d_s, n_rows, row0, n_eff, idx, dh, corr_v,
+                                                corr_r, n_slots, Ws);
   return cudaGetLastError();
 }
 

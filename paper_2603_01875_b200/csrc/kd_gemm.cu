@@ -1,8 +1,8 @@
 // kd_gemm.cu — tcgen05 GEMM for the backward products of the KD hot path (sm_100a).
 //
-//   dL/dh_s = G · W_s        ("backward passes"):  A = G [tokens, V] (K-major, K = V),
+//   dL/dh_s = G · W_s        ("backward passes"):  A = G [tokens, V], stored as Gᵀ [V][tokens] (MN-major),
 //                                                         B = W_s [V, d_s]   (MN-major: d_s contiguous)
-//   dL/dW_s = Gᵀ · H_s                                   A = G [tokens, V] read as [V, tokens] (MN-major),
+//   dL/dW_s = Gᵀ · H_s                                   A = Gᵀ [V][tokens] (K-major, K = tokens),
 //                                                         B = H_s [tokens, d_s] (MN-major)
 // G arrives as a split-bf16 pair (hi + lo, R11), so A is NUM_A = 2 planes that share every B
 // tile: D += A_hi·Bᵀ + A_lo·Bᵀ  — one B load feeds two MMAs.
@@ -238,8 +238,8 @@ cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, const CUtensor
   KD_GEMM_CASE(false, true, 1, EPI_STORE)
   KD_GEMM_CASE(true, false, 1, EPI_STORE)
   KD_GEMM_CASE(true, true, 1, EPI_STORE)
-  KD_GEMM_CASE(false, true, 2, EPI_STORE)   // dh = [G_hi|G_lo] · W_s
-  KD_GEMM_CASE(true, true, 2, EPI_ACCUM)    // dW += [G_hi|G_lo]ᵀ · H_s
+  KD_GEMM_CASE(true, true, 2, EPI_STORE)    // dh = [G_hi|G_lo] · W_s    (scratch holds Gᵀ: A MN-major)
+  KD_GEMM_CASE(false, true, 2, EPI_ACCUM)   // dW += [G_hi|G_lo]ᵀ · H_s  (Gᵀ: A K-major)
   KD_GEMM_CASE(true, true, 1, EPI_ACCUM)
 #undef KD_GEMM_CASE
   return cudaErrorNotSupported;

@@ -324,14 +324,16 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 jj[i & 1] += ok ? fabsf(d) : 0.f;
               }
             }
-            const size_t off = (size_t)r_local * p.g_ld + v0;
+            // G is stored transposed, Gᵀ [g_ld][n_rows]: for a fixed vocab column the warp's 32 rows are contiguous,
+            // so every store instruction writes one coalesced 64 B (bf16) / 128 B (fp32) segment.
+            const size_t col0 = (size_t)v0 * p.n_rows + r_local;
             if (KIND == KIND_FKL || KIND == KIND_RKL) {
               uint32_t hi[16], lo[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 split2(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
                 // exact residual of the split (hi + lo is exact in fp32, the subtraction is exact too);
-                // kept for the largest entries only, added back by k_corr_dh (2^-18 -> exact on those)
+                // kept for the largest entries only, added back by k_reduce_dh (2^-18 -> exact on those)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   const float gv = g[2 * i + h];
@@ -346,22 +348,22 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                   }
                 }
               }
-              uint8_t* ph = reinterpret_cast<uint8_t*>(p.g_hi + off);
-              uint8_t* pl = reinterpret_cast<uint8_t*>(p.g_lo + off);
+              __nv_bfloat16* ph = p.g_hi + col0;
+              __nv_bfloat16* pl = p.g_lo + col0;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                st_global_v4(ph + 16 * i, hi[4 * i], hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
-                st_global_v4(pl + 16 * i, lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+              for (int i = 0; i < 16; ++i) {
+                st_global_b16(ph + (size_t)(2 * i) * p.n_rows, (uint16_t)(hi[i] & 0xFFFFu));
+                st_global_b16(ph + (size_t)(2 * i + 1) * p.n_rows, (uint16_t)(hi[i] >> 16));
+                st_global_b16(pl + (size_t)(2 * i) * p.n_rows, (uint16_t)(lo[i] & 0xFFFFu));
+                st_global_b16(pl + (size_t)(2 * i + 1) * p.n_rows, (uint16_t)(lo[i] >> 16));
               }
             } else {
-              float* pa = p.g_a + off;
-              float* pb = p.g_b + off;
+              float* pa = p.g_a + col0;
+              float* pb = p.g_b + col0;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                st_global_v4(pa + 4 * i, __float_as_uint(g[4 * i]), __float_as_uint(g[4 * i + 1]),
-                             __float_as_uint(g[4 * i + 2]), __float_as_uint(g[4 * i + 3]));
-                st_global_v4(pb + 4 * i, __float_as_uint(gb[4 * i]), __float_as_uint(gb[4 * i + 1]),
-                             __float_as_uint(gb[4 * i + 2]), __float_as_uint(gb[4 * i + 3]));
+              for (int i = 0; i < 32; ++i) {
+                pa[(size_t)i * p.n_rows] = g[i];
+                pb[(size_t)i * p.n_rows] = gb[i];
               }
               kahan_add(Kacc, cK, kk[0] + kk[1]);
               kahan_add(Jacc, cJ, jj[0] + jj[1]);
