@@ -47,6 +47,7 @@ using namespace kd;
 // ------------------------------------------------------------------------------------ errors
 static thread_local std::string g_err = "ok";
 static thread_local int g_launches = 0;
+static void* g_dbg_ptr = nullptr;  // device buffer for KD_EPI_TIMING builds (kd_debug_set_buffer)
 
 static kd_status fail(kd_status st, const char* fmt, ...) {
   char buf[512];
@@ -146,6 +147,11 @@ static int pass_bn() {  // KD_PASS_BN=128 selects 128-wide vocab tiles (A/B expe
     return (e && atoi(e) == 128) ? 128 : 256;
   }();
   return v;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 static int device_sms() {
@@ -272,17 +278,17 @@ static Plan make_plan(const kd_problem* p) {
   P.off_idx = take((size_t)P.N * 4);
   P.off_ht = take((size_t)P.N * P.d_t * 2);
   P.off_hs = take((size_t)P.N * P.d_s * 2);
-  P.off_part = take((size_t)5 * P.n_split * kEpiHalves * P.Nc * 4);
+  P.off_part = take((size_t)5 * P.n_split * epi_parts(1, P.kind) * P.Nc * 4);
   P.off_fstats = take((size_t)5 * P.Nc * 4);
-  P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * kEpiHalves * P.Nc * 4 : 0);
+  P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * epi_parts(2, P.kind) * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
   P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
   P.off_glo = take((size_t)P.Nc * P.g_ld * 2);
   P.off_ga = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_gb = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
-  P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * kEpiHalves * kCorrSlots * P.Nc * 4);
-  P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * kEpiHalves * kCorrSlots * P.Nc * 4);
+  P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
+  P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
   P.total = o;
   return P;
 }
@@ -355,7 +361,7 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.n_split = P.n_split;
   pp.alpha = (float)(1.4426950408889634 / (double)p->temperature);
   pp.part = ws_at<float>(c.ws, P.off_part);
-  pp.part_plane = (long long)P.n_split * kEpiHalves * P.Nc;
+  pp.part_plane = (long long)P.n_split * epi_parts(1, P.kind) * P.Nc;
   pp.fstats = ws_at<float>(c.ws, P.off_fstats);
   const double cscale = (double)p->loss_scale / (double)p->temperature;
   pp.gscale = (float)(p->kind == KD_RKL ? cscale * 0.6931471805599453 : cscale);
@@ -368,6 +374,9 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.kpart = P.fix ? ws_at<float>(c.ws, P.off_kpart) : nullptr;
   pp.corr_v = P.fix ? nullptr : ws_at<int>(c.ws, P.off_corr_v);
   pp.corr_r = P.fix ? nullptr : ws_at<float>(c.ws, P.off_corr_r);
+  pp.dbg = reinterpret_cast<unsigned long long*>(g_dbg_ptr);
+  static const int l2_hints = env_int("KD_L2_HINTS", 0);  // measured neutral-to-negative (profiles/r01_ncu_pass_pair256.md)
+  pp.l2_hints = l2_hints;
   return pp;
 }
 
@@ -389,7 +398,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
                                                  : 0.5 * cscale);
-    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
+    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
                           pp.g_hi, pp.g_lo, P.num_sms, c.s));
   }
@@ -419,7 +428,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   }
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                                           P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
-                                          P.n_split * kEpiHalves * kCorrSlots, c.Ws, c.s));
+                                          P.n_split * epi_parts(2, P.kind) * kCorrSlots, c.Ws, c.s));
   if (dW) {
     CUtensorMap ma_hi, ma_lo, mh;
     // dW_s += Gᵀ · H_s: A = Gᵀ [g_ld][Nc] is K-major (K = tokens), B = H_s chunk MN-major
@@ -499,7 +508,7 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
-    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, P.kind, 0,
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
   }
@@ -531,7 +540,7 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
-    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * kEpiHalves, P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
                            nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, c.s));
   }
   return KD_OK;
@@ -610,6 +619,9 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
 }
 
 int32_t kd_last_launch_count(void) { return g_launches; }
+
+// Undocumented debug hook (not in kdfused.h): device buffer the KD_EPI_TIMING build accumulates into.
+void kd_debug_set_buffer(void* p) { g_dbg_ptr = p; }
 
 int32_t kd_profile_enable(int32_t on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);

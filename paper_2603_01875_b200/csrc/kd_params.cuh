@@ -11,11 +11,13 @@ constexpr int kBM = 128;        // token rows per tile (UMMA M, one TMEM lane pe
 constexpr int kBN = 128;        // vocab columns per tile in the fused passes
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kPassStages = 6;  // smem ring depth of the fused passes (6 x 32 KB)
-constexpr int kEpiWarps = 8;   // fused-pass epilogue: 2 warps per TMEM lane quarter, each owning half the columns
-constexpr int kEpiHalves = kEpiWarps / 4;
-constexpr int kPassThreads = 128 + 32 * kEpiWarps;  // warps 0-3: TMA / MMA / TMEM alloc / idle; 4..: epilogue
-// Per token row, each (vocab split, column half) writes its own partial record / K-J partial / residual slots:
-// "record slots" = n_split * kEpiHalves, merged downstream in a fixed order.
+// Fused-pass epilogue: kEpiParts warps per TMEM lane quarter, each owning a contiguous part of the tile's columns.
+// FKL/RKL (and every pass 1) use 3 parts (12 warps, <= 128 registers); JSD/TVD pass 2 needs more registers and uses 2.
+constexpr int kEpiPartsMax = 3;
+__host__ __device__ constexpr int epi_parts(int pass, int kind) { return (pass == 2 && kind >= 2) ? 2 : 3; }
+__host__ __device__ constexpr int pass_threads(int parts) { return 128 + 32 * 4 * parts; }  // warps 0-3: TMA/MMA/alloc/idle
+// Per token row, each (vocab split, column part) writes its own partial record / K-J partial / residual slots:
+// "record slots" = n_split * parts, merged downstream in a fixed order.
 constexpr int kCorrSlots = 2;              // residual slots per (token row, vocab split)
 constexpr float kCorrThresh = 7.8125e-3f;  // 2^-7: below it the split residual (< 2^-25·|W|) is negligible
 
@@ -30,7 +32,7 @@ struct PassParams {
   int V_r;            // local vocabulary rows
   int n_split;
   float alpha;        // log2(e) / T
-  // pass 1 output: partial records, plane f at part + f*part_plane, index (split*kEpiHalves + half)*n_rows + r
+  // pass 1 output: partial records, plane f at part + f*part_plane, index (split*parts + part)*n_rows + r
   float* part;
   long long part_plane;
   // pass 2 inputs/outputs
@@ -42,11 +44,13 @@ struct PassParams {
   float* g_a;           // JSD/TVD: [g_ld][n_rows] fp32 planes
   float* g_b;
   int g_ld;             // vocab rows of the scratch: multiple of 64, >= V_r
-  float* kpart;         // JSD/TVD: [2][n_split*kEpiHalves][n_rows] per-(unit, half) partial (K, J)
+  float* kpart;         // JSD/TVD: [2][n_split*parts][n_rows] per-(unit, part) partial (K, J)
   // FKL/RKL split-bf16 residual fix: per (split, slot, row) the vocab index and exact residual
-  // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split*kEpiHalves][kCorrSlots])
+  // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split*parts][kCorrSlots])
   int* corr_v;
   float* corr_r;
+  int l2_hints;         // 1: TMA loads of H evict_last, of W evict_first; G stores evict_first
+  unsigned long long* dbg;  // KD_EPI_TIMING builds only: epilogue cycle counters (see kd_pass.cu)
 };
 
 // Generic bf16 GEMM with fp32 TMEM accumulation: D[M, N] = sum_{a < NUM_A} A_a[M, K] * B[N, K]^T.

@@ -18,6 +18,8 @@
 // Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM allocator,
 // warps 4..7 = epilogue (thread i of warp 4+j owns token row 32j + i = TMEM lane 32j + i).
 // TMEM: 2 accumulator buffers × (teacher 128 cols + student 128 cols) = 512 columns.
+#include <utility>
+
 #include "kd_params.cuh"
 #include "sm100.cuh"
 
@@ -26,6 +28,16 @@
 #endif
 
 namespace kd {
+
+// Compile-time unrolled loop over i = 0..31 (the element index must be a constant for exp2_pair<i>).
+template <int N = 32, typename F, int... Is>
+__device__ __forceinline__ void kd_unroll_impl(F&& f, std::integer_sequence<int, Is...>) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <typename F>
+__device__ __forceinline__ void kd_unroll32(F&& f) {
+  kd_unroll_impl(f, std::make_integer_sequence<int, 32>{});
+}
 
 constexpr int kTileBytes = kBM * kBK * 2;  // 16 KB: one 128x64 bf16 tile (A or B)
 
@@ -57,8 +69,8 @@ __device__ __forceinline__ UnitRange unit_range(int u, int m_tiles, int n_split,
   return r;
 }
 
-template <int PASS, int KIND, int CG, int BN>
-__global__ void __launch_bounds__(kPassThreads, 1)
+template <int PASS, int KIND, int CG, int BN, int EP = epi_parts(PASS, KIND)>
+__global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
                    const PassParams p) {
@@ -94,7 +106,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     }
     for (int b = 0; b < kNB; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps * CG);  // one arrival per epilogue warp of every CTA in the group
+      mbar_init(&tempty[b], 4 * EP * CG);  // one arrival per epilogue warp of every CTA in the group
     }
     fence_barrier_init();
   }
@@ -133,7 +145,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
             const CUtensorMap* ma = tch ? &tm_ht : &tm_hs;
             const CUtensorMap* mb = tch ? &tm_wt : &tm_ws;
-            if (CG == 2) {
+            if (CG == 2 && p.l2_hints) {
+              // the hidden chunk (~50 MB) is re-read for every vocab tile: keep it; the heads stream through
+              tma_load_2d_pair_hint(ma, &full[st], sA + st * C::kABytes, k, row, kEvictLast);
+              tma_load_2d_pair_hint(mb, &full[st], sB + st * C::kBBytes, k, vrow, kEvictFirst);
+            } else if (CG == 2) {
               tma_load_2d_pair(ma, &full[st], sA + st * C::kABytes, k, row);
               tma_load_2d_pair(mb, &full[st], sB + st * C::kBBytes, k, vrow);
             } else {
@@ -153,28 +169,41 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
         const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
+#ifdef KD_EPI_TIMING
+        const long long m0 = clock64();
+        long long mfull = 0;
+#endif
         mbar_wait(&tempty[buf], tph ^ 1);
         tc_fence_after();
+#ifdef KD_EPI_TIMING
+        const long long m1 = clock64();
+#endif
         const uint32_t d_t = tmem_base + buf * (2 * BN);
         const uint32_t d_s = d_t + BN;
         for (int kb = 0; kb < p.kb_t + p.kb_s; ++kb, ++kit) {
           const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
+#ifdef KD_EPI_TIMING
+          const long long f0 = clock64();
+#endif
           mbar_wait(&full[st], ph);
+#ifdef KD_EPI_TIMING
+          mfull += clock64() - f0;
+#endif
           tc_fence_after();
           if (lane == 0) {
             const bool teacher = kb < p.kb_t;
             const int kb0 = teacher ? kb : kb - p.kb_t;
             const uint32_t d = teacher ? d_t : d_s;
-            const uint32_t a_addr = smem_u32(sA + st * C::kABytes);
-            const uint32_t b_addr = smem_u32(sB + st * C::kBBytes);
-            // K=16 sub-steps also last-to-first: with the reversed K-block order the hidden column 0 (the
-            // recipe's large bias column) then enters the accumulator in the very last MMA of the tile.
+            // descriptors of the stage's tiles, advanced along K by adding (32 B >> 4) to the start-address field
+            const uint64_t a_desc = sdesc_sw128(smem_u32(sA + st * C::kABytes), 16, 1024);
+            const uint64_t b_desc = sdesc_sw128(smem_u32(sB + st * C::kBBytes), 16, 1024);
+            // K=16 sub-steps last-to-first: with the reversed K-block order the hidden column 0 (the recipe's large
+            // bias column) then enters the accumulator in the very last MMA of the tile.
 #pragma unroll
             for (int j = 0; j < kBK / 16; ++j) {
-              const int k = KD_SUBSTEP_REVERSE ? kBK / 16 - 1 - j : j;
-              const uint64_t ad = sdesc_sw128(a_addr + k * 32, 16, 1024), bd = sdesc_sw128(b_addr + k * 32, 16, 1024);
-              if (CG == 2) umma_bf16_pair(d, ad, bd, idesc, (kb0 | j) != 0);
-              else umma_bf16(d, ad, bd, idesc, (kb0 | j) != 0);
+              const uint64_t koff = (uint64_t)(2 * (kBK / 16 - 1 - j));
+              if (CG == 2) umma_bf16_pair(d, a_desc + koff, b_desc + koff, idesc, (kb0 | j) != 0);
+              else umma_bf16(d, a_desc + koff, b_desc + koff, idesc, (kb0 | j) != 0);
             }
             if (CG == 2) {  // stage consumed in both CTAs; at tile end the accumulator is ready in both TMEMs
               umma_commit_pair(&empty[st], 0x3);
@@ -186,12 +215,21 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           }
           __syncwarp();
         }
+#ifdef KD_EPI_TIMING
+        if (p.dbg && lane == 0) {  // MMA warp: [wait tempty, wait full (sum), issue span], tiles
+          unsigned long long* d = p.dbg + 2ull * 148 * 16 * 4 + (((size_t)(PASS - 1) * gridDim.x + blockIdx.x) * 4);
+          d[0] += (unsigned long long)(m1 - m0);
+          d[1] += (unsigned long long)mfull;
+          d[2] += (unsigned long long)(clock64() - m1);
+          d[3] += 1ull;
+        }
+#endif
       }
     }
   } else if (warp >= 4) {
     // ================================================================ epilogue (one token row per thread)
     const uint32_t q4 = (warp - 4) & 3;             // TMEM lane quarter (warp w may only touch lanes 32(w%4)..)
-    const int half = (warp - 4) >> 2;               // which half of the tile's columns this warp owns
+    const int part = (warp - 4) >> 2;               // which part of the tile's columns this warp owns
     const int r_in_tile = q4 * 32 + lane;
     const uint32_t lane_addr = (q4 * 32) << 16;
     const float alpha = p.alpha;
@@ -203,7 +241,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;  // row within the chunk
       const bool row_ok = r_local < valid_rows;
       const int split = u / m_tiles;
-      const int rslot = split * kEpiHalves + half;  // this thread's record slot
+      const int rslot = split * EP + part;  // this thread's record slot
       // per-row state
       // pass 1 running record; S_p, S_q, U are Kahan-compensated at chunk granularity: S_p ≈ 1 + Σ(tiny) for a
       // peaked row, and plain fp32 adds of ~4700 small chunk sums onto ~1 lose ~1e-6 relative — exactly the
@@ -229,18 +267,37 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         iSt = exp2f(-lSt);
         iSs = exp2f(-lSs);
       }
+      // pass 2 FKL/RKL per-row constants: (gscale·2^-log2 S_t, gscale·2^-log2 S_s) — equal for equal statistics,
+      // so g = gscale·(q − p) stays exactly 0 when teacher and student agree; RKL's log-ratio offset
+      const float2 negM2 = make_float2(-Mt2, -Ms2);
+      const float2 cTS = make_float2(__fmul_rn(iSt, p.gscale), __fmul_rn(iSs, p.gscale));
+      const float dlr = (lSs - lSt) + ell2;
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
         const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
+#ifdef KD_EPI_TIMING
+        const long long tw0 = clock64();
+#endif
         mbar_wait(&tfull[buf], tph);
         tc_fence_after();
+#ifdef KD_EPI_TIMING
+        long long tld = 0;
+        const long long tw1 = clock64();
+#endif
         const uint32_t t_addr = tmem_base + lane_addr + buf * (2 * BN);
         const int vbase = vt * BN;
-        constexpr int kChunks = BN / 32 / kEpiHalves;  // 32-column chunks per warp
+        constexpr int kChunks = BN / 32;  // 32-column chunks per tile, split over the EP parts
+        const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
 #pragma unroll 1
-        for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
+        for (int c = c_beg; c < c_end; ++c) {
           float zt[32], zs[32];
+#ifdef KD_EPI_TIMING
+          const long long tl0 = clock64();
+#endif
           tmem_ld32x2_sync(t_addr + c * 32, t_addr + BN + c * 32, zt, zs);
-          if (c == (half + 1) * kChunks - 1) {  // this warp's part drained -> release toward the MMA warp
+#ifdef KD_EPI_TIMING
+          tld += clock64() - tl0;
+#endif
+          if (c == c_end - 1) {  // this warp's part drained -> release toward the MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -276,74 +333,71 @@ __global__ void __launch_bounds__(kPassThreads, 1)
               cSq = 0.f;
               Mp = nMp; Mq = nMq;
             }
-            float sp[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f}, uu[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float xp = fmaf(zp[i], alpha, -Mp);
-              const float xq = fmaf(zq[i], alpha, -Mq);
-              const float e = ex2(xp);
-              sp[i & 3] += e;
-              sq[i & 3] += ex2(xq);
-              uu[i & 3] = fmaf(e, xp - xq, uu[i & 3]);
-            }
-            kahan_add(Sp, cSp, (sp[0] + sp[1]) + (sp[2] + sp[3]));
-            kahan_add(Sq, cSq, (sq[0] + sq[1]) + (sq[2] + sq[3]));
+            // packed (p, q) lanes: one FFMA2 / FADD2 per element; every KD_EXP_EMU_STRIDE-th element's two exp2
+            // are evaluated on the FMA pipe (exp2_pair) to unload MUFU
+            const float2 a2 = make_float2(alpha, alpha), nm2 = make_float2(-Mp, -Mq);
+            float2 s2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float uu[4] = {0.f, 0.f, 0.f, 0.f};
+            kd_unroll32([&](auto I) {
+              constexpr int i = decltype(I)::value;
+              const float2 x = ffma2(make_float2(zp[i], zq[i]), a2, nm2);
+              const float2 e = exp2_pair<i>(x);
+              s2[i & 3] = fadd2(s2[i & 3], e);
+              uu[i & 3] = fmaf(e.x, x.x - x.y, uu[i & 3]);
+            });
+            const float2 s01 = fadd2(s2[0], s2[1]), s23 = fadd2(s2[2], s2[3]);
+            kahan_add(Sp, cSp, s01.x + s23.x);
+            kahan_add(Sq, cSq, s01.y + s23.y);
             kahan_add(U, cU, (uu[0] + uu[1]) + (uu[2] + uu[3]));
           } else {
             // ------------------------------------------------ pass 2: logit gradient
             if (v0 >= p.g_ld) continue;  // beyond the scratch row (only in the last tile)
-            float g[32], gb[32];
-            float kk[2] = {0.f, 0.f}, jj[2] = {0.f, 0.f};
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float ut = fmaf(zt[i], alpha, -Mt2), us = fmaf(zs[i], alpha, -Ms2);
-              // __fmul_rn: no FMA contraction into q − p (keeps q − p exactly 0 when the logits agree)
-              const float pt = __fmul_rn(ex2(ut), iSt), qs = __fmul_rn(ex2(us), iSs);
-              const float xt = ut - lSt;  // log2 p   (only the RKL / JSD terms use the logs)
-              const float xs = us - lSs;  // log2 q
-              const bool ok = row_ok && (i < nvalid);
-              if (KIND == KIND_FKL) {
-                g[i] = ok ? p.gscale * (qs - pt) : 0.f;
-              } else if (KIND == KIND_RKL) {
-                g[i] = ok ? p.gscale * qs * ((xs - xt) - ell2) : 0.f;
-              } else if (KIND == KIND_JSD) {
-                const float m = fmaxf(fmaf(p.beta, pt, (1.f - p.beta) * qs), 1.17549435e-38f);
-                const float lm = lg2(m);
-                const float lv = xs - lm;  // log2(q/m)
-                const float a = qs * lv;
-                g[i] = ok ? a : 0.f;
-                gb[i] = ok ? qs : 0.f;
-                kk[i & 1] += ok ? a : 0.f;
-                jj[i & 1] += ok ? pt * (xt - lm) : 0.f;
-              } else {  // TVD
-                const float d = qs - pt;
-                const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-                g[i] = ok ? qs * sgn : 0.f;
-                gb[i] = ok ? qs : 0.f;
-                kk[i & 1] += ok ? qs * sgn : 0.f;
-                jj[i & 1] += ok ? fabsf(d) : 0.f;
-              }
-            }
-            // G is stored transposed, Gᵀ [g_ld][n_rows]: for a fixed vocab column the warp's 32 rows are contiguous,
-            // so every store instruction writes one coalesced 64 B (bf16) / 128 B (fp32) segment.
+            // Gᵀ [g_ld][n_rows]: for a fixed vocab column the warp's 32 rows are contiguous (coalesced stores)
             const size_t col0 = (size_t)v0 * p.n_rows + r_local;
             if (KIND == KIND_FKL || KIND == KIND_RKL) {
+              float g[32];
+              if (row_ok && nvalid == 32) {
+                // fast path (every chunk but the vocab tail and the rows past the chunk end): packed fp32x2
+                // math on (teacher, student) pairs, normalisation + loss scale folded into per-row constants
+                kd_unroll32([&](auto I) {
+                  constexpr int i = decltype(I)::value;
+                  const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
+                  const float2 e = fmul2(exp2_pair<i>(u), cTS);  // (gscale·p, gscale·q) rounded
+                  if (KIND == KIND_FKL) g[i] = e.y - e.x;
+                  else g[i] = e.y * ((u.y - u.x) - dlr);  // gscale·q·(log2(q/p) − RKL/ln2)
+                });
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const bool ok = row_ok && (i < nvalid);
+                  const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
+                  const float2 e = fmul2(make_float2(ex2(u.x), ex2(u.y)), cTS);
+                  const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr);
+                  g[i] = ok ? gi : 0.f;
+                }
+              }
               uint32_t hi[16], lo[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                split2(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
-                // exact residual of the split (hi + lo is exact in fp32, the subtraction is exact too);
-                // kept for the largest entries only, added back by k_reduce_dh (2^-18 -> exact on those)
+              for (int i = 0; i < 16; ++i) split2_fast(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
+              // exact residuals of the split for the largest entries (added back by k_reduce_dh); the per-chunk
+              // max gates the bookkeeping so typical chunks pay ~0.5 instruction per element
+              float amax = 0.f;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const float gv = g[2 * i + h];
-                  if (fabsf(gv) > kCorrThresh) {
-                    const float rep = h ? bf16hi_to_f32(hi[i]) + bf16hi_to_f32(lo[i])
-                                        : bf16lo_to_f32(hi[i]) + bf16lo_to_f32(lo[i]);
-                    const float rr = gv - rep;
-                    if (fabsf(rr) > fabsf(cr1)) {
-                      if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
-                      else { cr1 = rr; cv1 = v0 + 2 * i + h; }
+              for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(g[i]));
+              if (amax > kCorrThresh) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    const float gv = g[2 * i + h];
+                    if (fabsf(gv) > kCorrThresh) {
+                      const float rep = h ? bf16hi_to_f32(hi[i]) + bf16hi_to_f32(lo[i])
+                                          : bf16lo_to_f32(hi[i]) + bf16lo_to_f32(lo[i]);
+                      const float rr = gv - rep;
+                      if (fabsf(rr) > fabsf(cr1)) {
+                        if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
+                        else { cr1 = rr; cv1 = v0 + 2 * i + h; }
+                      }
                     }
                   }
                 }
@@ -352,12 +406,43 @@ __global__ void __launch_bounds__(kPassThreads, 1)
               __nv_bfloat16* pl = p.g_lo + col0;
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                st_global_b16(ph + (size_t)(2 * i) * p.n_rows, (uint16_t)(hi[i] & 0xFFFFu));
-                st_global_b16(ph + (size_t)(2 * i + 1) * p.n_rows, (uint16_t)(hi[i] >> 16));
-                st_global_b16(pl + (size_t)(2 * i) * p.n_rows, (uint16_t)(lo[i] & 0xFFFFu));
-                st_global_b16(pl + (size_t)(2 * i + 1) * p.n_rows, (uint16_t)(lo[i] >> 16));
+                st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
+                st_global_b16(pl, (uint16_t)(lo[i] & 0xFFFFu));
+                ph += p.n_rows;
+                pl += p.n_rows;
+                st_global_b16(ph, (uint16_t)(hi[i] >> 16));
+                st_global_b16(pl, (uint16_t)(lo[i] >> 16));
+                ph += p.n_rows;
+                pl += p.n_rows;
               }
             } else {
+              float g[32], gb[32];
+              float kk[2] = {0.f, 0.f}, jj[2] = {0.f, 0.f};
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float ut = fmaf(zt[i], alpha, -Mt2), us = fmaf(zs[i], alpha, -Ms2);
+                const float pt = __fmul_rn(ex2(ut), iSt), qs = __fmul_rn(ex2(us), iSs);
+                const float xt = ut - lSt;  // log2 p
+                const float xs = us - lSs;  // log2 q
+                const bool ok = row_ok && (i < nvalid);
+                if (KIND == KIND_JSD) {
+                  const float m = fmaxf(fmaf(p.beta, pt, (1.f - p.beta) * qs), 1.17549435e-38f);
+                  const float lm = lg2(m);
+                  const float lv = xs - lm;  // log2(q/m)
+                  const float a = qs * lv;
+                  g[i] = ok ? a : 0.f;
+                  gb[i] = ok ? qs : 0.f;
+                  kk[i & 1] += ok ? a : 0.f;
+                  jj[i & 1] += ok ? pt * (xt - lm) : 0.f;
+                } else {  // TVD
+                  const float d = qs - pt;
+                  const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+                  g[i] = ok ? qs * sgn : 0.f;
+                  gb[i] = ok ? qs : 0.f;
+                  kk[i & 1] += ok ? qs * sgn : 0.f;
+                  jj[i & 1] += ok ? fabsf(d) : 0.f;
+                }
+              }
               float* pa = p.g_a + col0;
               float* pb = p.g_b + col0;
 #pragma unroll
@@ -370,6 +455,16 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             }
           }
         }
+#ifdef KD_EPI_TIMING
+        if (p.dbg && lane == 0) {  // per warp: [wait for MMA, TMEM loads, total epilogue] cycles, tile count
+          const long long tw2 = clock64();
+          unsigned long long* d = p.dbg + (((size_t)(PASS - 1) * gridDim.x + blockIdx.x) * 16 + (warp - 4)) * 4;
+          d[0] += (unsigned long long)(tw1 - tw0);
+          d[1] += (unsigned long long)tld;
+          d[2] += (unsigned long long)(tw2 - tw1);
+          d[3] += 1ull;
+        }
+#endif
       }
       // ---- unit done: emit per-row partials (rows inside the chunk's valid range only)
       if (row_ok) {
@@ -381,11 +476,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           p.part[3 * p.part_plane + idx] = Sq - cSq;
           p.part[4 * p.part_plane + idx] = U - cU;
         } else if (KIND == KIND_JSD || KIND == KIND_TVD) {
-          const size_t plane = (size_t)p.n_split * kEpiHalves * p.n_rows;
+          const size_t plane = (size_t)p.n_split * EP * p.n_rows;
           p.kpart[idx] = Kacc - cK;
           p.kpart[plane + idx] = Jacc - cJ;
         } else {
-          const size_t c0 = ((size_t)r_local * p.n_split * kEpiHalves + rslot) * kCorrSlots;
+          const size_t c0 = ((size_t)r_local * p.n_split * EP + rslot) * kCorrSlots;
           p.corr_v[c0] = cv0;
           p.corr_r[c0] = cr0;
           p.corr_v[c0 + 1] = cv1;
@@ -413,7 +508,7 @@ static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, i
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kPassThreads);
+  cfg.blockDim = dim3(pass_threads(epi_parts(PASS, KIND)));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

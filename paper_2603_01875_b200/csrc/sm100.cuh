@@ -9,8 +9,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
-#ifndef KD_WATCHDOG_SPINS
-#define KD_WATCHDOG_SPINS (1u << 28)  // ~seconds of spinning: a protocol bug traps instead of hanging
+#ifndef KD_WATCHDOG_CYCLES
+#define KD_WATCHDOG_CYCLES (1ll << 35)  // ~20 s of waiting on one barrier: a protocol bug traps instead of hanging
 #endif
 
 namespace kd {
@@ -47,6 +47,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef KD_WAIT_BACKOFF_NS
+#define KD_WAIT_BACKOFF_NS 0  // >0: after 32 fast polls, sleep this long between polls (A/B knob)
+#endif
+// Plain polling try_wait.  (A suspend-time hint was measured slower: the wake-up latency lands on the
+// MMA -> epilogue -> MMA critical path of the single-buffered TMEM tile.)
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -60,9 +65,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  uint32_t spins = 0;
+  if (mbar_try_wait(addr, parity)) return;
+  const long long t0 = clock64();
+  uint32_t polls = 0;
   while (!mbar_try_wait(addr, parity)) {
-    if (++spins > KD_WATCHDOG_SPINS) __trap();
+    if (KD_WAIT_BACKOFF_NS > 0 && ++polls > 32) __nanosleep(KD_WAIT_BACKOFF_NS);
+    if (clock64() - t0 > KD_WATCHDOG_CYCLES) __trap();  // protocol bug: fail loudly instead of hanging the GPU
   }
 }
 
@@ -146,6 +154,14 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
       "[%2];" ::"r"(smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(const CUtensorMap* map, uint64_t* bar, void* smem, int x, int y,
+                                                      uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(x), "r"(y), "l"(hint)
       : "memory");
 }
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
@@ -272,8 +288,98 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
   lo = pack_bf16x2(a - bf16lo_to_f32(hi), b - bf16hi_to_f32(hi));
 }
 
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FMUL2 — two lanes per issue slot), round-to-nearest.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+#ifndef KD_EXP_EMU_STRIDE
+#define KD_EXP_EMU_STRIDE 4  // every k-th element's two exp2 on the FMA pipe (0 = all on MUFU); A/B'd, DESIGN.md
+#endif
+// 2^x for both lanes on the FMA/ALU pipes (x <= 0): x = n + f, n = rint(x) via the 1.5·2^23 trick, 2^f by a
+// degree-5 polynomial on [-1/2, 1/2] (max rel. error 1.9e-7 < ex2.approx's 2^-22; exact at x = 0), 2^n added to
+// the exponent field.  Balances the MUFU (XU) pipe that bounds the fused-pass epilogue.
+__device__ __forceinline__ float2 exp2_emu2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(1.3268215116113424e-3f, 1.3268215116113424e-3f), f,
+                   make_float2(9.671511128544807e-3f, 9.671511128544807e-3f));
+  p = ffma2(p, f, make_float2(5.550721660256386e-2f, 5.550721660256386e-2f));
+  p = ffma2(p, f, make_float2(2.4022242426872253e-1f, 2.4022242426872253e-1f));
+  p = ffma2(p, f, make_float2(6.931470036506653e-1f, 6.931470036506653e-1f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+template <int I>
+__device__ __forceinline__ float2 exp2_pair(float2 x) {
+  if (KD_EXP_EMU_STRIDE > 0 && I % (KD_EXP_EMU_STRIDE > 0 ? KD_EXP_EMU_STRIDE : 1) == 0) return exp2_emu2(x);
+  return make_float2(ex2(x.x), ex2(x.y));
+}
+
+#ifndef KD_SPLIT_MODE
+#define KD_SPLIT_MODE 0  // 0: hi and lo via F2FP (XU pipe); 1: both via integer RNE (ALU); 2: hi F2FP, lo integer
+#endif
+// Round-to-nearest-even fp32 -> bf16 on the integer pipe: the upper 16 bits of the result are the bf16.
+__device__ __forceinline__ uint32_t rne_bf16_bits(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return b + 0x7FFFu + ((b >> 16) & 1u);
+}
+// Split two fp32 values into bf16 hi + lo planes (pairs packed lo-half first), choosing the pipe by KD_SPLIT_MODE.
+__device__ __forceinline__ void split2_fast(float a, float b, uint32_t& hi, uint32_t& lo) {
+  if (KD_SPLIT_MODE == 0) {
+    split2(a, b, hi, lo);
+  } else {
+    uint32_t ha, hb;
+    if (KD_SPLIT_MODE == 1) {
+      ha = rne_bf16_bits(a) & 0xFFFF0000u;
+      hb = rne_bf16_bits(b) & 0xFFFF0000u;
+      hi = __byte_perm(ha, hb, 0x7632);
+    } else {
+      hi = pack_bf16x2(a, b);
+      ha = hi << 16;
+      hb = hi & 0xFFFF0000u;
+    }
+    const float ra = a - __uint_as_float(ha), rb = b - __uint_as_float(hb);
+    lo = __byte_perm(rne_bf16_bits(ra), rne_bf16_bits(rb), 0x7632);
+  }
+}
+
+
 __device__ __forceinline__ void st_global_b16(void* p, uint16_t v) {
   asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_global_b16_hint(void* p, uint16_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(p), "h"(v), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
