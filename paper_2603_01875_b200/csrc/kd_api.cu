@@ -21,8 +21,8 @@
 #include "kd_params.cuh"
 
 namespace kd {
-cudaError_t launch_pass(int pass, int kind, int cg, int bn, const CUtensorMap* maps, const PassParams& p, int grid,
-                        cudaStream_t s);
+cudaError_t launch_pass(int pass, int kind, bool coupled, int cg, int bn, const CUtensorMap* maps, const PassParams& p,
+                        int grid, cudaStream_t s);
 cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, const CUtensorMap* a0, const CUtensorMap* a1,
                         const CUtensorMap* b, const GemmParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_compact(const uint8_t* mask, int N, int* idx, int* n_eff, cudaStream_t s);
@@ -31,7 +31,10 @@ cudaError_t launch_gather(const __nv_bfloat16* src, long long src_ld, __nv_bfloa
 cudaError_t launch_zero_masked(const uint8_t* mask, int N, float* loss, float* dh, int d_s, cudaStream_t s);
 cudaError_t launch_merge(const float* part, long long plane, long long split_stride, int n_split, int n_rows,
                          int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
-                         long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, cudaStream_t s);
+                         long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, int write_loss,
+                         cudaStream_t s);
+cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, float* loss,
+                             const int* idx, long long* nonfinite, cudaStream_t s);
 cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, int kind, float beta,
                         float* kfin, float* loss, const int* idx, long long* nonfinite, const float* ga,
                         const float* gb, int g_ld, float scale, __nv_bfloat16* ghi, __nv_bfloat16* glo,
@@ -280,7 +283,8 @@ static Plan make_plan(const kd_problem* p) {
   P.off_hs = take((size_t)P.N * P.d_s * 2);
   P.off_part = take((size_t)5 * P.n_split * epi_parts(1, P.kind) * P.Nc * 4);
   P.off_fstats = take((size_t)5 * P.Nc * 4);
-  P.off_kpart = take(P.fix ? (size_t)2 * P.n_split * epi_parts(2, P.kind) * P.Nc * 4 : 0);
+  // JSD/TVD: K and J partials; FKL: the loss partials of pass 2 (plane 0)
+  P.off_kpart = take((P.fix || P.kind == KD_FKL) ? (size_t)2 * P.n_split * epi_parts(2, P.kind) * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
   P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
   P.off_glo = take((size_t)P.Nc * P.g_ld * 2);
@@ -371,7 +375,7 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.g_a = P.fix ? ws_at<float>(c.ws, P.off_ga) : nullptr;
   pp.g_b = P.fix ? ws_at<float>(c.ws, P.off_gb) : nullptr;
   pp.g_ld = P.g_ld;
-  pp.kpart = P.fix ? ws_at<float>(c.ws, P.off_kpart) : nullptr;
+  pp.kpart = (P.fix || P.kind == KD_FKL) ? ws_at<float>(c.ws, P.off_kpart) : nullptr;
   pp.corr_v = P.fix ? nullptr : ws_at<int>(c.ws, P.off_corr_v);
   pp.corr_r = P.fix ? nullptr : ws_at<float>(c.ws, P.off_corr_r);
   pp.dbg = reinterpret_cast<unsigned long long*>(g_dbg_ptr);
@@ -393,7 +397,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
   const int grid = pass_grid(P);
-  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, P.cg, P.bn, c.maps, pp, grid, c.s));
+  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, true, P.cg, P.bn, c.maps, pp, grid, c.s));
   if (P.fix) {
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
@@ -507,10 +511,16 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    // decoupled pass 1 (independent teacher / student LSEs) for FKL/JSD/TVD; RKL needs its loss in pass 2
+    const bool coupled = P.kind == KD_RKL;
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 0,
-                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, c.s));
+                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, coupled ? 1 : 0,
+                           c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
+    if (P.kind == KD_FKL)
+      KD_LAUNCH(K_MERGE, launch_loss_rows(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, row0, c.n_eff, loss, c.idx,
+                                          c.nonfinite, c.s));
   }
   return KD_OK;
 }
@@ -539,9 +549,10 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    // the shard record carries the cross term U (merged across ranks into the loss): coupled pass 1
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, true, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
-                           nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, c.s));
+                           nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, 0, c.s));
   }
   return KD_OK;
 }
@@ -578,7 +589,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
     const int row0 = ch * P.Nc;
     // rank records [n_ranks][5][N] indexed by ORIGINAL row, merged in rank order
     KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
-                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite, c.s));
+                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite, 1, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s_partial, dW)) != KD_OK) return st;
   }
   return KD_OK;

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
                                                      float* __restrict__ fstats, float* __restrict__ loss,
                                                      float* __restrict__ rec, long long rec_plane,
                                                      const int* __restrict__ idx, int orig_rows,
-                                                     long long* __restrict__ nonfinite) {
+                                                     long long* __restrict__ nonfinite, int write_loss) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int valid = min(n_rows, *n_eff - row0);
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
   fstats[2 * n_rows + r] = (float)(rkl ? A.Mp : A.Mq);  // M_s
   fstats[3 * n_rows + r] = rkl ? lp : lq;        // log2 S_s
   fstats[4 * n_rows + r] = ell2;
-  if (kind == KIND_FKL || kind == KIND_RKL) {
+  if (write_loss && (kind == KIND_FKL || kind == KIND_RKL)) {
     const float ell = ell2 * kLn2;
     loss[orow] = ell;
     if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
@@ -321,9 +321,32 @@ cudaError_t launch_zero_masked(const uint8_t* mask, int N, float* loss, float* d
 }
 cudaError_t launch_merge(const float* part, long long plane, long long split_stride, int n_split, int n_rows,
                          int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
-                         long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, cudaStream_t s) {
+                         long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, int write_loss,
+                         cudaStream_t s) {
   k_merge_stats<<<(n_rows + 7) / 8, 256, 0, s>>>(part, plane, split_stride, n_split, n_rows, row0, n_eff, kind,
-                                                      mode, fstats, loss, rec, rec_plane, idx, orig_rows, nonfinite);
+                                                      mode, fstats, loss, rec, rec_plane, idx, orig_rows, nonfinite,
+                                                      write_loss);
+  return cudaGetLastError();
+}
+
+// FKL loss of the decoupled path: ℓ = ln2 · Σ_slots partial (each partial = Σ_v p_v (log2 p_v − log2 q_v) over one
+// (vocab split, column part)), summed in fp64 in fixed slot order.
+__global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ lpart, int n_slots, int n_rows, int row0,
+                                                   const int* __restrict__ n_eff, float* __restrict__ loss,
+                                                   const int* __restrict__ idx, long long* __restrict__ nonfinite) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int valid = min(n_rows, *n_eff - row0);
+  if (r >= valid) return;
+  double acc = 0.0;
+  for (int s = 0; s < n_slots; ++s) acc += (double)lpart[(size_t)s * n_rows + r];
+  const float ell = (float)(acc * 0.6931471805599453);
+  const int orow = idx ? idx[row0 + r] : row0 + r;
+  loss[orow] = ell;
+  if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
+}
+cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, float* loss,
+                             const int* idx, long long* nonfinite, cudaStream_t s) {
+  k_loss_rows<<<(n_rows + 255) / 256, 256, 0, s>>>(lpart, n_slots, n_rows, row0, n_eff, loss, idx, nonfinite);
   return cudaGetLastError();
 }
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s) {

@@ -69,14 +69,19 @@ __device__ __forceinline__ UnitRange unit_range(int u, int m_tiles, int n_split,
   return r;
 }
 
-template <int PASS, int KIND, int CG, int BN, int EP = epi_parts(PASS, KIND)>
+// DEC (pass 1 of FKL/JSD/TVD in kd_fused_fwd_bwd): the teacher and student LSEs are independent, so the two GEMMs
+// of a vocab tile run as separate half-tiles through TWO 256-column accumulators and each half's epilogue overlaps
+// the other half's MMAs (the coupled form keeps both accumulators live and exposes the epilogue).  The FKL loss then
+// comes from pass 2.  RKL (whose gradient needs its loss in pass 2) and the vocab-shard API use the coupled form.
+template <int PASS, int KIND, int CG, int BN, bool DEC = false, int EP = epi_parts(PASS, KIND)>
 __global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
                    const PassParams p) {
   using C = PassCfg<CG, BN>;
   constexpr int kStages = C::kStages;
-  constexpr int kNB = C::kNumBuf;
+  constexpr int kNB = DEC ? 2 * C::kNumBuf : C::kNumBuf;  // accumulator buffers (DEC: one side per buffer)
+  static_assert(!DEC || (PASS == 1 && KIND == KIND_FKL), "DEC is a pass-1 (FKL-role) mode");
   constexpr int kBMt = kBM * CG;  // token rows per work tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -165,6 +170,44 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     // ================================================================ MMA issuer (one thread of the leader)
     constexpr uint32_t idesc = idesc_bf16_f32(kBMt, BN, false, false);
     uint32_t kit = 0, it = 0;
+    if constexpr (DEC) {
+      // one half-tile per accumulator buffer: teacher K blocks, then student K blocks of the same vocab tile
+      for (int u = worker; u < n_units; u += n_workers) {
+        const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
+        for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
+          for (int side = 0; side < 2; ++side, ++it) {
+            const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+            mbar_wait(&tempty[buf], tph ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem_base + buf * BN;
+            const int nkb = side ? p.kb_s : p.kb_t;
+            for (int kb = 0; kb < nkb; ++kb, ++kit) {
+              const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
+              mbar_wait(&full[st], ph);
+              tc_fence_after();
+              if (lane == 0) {
+                const uint64_t a_desc = sdesc_sw128(smem_u32(sA + st * C::kABytes), 16, 1024);
+                const uint64_t b_desc = sdesc_sw128(smem_u32(sB + st * C::kBBytes), 16, 1024);
+#pragma unroll
+                for (int j = 0; j < kBK / 16; ++j) {
+                  const uint64_t koff = (uint64_t)(2 * (kBK / 16 - 1 - j));
+                  if (CG == 2) umma_bf16_pair(d, a_desc + koff, b_desc + koff, idesc, (kb | j) != 0);
+                  else umma_bf16(d, a_desc + koff, b_desc + koff, idesc, (kb | j) != 0);
+                }
+                if (CG == 2) {
+                  umma_commit_pair(&empty[st], 0x3);
+                  if (kb == nkb - 1) umma_commit_pair(&tfull[buf], 0x3);
+                } else {
+                  umma_commit(&empty[st]);
+                  if (kb == nkb - 1) umma_commit(&tfull[buf]);
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+      }
+    } else
     for (int u = worker; u < n_units; u += n_workers) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
@@ -236,6 +279,81 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     // the leader's tempty barrier collects the releases of both CTAs' epilogues
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     uint32_t it = 0;
+    if constexpr (DEC) {
+      constexpr int kChunks = BN / 32;
+      const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
+      for (int u = worker; u < n_units; u += n_workers) {
+        const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
+        const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;
+        const bool row_ok = r_local < valid_rows;
+        const int rslot = (u / m_tiles) * EP + part;
+        float M2[2] = {-INFINITY, -INFINITY}, S2[2] = {0.f, 0.f}, cS2[2] = {0.f, 0.f};  // teacher, student
+        for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
+          for (int side = 0; side < 2; ++side, ++it) {
+            const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+            mbar_wait(&tfull[buf], tph);
+            tc_fence_after();
+            const uint32_t t_addr = tmem_base + lane_addr + buf * BN;
+#pragma unroll 1
+            for (int c = c_beg; c < c_end; ++c) {
+              float z[32];
+              tmem_ld32_sync(t_addr + c * 32, z);
+              if (c == c_end - 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                  if (CG == 2) mbar_arrive_cluster(tempty_leader + buf * 8);
+                  else mbar_arrive(&tempty[buf]);
+                }
+              }
+              const int v0 = vt * BN + c * 32;
+              const int nvalid = min(32, p.V_r - v0);
+              if (nvalid <= 0) continue;
+              if (nvalid < 32) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i >= nvalid) z[i] = -1e30f;
+              }
+              // online base-2 LSE of one side, Kahan-compensated sum (see the coupled path below)
+              float cm = z[0];
+#pragma unroll
+              for (int i = 1; i < 32; ++i) cm = fmaxf(cm, z[i]);
+              float& M = M2[side];
+              float& S = S2[side];
+              float& cS = cS2[side];
+              const float nM = fmaxf(M, cm * alpha);
+              if (S == 0.f) {
+                M = nM;
+              } else if (nM > M) {
+                S = __fmul_rn(exp2f(M - nM), __fsub_rn(S, cS));
+                cS = 0.f;
+                M = nM;
+              }
+              const float2 a2 = make_float2(alpha, alpha), nm2 = make_float2(-M, -M);
+              float2 s2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};
+              kd_unroll32([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                if constexpr (i % 2 == 0) {
+                  const float2 x = ffma2(make_float2(z[i], z[i + 1]), a2, nm2);
+                  s2[(i / 2) & 3] = fadd2(s2[(i / 2) & 3], exp2_pair<i / 2>(x));
+                }
+              });
+              const float2 s01 = fadd2(s2[0], s2[1]), s23 = fadd2(s2[2], s2[3]);
+              kahan_add(S, cS, (s01.x + s01.y) + (s23.x + s23.y));
+            }
+          }
+        }
+        if (row_ok) {
+          const size_t idx = (size_t)rslot * p.n_rows + r_local;
+          p.part[idx] = M2[0];
+          p.part[p.part_plane + idx] = M2[1];
+          p.part[2 * p.part_plane + idx] = S2[0] - cS2[0];
+          p.part[3 * p.part_plane + idx] = S2[1] - cS2[1];
+          p.part[4 * p.part_plane + idx] = 0.f;  // no cross term: the FKL loss is accumulated in pass 2
+        }
+      }
+    } else
     for (int u = worker; u < n_units; u += n_workers) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;  // row within the chunk
@@ -272,6 +390,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       const float2 negM2 = make_float2(-Mt2, -Ms2);
       const float2 cTS = make_float2(__fmul_rn(iSt, p.gscale), __fmul_rn(iSs, p.gscale));
       const float dlr = (lSs - lSt) + ell2;
+      const float dlt = lSt - lSs;          // FKL: log2 p − log2 q = (u_t − u_s) − (log2 S_t − log2 S_s)
+      float Lacc = 0.f, cL = 0.f;           // FKL loss partial (pass 2)
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
         const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
 #ifdef KD_EPI_TIMING
@@ -359,22 +479,34 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (row_ok && nvalid == 32) {
                 // fast path (every chunk but the vocab tail and the rows past the chunk end): packed fp32x2
                 // math on (teacher, student) pairs, normalisation + loss scale folded into per-row constants
+                float la[2] = {0.f, 0.f};
                 kd_unroll32([&](auto I) {
                   constexpr int i = decltype(I)::value;
                   const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
-                  const float2 e = fmul2(exp2_pair<i>(u), cTS);  // (gscale·p, gscale·q) rounded
-                  if (KIND == KIND_FKL) g[i] = e.y - e.x;
-                  else g[i] = e.y * ((u.y - u.x) - dlr);  // gscale·q·(log2(q/p) − RKL/ln2)
+                  const float2 r = exp2_pair<i>(u);
+                  const float2 e = fmul2(r, cTS);  // (gscale·p, gscale·q) rounded
+                  if (KIND == KIND_FKL) {
+                    g[i] = e.y - e.x;
+                    // FKL loss in bits, unnormalised: Σ 2^{u_t} · (log2 p − log2 q); × 2^-log2 S_t at unit end
+                    la[i & 1] = fmaf(r.x, (u.x - u.y) - dlt, la[i & 1]);
+                  } else {
+                    g[i] = e.y * ((u.y - u.x) - dlr);  // gscale·q·(log2(q/p) − RKL/ln2)
+                  }
                 });
+                if (KIND == KIND_FKL) kahan_add(Lacc, cL, la[0] + la[1]);
               } else {
+                float la = 0.f;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   const bool ok = row_ok && (i < nvalid);
                   const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
-                  const float2 e = fmul2(make_float2(ex2(u.x), ex2(u.y)), cTS);
+                  const float2 r = make_float2(ex2(u.x), ex2(u.y));
+                  const float2 e = fmul2(r, cTS);
                   const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr);
                   g[i] = ok ? gi : 0.f;
+                  if (KIND == KIND_FKL && ok) la = fmaf(r.x, (u.x - u.y) - dlt, la);
                 }
+                if (KIND == KIND_FKL) kahan_add(Lacc, cL, la);
               }
               uint32_t hi[16], lo[16];
 #pragma unroll
@@ -480,6 +612,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           p.kpart[idx] = Kacc - cK;
           p.kpart[plane + idx] = Jacc - cJ;
         } else {
+          if (KIND == KIND_FKL && p.kpart) p.kpart[idx] = __fmul_rn(Lacc - cL, iSt);  // FKL loss partial (bits)
           const size_t c0 = ((size_t)r_local * p.n_split * EP + rslot) * kCorrSlots;
           p.corr_v[c0] = cv0;
           p.corr_r[c0] = cr0;
@@ -500,9 +633,9 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 }
 
 // ------------------------------------------------------------------------------- host-side launchers
-template <int PASS, int KIND, int CG, int BN>
+template <int PASS, int KIND, int CG, int BN, bool DEC = false>
 static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t stream) {
-  auto kern = kd_pass_kernel<PASS, KIND, CG, BN>;
+  auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC>;
   const int smem = PassCfg<CG, BN>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -522,12 +655,13 @@ static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, i
 }
 
 template <int CG, int BN>
-static cudaError_t launch_pass_cg(int pass, int kind, const CUtensorMap* maps, const PassParams& p, int grid,
-                                  cudaStream_t stream) {
+static cudaError_t launch_pass_cg(int pass, int kind, bool coupled, const CUtensorMap* maps, const PassParams& p,
+                                  int grid, cudaStream_t stream) {
   if (pass == 1) {
-    // pass 1 only distinguishes which side is "primary" (RKL swaps the roles)
-    return kind == KIND_RKL ? launch_pass_t<1, KIND_RKL, CG, BN>(maps, p, grid, stream)
-                            : launch_pass_t<1, KIND_FKL, CG, BN>(maps, p, grid, stream);
+    // pass 1 only distinguishes which side is "primary" (RKL swaps the roles) and coupled vs decoupled sides
+    if (kind == KIND_RKL) return launch_pass_t<1, KIND_RKL, CG, BN>(maps, p, grid, stream);
+    return coupled ? launch_pass_t<1, KIND_FKL, CG, BN>(maps, p, grid, stream)
+                   : launch_pass_t<1, KIND_FKL, CG, BN, true>(maps, p, grid, stream);
   }
   switch (kind) {
     case KIND_FKL: return launch_pass_t<2, KIND_FKL, CG, BN>(maps, p, grid, stream);
@@ -539,12 +673,13 @@ static cudaError_t launch_pass_cg(int pass, int kind, const CUtensorMap* maps, c
 
 // cg = 1: single-SM tiles (grid = #tile workers); cg = 2: SM pairs (grid = 2 x #pair workers).
 // bn = vocab tile (UMMA N) 128 or 256.  maps: [H_t, W_t, H_s, W_s] with W boxes of bn / cg rows.
-cudaError_t launch_pass(int pass, int kind, int cg, int bn, const CUtensorMap* maps, const PassParams& p, int grid,
-                        cudaStream_t stream) {
-  if (cg == 2) return bn == 256 ? launch_pass_cg<2, 256>(pass, kind, maps, p, grid, stream)
-                                : launch_pass_cg<2, 128>(pass, kind, maps, p, grid, stream);
-  return bn == 256 ? launch_pass_cg<1, 256>(pass, kind, maps, p, grid, stream)
-                   : launch_pass_cg<1, 128>(pass, kind, maps, p, grid, stream);
+// coupled = false selects the decoupled pass 1 for FKL/JSD/TVD (RKL is always coupled).
+cudaError_t launch_pass(int pass, int kind, bool coupled, int cg, int bn, const CUtensorMap* maps, const PassParams& p,
+                        int grid, cudaStream_t stream) {
+  if (cg == 2) return bn == 256 ? launch_pass_cg<2, 256>(pass, kind, coupled, maps, p, grid, stream)
+                                : launch_pass_cg<2, 128>(pass, kind, coupled, maps, p, grid, stream);
+  return bn == 256 ? launch_pass_cg<1, 256>(pass, kind, coupled, maps, p, grid, stream)
+                   : launch_pass_cg<1, 128>(pass, kind, coupled, maps, p, grid, stream);
 }
 
 }  // namespace kd

@@ -61,7 +61,7 @@ def test_workspace_size_host_only():
     # G scratch: chunk 4096 x 151936 x (bf16 hi + lo) dominates; packed hidden copies 0.4 GB
     assert 2.4e9 < n < 6e9
     pj = kd.make_problem(32768, 4096, 2048, 151936, kind="jsd")
-    assert kd.workspace_size(pj) > n + 4096 * 151936 * 8 - (8 << 20)  # + two fp32 G planes
+    assert kd.workspace_size(pj) > n + 0.99 * 4096 * 151936 * 8  # + two fp32 G planes
 
 
 @pytest.mark.parametrize("kw,status", [(dict(T=0.0), 1), (dict(T=float("nan")), 1), (dict(kind=7), 1),
