@@ -41,10 +41,12 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str = OUT) -> str:
+    """defines: extra -D macros for instrumented variants (e.g. ("KD_EPI_TIMING",) -> libkdfused_tim.so, used by
+    scripts/probe_epi.py); the product library is built without any."""
+    if not force and out == OUT and not _stale():
         return OUT
-    bdir = os.path.join(HERE, "_build")
+    bdir = os.path.join(HERE, "_build" + ("_" + "_".join(defines).lower() if defines else ""))
     os.makedirs(bdir, exist_ok=True)
     cc = nvcc()
     objs = []
@@ -52,15 +54,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for s in SOURCES:
         o = os.path.join(bdir, s.replace(".cu", ".o"))
         objs.append(o)
-        cmd = [cc, *flags(verbose), "-c", os.path.join(CSRC, s), "-o", o]
+        cmd = [cc, *flags(verbose), *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", o]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     for cmd, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0:
-            raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{out}")
-        if verbose and out:
-            print(out)
-    tmp = OUT + ".tmp"
+            raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{log}")
+        if verbose and log:
+            print(log)
+    tmp = out + ".tmp"
     link = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcuda"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
@@ -70,9 +72,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    if "--timing" in sys.argv:
+        print(build(force=True, defines=("KD_EPI_TIMING",), out=os.path.join(HERE, "libkdfused_tim.so")))
+    else:
+        print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))

@@ -183,7 +183,7 @@ struct Plan {
   int bn;  // vocab tile of the fused passes (UMMA N): 256 or 128
   bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
-      off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, total;
+      off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, off_zscr, total;
 };
 
 // Static round-robin of units over a persistent grid: makespan in tiles (+ per-unit refill cost).
@@ -262,7 +262,14 @@ static Plan make_plan(const kd_problem* p) {
   P.cg = cta_group();
   P.bn = pass_bn();
   const int bmt = kBM * P.cg;  // token rows per fused-pass work tile
-  int nc = p->chunk_tokens > 0 ? p->chunk_tokens : 4096;
+  // Default chunk: the fused passes re-read the chunk's hidden rows for every vocab tile, so they must stay
+  // L2-resident next to the streaming heads: ~24 MiB of H_t|H_s per chunk (measured: c2 at 8192 tokens = 100 MB
+  // of hidden rows runs 12% slower than at 2048; profiles/r01_tuning.md).  KD_CHUNK_TOKENS overrides (experiments).
+  static const int nc_env = env_int("KD_CHUNK_TOKENS", 0);
+  int nc_default = (int)((24ll << 20) / ((long long)(P.d_t + P.d_s) * 2));
+  nc_default = nc_default < 1024 ? 1024 : (nc_default > 8192 ? 8192 : nc_default);
+  if (nc_env > 0) nc_default = nc_env;
+  int nc = p->chunk_tokens > 0 ? p->chunk_tokens : nc_default;
   const int n_pad = ((P.N + bmt - 1) / bmt) * bmt;
   if (nc > n_pad) nc = n_pad;
   nc = ((nc + bmt - 1) / bmt) * bmt;
@@ -293,6 +300,7 @@ static Plan make_plan(const kd_problem* p) {
   P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
   P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
   P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
+  P.off_zscr = take((size_t)P.num_sms * P.bn * kBM * 4);  // decoupled pass 2 staging (19 MB: L2-resident)
   P.total = o;
   return P;
 }
@@ -378,6 +386,7 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.kpart = (P.fix || P.kind == KD_FKL) ? ws_at<float>(c.ws, P.off_kpart) : nullptr;
   pp.corr_v = P.fix ? nullptr : ws_at<int>(c.ws, P.off_corr_v);
   pp.corr_r = P.fix ? nullptr : ws_at<float>(c.ws, P.off_corr_r);
+  pp.zscr = ws_at<float>(c.ws, P.off_zscr);
   pp.dbg = reinterpret_cast<unsigned long long*>(g_dbg_ptr);
   static const int l2_hints = env_int("KD_L2_HINTS", 0);  // measured neutral-to-negative (profiles/r01_ncu_pass_pair256.md)
   pp.l2_hints = l2_hints;
@@ -397,7 +406,8 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
   const int grid = pass_grid(P);
-  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, true, P.cg, P.bn, c.maps, pp, grid, c.s));
+  static const bool p2_coupled = env_int("KD_P2_COUPLED", 0) != 0;
+  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, p2_coupled, P.cg, P.bn, c.maps, pp, grid, c.s));
   if (P.fix) {
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453

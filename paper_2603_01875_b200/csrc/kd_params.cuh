@@ -49,7 +49,9 @@ struct PassParams {
   // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split*parts][kCorrSlots])
   int* corr_v;
   float* corr_r;
-  int l2_hints;         // 1: TMA loads of H evict_last, of W evict_first; G stores evict_first
+  float* zscr;          // decoupled pass 2: per-CTA [BN][128] fp32 staging of the teacher half-tile
+  int l2_hints;         // bit 0: TMA loads of H evict_last, of W evict_first; bit 1: discard staged z_t lines;
+                        // bit 2: streaming G stores; bit 3: L2 prefetch of the next vocab tile's head rows
   unsigned long long* dbg;  // KD_EPI_TIMING builds only: epilogue cycle counters (see kd_pass.cu)
 };
 

@@ -69,10 +69,13 @@ __device__ __forceinline__ UnitRange unit_range(int u, int m_tiles, int n_split,
   return r;
 }
 
-// DEC (pass 1 of FKL/JSD/TVD in kd_fused_fwd_bwd): the teacher and student LSEs are independent, so the two GEMMs
-// of a vocab tile run as separate half-tiles through TWO 256-column accumulators and each half's epilogue overlaps
-// the other half's MMAs (the coupled form keeps both accumulators live and exposes the epilogue).  The FKL loss then
-// comes from pass 2.  RKL (whose gradient needs its loss in pass 2) and the vocab-shard API use the coupled form.
+// DEC (decoupled): the two GEMMs of a vocab tile run as separate half-tiles (teacher K blocks, then student K blocks)
+// through TWO BN-column accumulators, so each half's epilogue overlaps the other half's MMAs (the coupled form keeps
+// both accumulators of a tile live and exposes the epilogue).
+//   pass 1: the teacher and student LSEs are independent; the FKL loss then comes from pass 2.  RKL (whose gradient
+//           needs its loss in pass 2) and the vocab-shard API keep the coupled pass 1 with its cross term U.
+//   pass 2: the teacher half-tile is parked in a per-CTA fp32 staging buffer (p.zscr) and rejoins its student
+//           half-tile in the student epilogue.
 template <int PASS, int KIND, int CG, int BN, bool DEC = false, int EP = epi_parts(PASS, KIND)>
 __global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
@@ -80,8 +83,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
                    const PassParams p) {
   using C = PassCfg<CG, BN>;
   constexpr int kStages = C::kStages;
-  constexpr int kNB = DEC ? 2 * C::kNumBuf : C::kNumBuf;  // accumulator buffers (DEC: one side per buffer)
-  static_assert(!DEC || (PASS == 1 && KIND == KIND_FKL), "DEC is a pass-1 (FKL-role) mode");
+  constexpr int kNB = DEC ? 2 : C::kNumBuf;  // accumulator buffers (DEC: one half-tile side per buffer)
+  static_assert(!DEC || PASS == 2 || KIND == KIND_FKL, "decoupled pass 1 uses the FKL role order");
   constexpr int kBMt = kBM * CG;  // token rows per work tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,6 +99,10 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
+#ifdef KD_EPI_TIMING
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const int worker = blockIdx.x / CG, n_workers = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
             const CUtensorMap* ma = tch ? &tm_ht : &tm_hs;
             const CUtensorMap* mb = tch ? &tm_wt : &tm_ws;
-            if (CG == 2 && p.l2_hints) {
+            if (CG == 2 && (p.l2_hints & 1)) {
               // the hidden chunk (~50 MB) is re-read for every vocab tile: keep it; the heads stream through
               tma_load_2d_pair_hint(ma, &full[st], sA + st * C::kABytes, k, row, kEvictLast);
               tma_load_2d_pair_hint(mb, &full[st], sB + st * C::kBBytes, k, vrow, kEvictFirst);
@@ -161,6 +168,12 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               tma_load_2d(ma, &full[st], sA + st * C::kABytes, k, row);
               tma_load_2d(mb, &full[st], sB + st * C::kBBytes, k, vrow);
             }
+          }
+          if ((p.l2_hints & 8) && lane == 0 && vt + 1 < ur.vt1) {
+            // pull the same K block of the next vocab tile's head rows into L2 one tile ahead of its TMA load
+            const bool tch = kb < p.kb_t;
+            const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
+            tma_prefetch_l2_2d(tch ? &tm_wt : &tm_ws, k, vrow + BN);
           }
           __syncwarp();
         }
@@ -177,13 +190,26 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
           for (int side = 0; side < 2; ++side, ++it) {
             const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+#ifdef KD_EPI_TIMING
+            const long long m0 = clock64();
+            long long mfull = 0;
+#endif
             mbar_wait(&tempty[buf], tph ^ 1);
             tc_fence_after();
+#ifdef KD_EPI_TIMING
+            const long long m1 = clock64();
+#endif
             const uint32_t d = tmem_base + buf * BN;
             const int nkb = side ? p.kb_s : p.kb_t;
             for (int kb = 0; kb < nkb; ++kb, ++kit) {
               const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
+#ifdef KD_EPI_TIMING
+              const long long f0 = clock64();
+#endif
               mbar_wait(&full[st], ph);
+#ifdef KD_EPI_TIMING
+              mfull += clock64() - f0;
+#endif
               tc_fence_after();
               if (lane == 0) {
                 const uint64_t a_desc = sdesc_sw128(smem_u32(sA + st * C::kABytes), 16, 1024);
@@ -204,6 +230,15 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               }
               __syncwarp();
             }
+#ifdef KD_EPI_TIMING
+            if (p.dbg && lane == 0) {  // MMA warp (decoupled: per half-tile, counted as half a tile)
+              unsigned long long* d = p.dbg + 2ull * 148 * 16 * 4 + (((size_t)(PASS - 1) * gridDim.x + blockIdx.x) * 4);
+              d[0] += (unsigned long long)(m1 - m0);
+              d[1] += (unsigned long long)mfull;
+              d[2] += (unsigned long long)(clock64() - m1);
+              d[3] += side;
+            }
+#endif
           }
         }
       }
@@ -279,7 +314,16 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     // the leader's tempty barrier collects the releases of both CTAs' epilogues
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     uint32_t it = 0;
-    if constexpr (DEC) {
+    // this warp's part of accumulator buffer `buf` drained -> release it toward the MMA warp
+    auto release = [&](uint32_t buf) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + buf * 8);
+        else mbar_arrive_relaxed(&tempty[buf]);
+      }
+    };
+    if constexpr (DEC && PASS == 1) {
       constexpr int kChunks = BN / 32;
       const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
       for (int u = worker; u < n_units; u += n_workers) {
@@ -302,8 +346,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                  if (CG == 2) mbar_arrive_cluster(tempty_leader + buf * 8);
-                  else mbar_arrive(&tempty[buf]);
+                  if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + buf * 8);
+                  else mbar_arrive_relaxed(&tempty[buf]);
                 }
               }
               const int v0 = vt * BN + c * 32;
@@ -392,6 +436,226 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       const float dlr = (lSs - lSt) + ell2;
       const float dlt = lSt - lSs;          // FKL: log2 p − log2 q = (u_t − u_s) − (log2 S_t − log2 S_s)
       float Lacc = 0.f, cL = 0.f;           // FKL loss partial (pass 2)
+      // pass 2, one 32-column chunk of the tile: the logit gradient of this row from both sides' raw logits
+      auto p2chunk = [&](float (&zt)[32], float (&zs)[32], int v0, int nvalid) {
+        // ------------------------------------------------ pass 2: logit gradient
+        if (v0 >= p.g_ld) return;  // beyond the scratch row (only in the last tile)
+        // Gᵀ [g_ld][n_rows]: for a fixed vocab column the warp's 32 rows are contiguous (coalesced stores)
+        const size_t col0 = (size_t)v0 * p.n_rows + r_local;
+        if (KIND == KIND_FKL || KIND == KIND_RKL) {
+          float g[32];
+          if (row_ok && nvalid == 32) {
+            // fast path (every chunk but the vocab tail and the rows past the chunk end): packed fp32x2
+            // math on (teacher, student) pairs, normalisation + loss scale folded into per-row constants
+            float la[2] = {0.f, 0.f};
+            kd_unroll32([&](auto I) {
+              constexpr int i = decltype(I)::value;
+              const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
+              const float2 r = exp2_pair<i>(u);
+              const float2 e = fmul2(r, cTS);  // (gscale·p, gscale·q) rounded
+              if (KIND == KIND_FKL) {
+                g[i] = e.y - e.x;
+                // FKL loss in bits, unnormalised: Σ 2^{u_t} · (log2 p − log2 q); × 2^-log2 S_t at unit end
+                la[i & 1] = fmaf(r.x, (u.x - u.y) - dlt, la[i & 1]);
+              } else {
+                g[i] = e.y * ((u.y - u.x) - dlr);  // gscale·q·(log2(q/p) − RKL/ln2)
+              }
+            });
+            if (KIND == KIND_FKL) kahan_add(Lacc, cL, la[0] + la[1]);
+          } else {
+            float la = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const bool ok = row_ok && (i < nvalid);
+              const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
+              const float2 r = make_float2(ex2(u.x), ex2(u.y));
+              const float2 e = fmul2(r, cTS);
+              const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr);
+              g[i] = ok ? gi : 0.f;
+              if (KIND == KIND_FKL && ok) la = fmaf(r.x, (u.x - u.y) - dlt, la);
+            }
+            if (KIND == KIND_FKL) kahan_add(Lacc, cL, la);
+          }
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) split2_fast(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
+          // exact residuals of the split for the largest entries (added back by k_reduce_dh); the per-chunk
+          // max gates the bookkeeping so typical chunks pay ~0.5 instruction per element
+          float amax = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(g[i]));
+          if (amax > kCorrThresh) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const float gv = g[2 * i + h];
+                if (fabsf(gv) > kCorrThresh) {
+                  const float rep = h ? bf16hi_to_f32(hi[i]) + bf16hi_to_f32(lo[i])
+                                      : bf16lo_to_f32(hi[i]) + bf16lo_to_f32(lo[i]);
+                  const float rr = gv - rep;
+                  if (fabsf(rr) > fabsf(cr1)) {
+                    if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
+                    else { cr1 = rr; cv1 = v0 + 2 * i + h; }
+                  }
+                }
+              }
+            }
+          }
+          __nv_bfloat16* ph = p.g_hi + col0;
+          __nv_bfloat16* pl = p.g_lo + col0;
+          if (p.l2_hints & 4) {  // G is consumed by the next kernel: stream it past L2's operand working set
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              st_global_b16_cs(ph, (uint16_t)(hi[i] & 0xFFFFu));
+              st_global_b16_cs(pl, (uint16_t)(lo[i] & 0xFFFFu));
+              ph += p.n_rows;
+              pl += p.n_rows;
+              st_global_b16_cs(ph, (uint16_t)(hi[i] >> 16));
+              st_global_b16_cs(pl, (uint16_t)(lo[i] >> 16));
+              ph += p.n_rows;
+              pl += p.n_rows;
+            }
+            return;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
+            st_global_b16(pl, (uint16_t)(lo[i] & 0xFFFFu));
+            ph += p.n_rows;
+            pl += p.n_rows;
+            st_global_b16(ph, (uint16_t)(hi[i] >> 16));
+            st_global_b16(pl, (uint16_t)(lo[i] >> 16));
+            ph += p.n_rows;
+            pl += p.n_rows;
+          }
+        } else {
+          float g[32], gb[32];
+          float kk[2] = {0.f, 0.f}, jj[2] = {0.f, 0.f};
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float ut = fmaf(zt[i], alpha, -Mt2), us = fmaf(zs[i], alpha, -Ms2);
+            const float pt = __fmul_rn(ex2(ut), iSt), qs = __fmul_rn(ex2(us), iSs);
+            const float xt = ut - lSt;  // log2 p
+            const float xs = us - lSs;  // log2 q
+            const bool ok = row_ok && (i < nvalid);
+            if (KIND == KIND_JSD) {
+              const float m = fmaxf(fmaf(p.beta, pt, (1.f - p.beta) * qs), 1.17549435e-38f);
+              const float lm = lg2(m);
+              const float lv = xs - lm;  // log2(q/m)
+              const float a = qs * lv;
+              g[i] = ok ? a : 0.f;
+              gb[i] = ok ? qs : 0.f;
+              kk[i & 1] += ok ? a : 0.f;
+              jj[i & 1] += ok ? pt * (xt - lm) : 0.f;
+            } else {  // TVD
+              const float d = qs - pt;
+              const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+              g[i] = ok ? qs * sgn : 0.f;
+              gb[i] = ok ? qs : 0.f;
+              kk[i & 1] += ok ? qs * sgn : 0.f;
+              jj[i & 1] += ok ? fabsf(d) : 0.f;
+            }
+          }
+          float* pa = p.g_a + col0;
+          float* pb = p.g_b + col0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            pa[(size_t)i * p.n_rows] = g[i];
+            pb[(size_t)i * p.n_rows] = gb[i];
+          }
+          kahan_add(Kacc, cK, kk[0] + kk[1]);
+          kahan_add(Jacc, cJ, jj[0] + jj[1]);
+        }
+      };
+      if constexpr (DEC && PASS == 2) {
+        // decoupled pass 2: the teacher half-tile's raw fp32 logits are parked in this CTA's private staging
+        // buffer (BN x 128 fp32, L2-resident), freeing its accumulator at once; the student half-tile's epilogue
+        // reads them back — same thread, same addresses, so program order suffices — and runs the gradient math
+        // while the next vocab tile's teacher MMAs proceed.
+        // staging layout [column / 4][row][4]: each lane moves 16 B per access and a warp's access is one
+        // contiguous 512 B run
+        float4* zrow = reinterpret_cast<float4*>(p.zscr + (size_t)blockIdx.x * (BN * kBM)) + r_in_tile;
+        constexpr int kChunks = BN / 32;
+        const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
+        for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
+#ifdef KD_EPI_TIMING
+          long long tw = 0, tt = 0, ts = 0, t0 = clock64();
+#endif
+          {  // teacher half
+            const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+            ++it;
+            mbar_wait(&tfull[buf], tph);
+            tc_fence_after();
+#ifdef KD_EPI_TIMING
+            const long long t1 = clock64();
+            tw += t1 - t0;
+            t0 = t1;
+#endif
+            const uint32_t t_addr = tmem_base + lane_addr + buf * BN;
+#pragma unroll 1
+            for (int c = c_beg; c < c_end; ++c) {
+              float z[32];
+              tmem_ld32_sync(t_addr + c * 32, z);
+              if (c == c_end - 1) release(buf);
+              float4* zc = zrow + (size_t)c * 8 * kBM;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) zc[j * kBM] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
+            }
+          }
+#ifdef KD_EPI_TIMING
+          {
+            const long long t1 = clock64();
+            tt += t1 - t0;
+            t0 = t1;
+          }
+#endif
+          {  // student half
+            const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+            ++it;
+            mbar_wait(&tfull[buf], tph);
+            tc_fence_after();
+#ifdef KD_EPI_TIMING
+            const long long t1 = clock64();
+            tw += t1 - t0;
+            t0 = t1;
+#endif
+            const uint32_t t_addr = tmem_base + lane_addr + buf * BN;
+#pragma unroll 1
+            for (int c = c_beg; c < c_end; ++c) {
+              float zt[32], zs[32];
+              const float4* zc = zrow + (size_t)c * 8 * kBM;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 v = zc[j * kBM];
+                zt[4 * j] = v.x;
+                zt[4 * j + 1] = v.y;
+                zt[4 * j + 2] = v.z;
+                zt[4 * j + 3] = v.w;
+              }
+              tmem_ld32_sync(t_addr + c * 32, zs);
+              if (c == c_end - 1) release(buf);
+              const int v0 = vt * BN + c * 32;
+              p2chunk(zt, zs, v0, min(32, p.V_r - v0));
+              if (p.l2_hints & 2) {
+                // the staged lines are dead: drop them from L2 without a write-back (the warp's 4 KB of the chunk)
+                __syncwarp();
+                l2_discard128(reinterpret_cast<const char*>(zc - lane) + (size_t)(lane >> 2) * kBM * 16 + (lane & 3) * 128);
+              }
+            }
+          }
+#ifdef KD_EPI_TIMING
+          ts += clock64() - t0;
+          if (p.dbg && lane == 0) {  // per warp: [wait for MMA, teacher-half work, student-half work], tiles
+            unsigned long long* d = p.dbg + (((size_t)(PASS - 1) * gridDim.x + blockIdx.x) * 16 + (warp - 4)) * 4;
+            d[0] += (unsigned long long)tw;
+            d[1] += (unsigned long long)tt;
+            d[2] += (unsigned long long)ts;
+            d[3] += 1ull;
+          }
+#endif
+        }
+      } else
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
         const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
 #ifdef KD_EPI_TIMING
@@ -421,8 +685,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-              if (CG == 2) mbar_arrive_cluster(tempty_leader + buf * 8);
-              else mbar_arrive(&tempty[buf]);
+              if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + buf * 8);
+              else mbar_arrive_relaxed(&tempty[buf]);
             }
           }
           const int v0 = vbase + c * 32;
@@ -470,121 +734,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             kahan_add(Sq, cSq, s01.y + s23.y);
             kahan_add(U, cU, (uu[0] + uu[1]) + (uu[2] + uu[3]));
           } else {
-            // ------------------------------------------------ pass 2: logit gradient
-            if (v0 >= p.g_ld) continue;  // beyond the scratch row (only in the last tile)
-            // Gᵀ [g_ld][n_rows]: for a fixed vocab column the warp's 32 rows are contiguous (coalesced stores)
-            const size_t col0 = (size_t)v0 * p.n_rows + r_local;
-            if (KIND == KIND_FKL || KIND == KIND_RKL) {
-              float g[32];
-              if (row_ok && nvalid == 32) {
-                // fast path (every chunk but the vocab tail and the rows past the chunk end): packed fp32x2
-                // math on (teacher, student) pairs, normalisation + loss scale folded into per-row constants
-                float la[2] = {0.f, 0.f};
-                kd_unroll32([&](auto I) {
-                  constexpr int i = decltype(I)::value;
-                  const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
-                  const float2 r = exp2_pair<i>(u);
-                  const float2 e = fmul2(r, cTS);  // (gscale·p, gscale·q) rounded
-                  if (KIND == KIND_FKL) {
-                    g[i] = e.y - e.x;
-                    // FKL loss in bits, unnormalised: Σ 2^{u_t} · (log2 p − log2 q); × 2^-log2 S_t at unit end
-                    la[i & 1] = fmaf(r.x, (u.x - u.y) - dlt, la[i & 1]);
-                  } else {
-                    g[i] = e.y * ((u.y - u.x) - dlr);  // gscale·q·(log2(q/p) − RKL/ln2)
-                  }
-                });
-                if (KIND == KIND_FKL) kahan_add(Lacc, cL, la[0] + la[1]);
-              } else {
-                float la = 0.f;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const bool ok = row_ok && (i < nvalid);
-                  const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
-                  const float2 r = make_float2(ex2(u.x), ex2(u.y));
-                  const float2 e = fmul2(r, cTS);
-                  const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr);
-                  g[i] = ok ? gi : 0.f;
-                  if (KIND == KIND_FKL && ok) la = fmaf(r.x, (u.x - u.y) - dlt, la);
-                }
-                if (KIND == KIND_FKL) kahan_add(Lacc, cL, la);
-              }
-              uint32_t hi[16], lo[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) split2_fast(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
-              // exact residuals of the split for the largest entries (added back by k_reduce_dh); the per-chunk
-              // max gates the bookkeeping so typical chunks pay ~0.5 instruction per element
-              float amax = 0.f;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(g[i]));
-              if (amax > kCorrThresh) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-#pragma unroll
-                  for (int h = 0; h < 2; ++h) {
-                    const float gv = g[2 * i + h];
-                    if (fabsf(gv) > kCorrThresh) {
-                      const float rep = h ? bf16hi_to_f32(hi[i]) + bf16hi_to_f32(lo[i])
-                                          : bf16lo_to_f32(hi[i]) + bf16lo_to_f32(lo[i]);
-                      const float rr = gv - rep;
-                      if (fabsf(rr) > fabsf(cr1)) {
-                        if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
-                        else { cr1 = rr; cv1 = v0 + 2 * i + h; }
-                      }
-                    }
-                  }
-                }
-              }
-              __nv_bfloat16* ph = p.g_hi + col0;
-              __nv_bfloat16* pl = p.g_lo + col0;
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
-                st_global_b16(pl, (uint16_t)(lo[i] & 0xFFFFu));
-                ph += p.n_rows;
-                pl += p.n_rows;
-                st_global_b16(ph, (uint16_t)(hi[i] >> 16));
-                st_global_b16(pl, (uint16_t)(lo[i] >> 16));
-                ph += p.n_rows;
-                pl += p.n_rows;
-              }
-            } else {
-              float g[32], gb[32];
-              float kk[2] = {0.f, 0.f}, jj[2] = {0.f, 0.f};
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const float ut = fmaf(zt[i], alpha, -Mt2), us = fmaf(zs[i], alpha, -Ms2);
-                const float pt = __fmul_rn(ex2(ut), iSt), qs = __fmul_rn(ex2(us), iSs);
-                const float xt = ut - lSt;  // log2 p
-                const float xs = us - lSs;  // log2 q
-                const bool ok = row_ok && (i < nvalid);
-                if (KIND == KIND_JSD) {
-                  const float m = fmaxf(fmaf(p.beta, pt, (1.f - p.beta) * qs), 1.17549435e-38f);
-                  const float lm = lg2(m);
-                  const float lv = xs - lm;  // log2(q/m)
-                  const float a = qs * lv;
-                  g[i] = ok ? a : 0.f;
-                  gb[i] = ok ? qs : 0.f;
-                  kk[i & 1] += ok ? a : 0.f;
-                  jj[i & 1] += ok ? pt * (xt - lm) : 0.f;
-                } else {  // TVD
-                  const float d = qs - pt;
-                  const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-                  g[i] = ok ? qs * sgn : 0.f;
-                  gb[i] = ok ? qs : 0.f;
-                  kk[i & 1] += ok ? qs * sgn : 0.f;
-                  jj[i & 1] += ok ? fabsf(d) : 0.f;
-                }
-              }
-              float* pa = p.g_a + col0;
-              float* pb = p.g_b + col0;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                pa[(size_t)i * p.n_rows] = g[i];
-                pb[(size_t)i * p.n_rows] = gb[i];
-              }
-              kahan_add(Kacc, cK, kk[0] + kk[1]);
-              kahan_add(Jacc, cJ, jj[0] + jj[1]);
-            }
+            p2chunk(zt, zs, v0, nvalid);
           }
         }
 #ifdef KD_EPI_TIMING
@@ -626,6 +776,19 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
   if (CG == 2) cluster_sync();  // neither CTA leaves while its partner may still signal its barriers
   else __syncthreads();
   tc_fence_after();
+#ifdef KD_EPI_TIMING
+  if (p.dbg && threadIdx.x == 0) {  // per CTA: [start ns, end ns, SM id, units]
+    unsigned long long t_end;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* d = p.dbg + 2ull * 148 * 16 * 4 + 2ull * 148 * 4 + (((size_t)(PASS - 1) * gridDim.x + blockIdx.x) * 4);
+    d[0] = t_start;
+    d[1] = t_end;
+    d[2] = smid;
+    d[3] = (unsigned long long)((n_units - worker + n_workers - 1) / n_workers);
+  }
+#endif
   if (warp == 2) {
     if (CG == 2) tmem_dealloc_pair(tmem_base, 512);
     else tmem_dealloc(tmem_base, 512);
@@ -663,6 +826,12 @@ static cudaError_t launch_pass_cg(int pass, int kind, bool coupled, const CUtens
     return coupled ? launch_pass_t<1, KIND_FKL, CG, BN>(maps, p, grid, stream)
                    : launch_pass_t<1, KIND_FKL, CG, BN, true>(maps, p, grid, stream);
   }
+  if (!coupled) switch (kind) {
+      case KIND_FKL: return launch_pass_t<2, KIND_FKL, CG, BN, true>(maps, p, grid, stream);
+      case KIND_RKL: return launch_pass_t<2, KIND_RKL, CG, BN, true>(maps, p, grid, stream);
+      case KIND_JSD: return launch_pass_t<2, KIND_JSD, CG, BN, true>(maps, p, grid, stream);
+      default: return launch_pass_t<2, KIND_TVD, CG, BN, true>(maps, p, grid, stream);
+    }
   switch (kind) {
     case KIND_FKL: return launch_pass_t<2, KIND_FKL, CG, BN>(maps, p, grid, stream);
     case KIND_RKL: return launch_pass_t<2, KIND_RKL, CG, BN>(maps, p, grid, stream);
@@ -673,7 +842,8 @@ static cudaError_t launch_pass_cg(int pass, int kind, bool coupled, const CUtens
 
 // cg = 1: single-SM tiles (grid = #tile workers); cg = 2: SM pairs (grid = 2 x #pair workers).
 // bn = vocab tile (UMMA N) 128 or 256.  maps: [H_t, W_t, H_s, W_s] with W boxes of bn / cg rows.
-// coupled = false selects the decoupled pass 1 for FKL/JSD/TVD (RKL is always coupled).
+// coupled = false selects the decoupled form (pass 1: FKL/JSD/TVD only, RKL is always coupled; pass 2: all kinds,
+// p.zscr must then hold grid x bn x 128 floats).
 cudaError_t launch_pass(int pass, int kind, bool coupled, int cg, int bn, const CUtensorMap* maps, const PassParams& p,
                         int grid, cudaStream_t stream) {
   if (cg == 2) return bn == 256 ? launch_pass_cg<2, 256>(pass, kind, coupled, maps, p, grid, stream)

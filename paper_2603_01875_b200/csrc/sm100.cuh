@@ -94,6 +94,12 @@ __device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(hint)
       : "memory");
 }
+// Prefetch one 2-D tile of a tensor map into L2 (no shared-memory destination, no completion signal).
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y)
+               : "memory");
+}
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 
@@ -146,6 +152,26 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMEM-release arrive: the accumulator reads it orders are complete (tcgen05.wait::ld) and fenced by
+// tcgen05.fence::before_thread_sync, so no memory release is needed — a release.cluster arrive would stall the
+// epilogue until every global store it issued before is acknowledged by L2.
+#ifndef KD_RELAXED_TEMPTY
+#define KD_RELAXED_TEMPTY 1
+#endif
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+#if KD_RELAXED_TEMPTY
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+#if KD_RELAXED_TEMPTY
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+#endif
 }
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // clears the CTA-pair peer bit: the leader's copy of a barrier
 // 2-D tile load issued by either CTA of a pair; completion is signalled on the LEADER's barrier.
@@ -370,9 +396,17 @@ __device__ __forceinline__ void split2_fast(float a, float b, uint32_t& hi, uint
 }
 
 
+__device__ __forceinline__ void st_global_b16_cs(void* p, uint16_t v) {  // streaming (evict-first) store
+  asm volatile("st.global.cs.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
 __device__ __forceinline__ void st_global_b16(void* p, uint16_t v) {
   asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
 }
+// Invalidate one 128-byte L2 line without writing it back (its contents become undefined).
+__device__ __forceinline__ void l2_discard128(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));

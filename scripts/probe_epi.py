@@ -12,7 +12,7 @@ H_t, H_s = KI.make_hidden(n, W_t, W_s, seed=1001, head_seed=1000)
 up = lambda b: torch.from_numpy(b.view(np.int16)).cuda().view(torch.bfloat16)
 Ht, Hs, Wt, Ws = up(H_t), up(H_s), up(W_t), up(W_s)
 L = kd.lib()
-dbg = torch.zeros(2 * 148 * 16 * 4 + 2 * 148 * 4, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(2 * 148 * 16 * 4 + 2 * 148 * 4 + 2 * 148 * 4, dtype=torch.int64, device="cuda")
 L.kd_debug_set_buffer.argtypes = [ctypes.c_void_p]
 kd.fused_fwd_bwd(Ht, Wt, Hs, Ws, T=1.0, kind=cfg.kind)  # warm
 torch.cuda.synchronize()
@@ -27,7 +27,19 @@ for name, pass_id in (("pass1+pass2", 0),):
     L.kd_debug_set_buffer(None)
     allv = dbg.cpu().numpy().astype(np.float64)
     dd = allv[:2 * 148 * 16 * 4].reshape(2, 148, 16, 4)
-    mm = allv[2 * 148 * 16 * 4:].reshape(2, 148, 4)
+    mm = allv[2 * 148 * 16 * 4:2 * 148 * 16 * 4 + 2 * 148 * 4].reshape(2, 148, 4)
+    cta = dbg.cpu().numpy()[2 * 148 * 16 * 4 + 2 * 148 * 4:].reshape(2, 148, 4)
+    for ps in range(2):
+        c = cta[ps]
+        c = c[c[:, 1] > 0]
+        t0 = c[:, 0].min()
+        st, en = (c[:, 0] - t0) / 1e3, (c[:, 1] - t0) / 1e3
+        dur = en - st
+        print(cfg.name, f"pass{ps + 1} CTAs {len(c)}: start spread {st.max():.1f} us, end min/median/max "
+              f"{en.min():.1f}/{np.median(en):.1f}/{en.max():.1f} us, busy fraction {dur.sum() / (len(c) * en.max()):.3f}, "
+              f"units/CTA {sorted(set(c[:, 3].tolist()))}")
+        order = np.argsort(en)
+        print("   earliest-finishing SMs", c[order[:6], 2].tolist(), "latest", c[order[-6:], 2].tolist())
     for ps in range(2):
         m = mm[ps]
         t = m[..., 3].sum()
@@ -37,6 +49,6 @@ for name, pass_id in (("pass1+pass2", 0),):
         d = dd[ps]
         tiles = d[..., 3].sum()
         print(cfg.name, f"pass{ps + 1} epilogue warps: warp-tiles", int(tiles),
-              "avg cycles/tile: wait-for-MMA %.0f, TMEM loads %.0f, epilogue total %.0f"
+              "avg cycles/tile: wait-for-MMA %.0f, [coupled: TMEM loads | decoupled pass 2: teacher half] %.0f, [epilogue total | student half] %.0f"
               % (d[..., 0].sum() / tiles, d[..., 1].sum() / tiles, d[..., 2].sum() / tiles))
     print({k: round(v[1], 3) for k, v in prof.items()})

@@ -56,12 +56,20 @@ int main(void) {
 
 
 def test_workspace_size_host_only():
-    p = kd.make_problem(32768, 4096, 2048, 151936)
+    p = kd.make_problem(32768, 4096, 2048, 151936, chunk_tokens=4096)
     n = kd.workspace_size(p)
     # G scratch: chunk 4096 x 151936 x (bf16 hi + lo) dominates; packed hidden copies 0.4 GB
     assert 2.4e9 < n < 6e9
-    pj = kd.make_problem(32768, 4096, 2048, 151936, kind="jsd")
+    pj = kd.make_problem(32768, 4096, 2048, 151936, kind="jsd", chunk_tokens=4096)
     assert kd.workspace_size(pj) > n + 0.99 * 4096 * 151936 * 8  # + two fp32 G planes
+
+
+def test_default_chunk_keeps_hidden_rows_l2_resident():
+    # default chunk = 24 MiB of H_t|H_s rows: 2048 tokens at d_t + d_s = 6144, 4096 at 3072 (kdfused.h chunk_tokens)
+    for d_t, d_s, nc in ((4096, 2048, 2048), (2048, 1024, 4096)):
+        dflt = kd.workspace_size(kd.make_problem(65536, d_t, d_s, 151936))
+        explicit = kd.workspace_size(kd.make_problem(65536, d_t, d_s, 151936, chunk_tokens=nc))
+        assert dflt == explicit
 
 
 @pytest.mark.parametrize("kw,status", [(dict(T=0.0), 1), (dict(T=float("nan")), 1), (dict(kind=7), 1),
