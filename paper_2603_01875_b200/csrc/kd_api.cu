@@ -23,8 +23,8 @@
 namespace kd {
 cudaError_t launch_pass(int pass, int kind, bool coupled, int cg, int bn, const CUtensorMap* maps, const PassParams& p,
                         int grid, cudaStream_t s);
-cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, const CUtensorMap* a0, const CUtensorMap* a1,
-                        const CUtensorMap* b, const GemmParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, int cg, const CUtensorMap* a0, const CUtensorMap* a1,
+                        const CUtensorMap* b, const GemmParams& p, int sms, cudaStream_t stream);
 cudaError_t launch_compact(const uint8_t* mask, int N, int* idx, int* n_eff, cudaStream_t s);
 cudaError_t launch_gather(const __nv_bfloat16* src, long long src_ld, __nv_bfloat16* dst, int d, int N,
                           const int* idx, const int* n_eff, cudaStream_t s);
@@ -144,6 +144,14 @@ static int cta_group() {  // KD_CTA_GROUP=1 selects single-SM pass tiles (A/B ex
   return v;
 }
 
+static int gemm_cg() {  // KD_GEMM_CG=1 selects single-SM backward GEMM tiles (A/B experiments); default: SM pairs
+  static int v = [] {
+    const char* e = getenv("KD_GEMM_CG");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return v;
+}
+
 static int pass_bn() {  // KD_PASS_BN=128 selects 128-wide vocab tiles (A/B experiments); default 256
   static int v = [] {
     const char* e = getenv("KD_PASS_BN");
@@ -213,15 +221,18 @@ static int choose_n_split(int m_tiles, int v_tiles, int sms) {
   return best;
 }
 
-static int choose_k_split(int m_tiles, int n_tiles, int kbs, int sms) {
+// Split-K factor of the dh GEMM: units = m_tiles * n_tiles * k over a persistent grid of `workers` (SMs or SM
+// pairs).  Cost in K-block times (1024 cycles: one 64-deep K block of a full-rate tile): waves x (K blocks per
+// unit + ~2 fill/drain) + the split-K reduction re-reading (k - 1) extra fp32 slabs of M x N (~3.4 MB per K-block
+// time at HBM speed).  At c2 (64 tile units on 74 pairs) this picks k = 8: 7 full waves instead of one 86%-full one.
+static int choose_k_split(int m_tiles, int n_tiles, int kbs, int workers, long long M, long long N) {
   int best = 1;
   double best_cost = 1e300;
+  const double slab_kb = (double)M * (double)N * 4.0 / 3.4e6;
   for (int k = 1; k <= 16 && k <= kbs; ++k) {
-    const int units = m_tiles * n_tiles * k;
-    const int grid = units < sms ? units : sms;
-    const double per = (double)((kbs + k - 1) / k) + 2.0;  // k-blocks per unit + epilogue/refill
-    const double waves = (double)((units + grid - 1) / grid);
-    const double c = waves * per + 0.02 * kbs * (k - 1);   // + reduction traffic
+    const long long units = (long long)m_tiles * n_tiles * k;
+    const double waves = (double)((units + workers - 1) / workers);
+    const double c = waves * ((double)((kbs + k - 1) / k) + 2.0) + slab_kb * (k - 1);
     if (c < best_cost * 0.999) { best_cost = c; best = k; }
   }
   return best;
@@ -280,7 +291,8 @@ static Plan make_plan(const kd_problem* p) {
   P.v_tiles = (P.V_r + P.bn - 1) / P.bn;
   P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, P.num_sms / P.cg);
   P.g_ld = ((P.V_r + 63) / 64) * 64;
-  P.k_split = choose_k_split(P.m_tiles_c, (P.d_s + kGemmBN - 1) / kGemmBN, (P.V_r + kBK - 1) / kBK, P.num_sms);
+  P.k_split = choose_k_split((P.Nc + kBM * gemm_cg() - 1) / (kBM * gemm_cg()), (P.d_s + kGemmBN - 1) / kGemmBN,
+                             (P.V_r + kBK - 1) / kBK, P.num_sms / gemm_cg(), P.Nc, P.d_s);
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
   P.off_neff = take(8);
@@ -435,11 +447,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
   gp.out = ws_at<float>(c.ws, P.off_dhp);
   gp.out_ld = P.d_s;
   gp.out_split_stride = (long long)P.Nc * P.d_s;
-  {
-    const int units = P.m_tiles_c * ((P.d_s + kGemmBN - 1) / kGemmBN) * P.k_split;
-    KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, 2, EPI_STORE, &mg_hi, &mg_lo, &mw, gp, units < P.num_sms ? units : P.num_sms,
-                          c.s));
-  }
+  KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, 2, EPI_STORE, gemm_cg(), &mg_hi, &mg_lo, &mw, gp, P.num_sms, c.s));
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                                           P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
                                           P.n_split * epi_parts(2, P.kind) * kCorrSlots, c.Ws, c.s));
@@ -463,9 +471,7 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
     wp.out = dW;
     wp.out_ld = P.d_s;
     wp.out_split_stride = 0;
-    const int units = ((P.V_r + kBM - 1) / kBM) * ((P.d_s + kGemmBN - 1) / kGemmBN);
-    KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, 2, EPI_ACCUM, &ma_hi, &ma_lo, &mh, wp, units < P.num_sms ? units : P.num_sms,
-                          c.s));
+    KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, 2, EPI_ACCUM, gemm_cg(), &ma_hi, &ma_lo, &mh, wp, P.num_sms, c.s));
   }
   return KD_OK;
 }
@@ -621,7 +627,7 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
   else st = make_map(&ma, A, K, M, (uint64_t)K * 2, kBK, kBM);
   if (st != KD_OK) return st;
   if (b_mn_major) st = make_map(&mb, B, N, K, (uint64_t)N * 2, 64, kBK);
-  else st = make_map(&mb, B, K, N, (uint64_t)K * 2, kBK, kGemmBN);
+  else st = make_map(&mb, B, K, N, (uint64_t)K * 2, kBK, kGemmBN / gemm_cg());  // each CTA of a pair: half the tile
   if (st != KD_OK) return st;
   GemmParams gp{};
   gp.M = M;
@@ -632,10 +638,8 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
   gp.kb_per_acc = 1 << 30;  // plain GEMM: one accumulator per output tile
   gp.out = D;
   gp.out_ld = N;
-  const int sms = device_sms();
-  const int units = ((M + kBM - 1) / kBM) * ((N + kGemmBN - 1) / kGemmBN);
-  KD_LAUNCH(K_GEMM, launch_gemm(a_mn_major != 0, b_mn_major != 0, 1, EPI_STORE, &ma, nullptr, &mb, gp,
-                        units < sms ? units : sms, static_cast<cudaStream_t>(stream)));
+  KD_LAUNCH(K_GEMM, launch_gemm(a_mn_major != 0, b_mn_major != 0, 1, EPI_STORE, gemm_cg(), &ma, nullptr, &mb, gp,
+                                device_sms(), static_cast<cudaStream_t>(stream)));
   return KD_OK;
 }
 

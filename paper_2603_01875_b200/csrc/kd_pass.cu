@@ -27,6 +27,10 @@
 #define KD_SUBSTEP_REVERSE 1
 #endif
 
+#ifndef KD_PASS_SMEM_KB
+#define KD_PASS_SMEM_KB 224
+#endif
+
 namespace kd {
 
 // Compile-time unrolled loop over i = 0..31 (the element index must be a constant for exp2_pair<i>).
@@ -52,7 +56,9 @@ template <int CG, int BN>
 struct PassCfg {
   static constexpr int kABytes = kTileBytes;                 // 128 rows of H per CTA
   static constexpr int kBBytes = (BN / CG) * kBK * 2;        // BN/CG rows of W per CTA
-  static constexpr int kStages = (192 * 1024) / (kABytes + kBBytes);
+  // operand pipeline: as deep as shared memory allows — the epilogue's global traffic (G stores, z_t staging)
+  // raises the TMA latency the pipeline must cover (7 x 32 KB stages for the SM-pair 256-col tile)
+  static constexpr int kStages = (KD_PASS_SMEM_KB * 1024) / (kABytes + kBBytes);
   static constexpr int kNumBuf = 512 / (2 * BN);             // TMEM accumulator buffers
   static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -102,6 +108,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 #ifdef KD_EPI_TIMING
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const long long c_start = clock64();
 #endif
   const int worker = blockIdx.x / CG, n_workers = gridDim.x / CG;
 
@@ -518,6 +525,15 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             }
             return;
           }
+#ifdef KD_X_NOGSTORE  // experiment builds only: G computed but not stored
+          {
+            uint32_t x = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x ^= hi[i] ^ lo[i];
+            if (x == 0x9E3779B9u) *ph = __float2bfloat16(1.f);
+            return;
+          }
+#endif
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
@@ -599,8 +615,12 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               tmem_ld32_sync(t_addr + c * 32, z);
               if (c == c_end - 1) release(buf);
               float4* zc = zrow + (size_t)c * 8 * kBM;
+#ifndef KD_X_NOSTAGE  // experiment builds only: no staging traffic (the student half reuses its own logits)
 #pragma unroll
               for (int j = 0; j < 8; ++j) zc[j * kBM] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
+#else
+              if (z[0] == 1.2345f) zc[0] = make_float4(z[1], z[2], z[3], z[4]);
+#endif
             }
           }
 #ifdef KD_EPI_TIMING
@@ -625,6 +645,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             for (int c = c_beg; c < c_end; ++c) {
               float zt[32], zs[32];
               const float4* zc = zrow + (size_t)c * 8 * kBM;
+#ifndef KD_X_NOSTAGE
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const float4 v = zc[j * kBM];
@@ -634,6 +655,11 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
                 zt[4 * j + 3] = v.w;
               }
               tmem_ld32_sync(t_addr + c * 32, zs);
+#else
+              tmem_ld32_sync(t_addr + c * 32, zs);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) zt[i] = zs[i] * 1.0625f;
+#endif
               if (c == c_end - 1) release(buf);
               const int v0 = vt * BN + c * 32;
               p2chunk(zt, zs, v0, min(32, p.V_r - v0));
@@ -777,7 +803,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
   else __syncthreads();
   tc_fence_after();
 #ifdef KD_EPI_TIMING
-  if (p.dbg && threadIdx.x == 0) {  // per CTA: [start ns, end ns, SM id, units]
+  if (p.dbg && threadIdx.x == 0) {  // per CTA: [start ns, end ns, SM id, elapsed SM cycles]
     unsigned long long t_end;
     uint32_t smid;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -786,7 +812,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     d[0] = t_start;
     d[1] = t_end;
     d[2] = smid;
-    d[3] = (unsigned long long)((n_units - worker + n_workers - 1) / n_workers);
+    d[3] = (unsigned long long)(clock64() - c_start);
   }
 #endif
   if (warp == 2) {

@@ -37,7 +37,7 @@ for name, pass_id in (("pass1+pass2", 0),):
         dur = en - st
         print(cfg.name, f"pass{ps + 1} CTAs {len(c)}: start spread {st.max():.1f} us, end min/median/max "
               f"{en.min():.1f}/{np.median(en):.1f}/{en.max():.1f} us, busy fraction {dur.sum() / (len(c) * en.max()):.3f}, "
-              f"units/CTA {sorted(set(c[:, 3].tolist()))}")
+              f"SM cycles/CTA median {np.median(c[:, 3]):.0f} (clock {np.median(c[:, 3] / (dur * 1e3)):.3f} GHz)")
         order = np.argsort(en)
         print("   earliest-finishing SMs", c[order[:6], 2].tolist(), "latest", c[order[-6:], 2].tolist())
     for ps in range(2):
