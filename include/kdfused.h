@@ -99,7 +99,8 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
                            int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- vocabulary-sharded execution (north_star: "vocabulary sharding of W_t/W_s, with a tiny
- * all-reduce of per-token stats").  Rank r owns rows [v_begin, v_end) of both heads.  FKL/RKL only.
+ * all-reduce of per-token stats").  Rank r owns rows [v_begin, v_end) of both heads.
+ * FKL/RKL: kd_vocab_stats -> exchange -> kd_vocab_backward.  JSD/TVD: see kd_vocab_partials below.
  *   1) kd_vocab_stats      -> rec [5][N] f32: this shard's per-token record (base-2 running maxima,
  *                              sums and cross term; R10), 0-filled for masked rows.
  *   2) caller all-gathers the P records into recs [P][5][N] (any transport; 20 B/token/rank).
@@ -113,6 +114,27 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
                             const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
                             float* loss, float* dh_s_partial, float* dW_s, int64_t* n_nonfinite,
                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- JSD / TVD vocab shards: one more exchange.  The JSD gradient needs the per-token
+ * K = KL(q||m) = sum over the FULL vocabulary (the TVD one sum_v q*sign(q - p)), known only after every
+ * shard's pass 2 (R4, R5).  Per token chunk (n_tokens <= the chunk, KD_ERR_SHAPE otherwise; the
+ * caller slices the batch, see sharding.py):
+ *   1) kd_vocab_stats as above over the chunk's rows; all-gather recs [P][5][n].
+ *   2) kd_vocab_partials: merge (rank order) + pass 2 -> this shard's G planes (kept in `workspace`) and
+ *      kj [2][n] f32 = (K, J) partial sums over this shard's vocab rows, in bits (J: the loss sum of the
+ *      same shard: JSD sum p*log2(p/m), TVD sum |q - p|), 0 for masked rows.
+ *   3) caller all-gathers kj into kj_all [P][2][n] (8 B/token/rank).
+ *   4) kd_vocab_finish with the SAME problem, inputs and workspace (no other call on it in between): sums
+ *      kj_all in rank order (deterministic), writes the loss, the G fix-up, this shard's PARTIAL dh_s
+ *      (caller all-reduces SUM) and the local dW_s rows.
+ * Errors: KD_ERR_UNSUPPORTED for FKL/RKL (use kd_vocab_backward); others as kd_fused_fwd_bwd. */
+kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                            const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
+                            float* kj, void* workspace, size_t workspace_bytes, void* stream);
+kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                          const void* W_s, const uint8_t* mask, const float* kj_all, int32_t n_ranks,
+                          float* loss, float* dh_s_partial, float* dW_s, int64_t* n_nonfinite,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* Building block exposed for verification: D[M, N] = A · Bᵀ with bf16 operands and fp32 tcgen05
  * accumulation.  A is [M, K] (a_mn_major = 0) or stored transposed as [K, M] (a_mn_major = 1); B is

@@ -38,7 +38,9 @@ cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int ro
 cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, int kind, float beta,
                         float* kfin, float* loss, const int* idx, long long* nonfinite, const float* ga,
                         const float* gb, int g_ld, float scale, __nv_bfloat16* ghi, __nv_bfloat16* glo,
-                        int num_sms, cudaStream_t s);
+                        int num_sms, const float* kj_ranks, int n_ranks, long long N, cudaStream_t s);
+cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, const int* idx,
+                           float* kj, long long N, cudaStream_t s);
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
                              const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
                              int n_slots, const __nv_bfloat16* Ws, cudaStream_t s);
@@ -411,22 +413,30 @@ static int pass_grid(const Plan& P) {  // CTAs (a multiple of the CTA group)
   return (units < workers ? units : workers) * P.cg;
 }
 
-// pass 2 (+ JSD/TVD fix-up) + dh GEMM (+ split-K reduce) + dW GEMM for one chunk whose final per-token
-// statistics are already in fstats.
-static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW) {
+// pass 2 for one chunk whose final per-token statistics are already in fstats: G (FKL/RKL) or the two JSD/TVD
+// planes + partial K, J.
+static kd_status grad_chunk(Ctx& c, int row0) {
+  const Plan& P = c.P;
+  PassParams pp = pass_params(c, row0);
+  static const bool p2_coupled = env_int("KD_P2_COUPLED", 0) != 0;
+  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, p2_coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+  return KD_OK;
+}
+
+// After pass 2: [JSD/TVD fix-up with the local K partials, or with the P ranks' per-token totals kj_ranks]
+// + dh GEMM (+ split-K reduce) + dW GEMM for one chunk.
+static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW, const float* kj_ranks,
+                              int n_ranks) {
   const Plan& P = c.P;
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
-  const int grid = pass_grid(P);
-  static const bool p2_coupled = env_int("KD_P2_COUPLED", 0) != 0;
-  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, p2_coupled, P.cg, P.bn, c.maps, pp, grid, c.s));
   if (P.fix) {
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
                                                  : 0.5 * cscale);
     KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
-                          pp.g_hi, pp.g_lo, P.num_sms, c.s));
+                          pp.g_hi, pp.g_lo, P.num_sms, kj_ranks, n_ranks, (long long)P.N, c.s));
   }
   // dh_s rows of this chunk: [G_hi | G_lo] · W_s  (K = V_r); the scratch holds Gᵀ [g_ld][Nc], i.e. the A operand
   // [tokens, V] is MN-major; W_s [V_r, d_s] is the MN-major B operand.  Split-K slabs, then reduce + scatter.
@@ -474,6 +484,12 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
     KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, 2, EPI_ACCUM, gemm_cg(), &ma_hi, &ma_lo, &mh, wp, P.num_sms, c.s));
   }
   return KD_OK;
+}
+
+static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW) {
+  kd_status st = grad_chunk(c, row0);
+  if (st != KD_OK) return st;
+  return finish_chunk(c, row0, loss, dh, dW, nullptr, 0);
 }
 
 static kd_status check_common(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
@@ -547,8 +563,6 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = validate(p, false);
   if (st != KD_OK) return st;
-  if (p->kind != KD_FKL && p->kind != KD_RKL)
-    return fail(KD_ERR_UNSUPPORTED, "vocab-sharded mode supports FKL/RKL (JSD/TVD need a K exchange: NEXT)");
   Ctx c{};
   c.p = p;
   c.P = make_plan(p);
@@ -582,7 +596,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
   kd_status st = validate(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL && p->kind != KD_RKL)
-    return fail(KD_ERR_UNSUPPORTED, "vocab-sharded mode supports FKL/RKL (JSD/TVD need a K exchange: NEXT)");
+    return fail(KD_ERR_UNSUPPORTED, "JSD/TVD vocab shards need the K exchange: use kd_vocab_partials + kd_vocab_finish");
   if (n_ranks < 1) return fail(KD_ERR_INVALID_ARG, "n_ranks must be >= 1");
   Ctx c{};
   c.p = p;
@@ -609,6 +623,73 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
     if ((st = backward_chunk(c, row0, loss, dh_s_partial, dW)) != KD_OK) return st;
   }
   return KD_OK;
+}
+
+// JSD/TVD vocab shards (C2 exchange): one token chunk per call pair, the workspace carrying the chunk's G planes
+// from kd_vocab_partials to kd_vocab_finish.
+static kd_status vocab_fix_setup(Ctx& c, const kd_problem* p, void* workspace, size_t workspace_bytes, void* stream,
+                                 int32_t n_ranks) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = validate(p, false);
+  if (st != KD_OK) return st;
+  if (p->kind != KD_JSD && p->kind != KD_TVD)
+    return fail(KD_ERR_UNSUPPORTED, "kd_vocab_partials/finish are the JSD/TVD shard path; FKL/RKL use kd_vocab_backward");
+  if (n_ranks < 1) return fail(KD_ERR_INVALID_ARG, "n_ranks must be >= 1");
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  if (c.P.n_chunks > 1)
+    return fail(KD_ERR_SHAPE, "JSD/TVD vocab shards run one token chunk per call: n_tokens (%d) must be <= the chunk (%d)",
+                c.P.N, c.P.Nc);
+  if (!workspace || workspace_bytes < c.P.total) return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+  return KD_OK;
+}
+
+kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                            const uint8_t* mask, const float* recs, int32_t n_ranks, float* kj, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  Ctx c{};
+  kd_status st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, n_ranks);
+  if (st != KD_OK) return st;
+  const Plan& P = c.P;
+  if (P.N == 0) return KD_OK;
+  if (!recs || !kj) return fail(KD_ERR_INVALID_ARG, "recs / kj is NULL");
+  if (!aligned16(kj)) return fail(KD_ERR_ALIGNMENT, "kj must be 16-byte aligned");
+  if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
+  KD_CUDA(cudaMemsetAsync(kj, 0, (size_t)2 * P.N * sizeof(float), c.s));
+  KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, 0, c.n_eff, P.kind, 0,
+                                  ws_at<float>(c.ws, P.off_fstats), nullptr, nullptr, 0, c.idx, 1, c.nonfinite, 0, c.s));
+  if ((st = grad_chunk(c, 0)) != KD_OK) return st;
+  PassParams pp = pass_params(c, 0);
+  KD_LAUNCH(K_KFIX, launch_kj_rows(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, 0, c.n_eff, c.idx, kj,
+                                   (long long)P.N, c.s));
+  return KD_OK;
+}
+
+kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                          const uint8_t* mask, const float* kj_all, int32_t n_ranks, float* loss,
+                          float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  Ctx c{};
+  kd_status st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, n_ranks);
+  if (st != KD_OK) return st;
+  const Plan& P = c.P;
+  float* dW = p->want_dW ? dW_s : nullptr;
+  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s_partial, dW, workspace, workspace_bytes, P)) != KD_OK)
+    return st;
+  if (dW && !p->accumulate_dW) KD_CUDA(cudaMemsetAsync(dW, 0, (size_t)P.V_r * P.d_s * 4, c.s));
+  if (P.N == 0) {
+    if (n_nonfinite) KD_CUDA(cudaMemsetAsync(n_nonfinite, 0, 8, c.s));
+    return KD_OK;
+  }
+  if (!kj_all) return fail(KD_ERR_INVALID_ARG, "kj_all is NULL");
+  // the prologue is deterministic in the inputs: it rebuilds the same row compaction / packed rows that
+  // kd_vocab_partials used, leaving the chunk's G planes in the workspace untouched
+  if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
+  return finish_chunk(c, 0, loss, dh_s_partial, dW, kj_all, n_ranks);
 }
 
 kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,

@@ -179,27 +179,57 @@ __global__ void k_zero_records(const uint8_t* __restrict__ mask, int N, float* _
 }
 
 // ------------------------------------------------------------------ A3b: JSD / TVD
+// Per-row K (and the loss from K, J).  Local mode (kj_ranks == NULL): sum this call's per-(unit, part) partials
+// kpart [2][n_split][n_rows].  Vocab-shard mode: sum the P ranks' per-token totals kj_ranks [P][2][N] (original
+// row index) in rank order — the C2 exchange of SURVEY §8(e), deterministic for a fixed P.
 __global__ void __launch_bounds__(256) k_kfix_rows(const float* __restrict__ kpart, int n_split, int n_rows, int row0,
                                                    const int* __restrict__ n_eff, int kind, float beta,
                                                    float* __restrict__ kfin, float* __restrict__ loss,
-                                                   const int* __restrict__ idx, long long* __restrict__ nonfinite) {
+                                                   const int* __restrict__ idx, long long* __restrict__ nonfinite,
+                                                   const float* __restrict__ kj_ranks, int n_ranks, long long N) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int valid = min(n_rows, *n_eff - row0);
   if (r >= n_rows) return;
   if (r >= valid) { kfin[r] = 0.f; return; }
+  const int orow = idx ? idx[row0 + r] : row0 + r;
+  float K = 0.f, J = 0.f;
+  if (kj_ranks) {
+    for (int q = 0; q < n_ranks; ++q) {
+      K += kj_ranks[(size_t)q * 2 * N + orow];
+      J += kj_ranks[(size_t)q * 2 * N + N + orow];
+    }
+  } else {
+    const size_t plane = (size_t)n_split * n_rows;
+    for (int s = 0; s < n_split; ++s) {
+      K += kpart[(size_t)s * n_rows + r];
+      J += kpart[plane + (size_t)s * n_rows + r];
+    }
+  }
+  kfin[r] = K;
+  float ell;
+  if (kind == KIND_JSD) ell = kLn2 * (beta * J + (1.f - beta) * K);  // K, J in bits
+  else ell = 0.5f * J;
+  loss[orow] = ell;
+  if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
+}
+
+// This shard's per-token (K, J) totals for the C2 exchange: kj [2][N] at the original row, summed over the
+// call's (unit, part) partials in slot order.  Rows not visited (masked) stay as the caller zeroed them.
+__global__ void __launch_bounds__(256) k_kj_rows(const float* __restrict__ kpart, int n_split, int n_rows, int row0,
+                                                 const int* __restrict__ n_eff, const int* __restrict__ idx,
+                                                 float* __restrict__ kj, long long N) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int valid = min(n_rows, *n_eff - row0);
+  if (r >= valid) return;
   float K = 0.f, J = 0.f;
   const size_t plane = (size_t)n_split * n_rows;
   for (int s = 0; s < n_split; ++s) {
     K += kpart[(size_t)s * n_rows + r];
     J += kpart[plane + (size_t)s * n_rows + r];
   }
-  kfin[r] = K;
-  float ell;
-  if (kind == KIND_JSD) ell = kLn2 * (beta * J + (1.f - beta) * K);  // K, J in bits
-  else ell = 0.5f * J;
   const int orow = idx ? idx[row0 + r] : row0 + r;
-  loss[orow] = ell;
-  if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
+  kj[orow] = K;
+  kj[N + orow] = J;
 }
 
 // G = scale·(G_a − K_r·G_b) -> split bf16, over the transposed scratch [g_ld][n_rows]: element (v, r) at v*n_rows + r,
@@ -356,10 +386,15 @@ cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long lon
 cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, int kind, float beta,
                         float* kfin, float* loss, const int* idx, long long* nonfinite, const float* ga,
                         const float* gb, int g_ld, float scale, __nv_bfloat16* ghi, __nv_bfloat16* glo,
-                        int num_sms, cudaStream_t s) {
+                        int num_sms, const float* kj_ranks, int n_ranks, long long N, cudaStream_t s) {
   k_kfix_rows<<<(n_rows + 255) / 256, 256, 0, s>>>(kpart, n_split, n_rows, row0, n_eff, kind, beta, kfin, loss, idx,
-                                                    nonfinite);
+                                                    nonfinite, kj_ranks, n_ranks, N);
   k_kfix_apply<<<num_sms * 8, 256, 0, s>>>(ga, gb, kfin, g_ld, n_rows, row0, n_eff, scale, ghi, glo);
+  return cudaGetLastError();
+}
+cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, const int* idx,
+                           float* kj, long long N, cudaStream_t s) {
+  k_kj_rows<<<(n_rows + 255) / 256, 256, 0, s>>>(kpart, n_split, n_rows, row0, n_eff, idx, kj, N);
   return cudaGetLastError();
 }
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,

@@ -19,7 +19,8 @@ LIB_PATH = os.environ.get("KD_LIB_PATH") or os.path.join(_HERE, "libkdfused.so")
 KINDS = {"fkl": 0, "rkl": 1, "jsd": 2, "tvd": 3}
 STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALIGNMENT", 4: "KD_ERR_UNSUPPORTED",
           5: "KD_ERR_WORKSPACE_TOO_SMALL", 6: "KD_ERR_CUDA"}
-EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward", "kd_gemm_bf16_f32",
+EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward",
+            "kd_vocab_partials", "kd_vocab_finish", "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
             "kd_last_error", "kd_abi_version")
 
@@ -62,6 +63,10 @@ def lib() -> ctypes.CDLL:
     L.kd_vocab_stats.restype = ctypes.c_int
     L.kd_vocab_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
     L.kd_vocab_backward.restype = ctypes.c_int
+    L.kd_vocab_partials.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, sz, vp]
+    L.kd_vocab_partials.restype = ctypes.c_int
+    L.kd_vocab_finish.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
+    L.kd_vocab_finish.restype = ctypes.c_int
     L.kd_gemm_bf16_f32.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     L.kd_gemm_bf16_f32.restype = ctypes.c_int
     L.kd_last_launch_count.restype = ctypes.c_int32
@@ -229,6 +234,60 @@ def vocab_backward(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, vocab, v_
                                    _ptr(mask), _ptr(recs), int(recs.shape[0]), _ptr(loss), _ptr(dh),
                                    _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),
                                    _stream_handle(stream)))
+    return KDResult(loss, dh, dW_s if want_dW else None, nnf)
+
+
+@dataclass
+class VocabFixState:
+    """What kd_vocab_partials leaves for kd_vocab_finish: the problem and the workspace holding the chunk's
+    G planes (a private buffer, so no other call can reuse it in between)."""
+    problem: KDProblem
+    workspace: torch.Tensor
+
+
+def vocab_partials(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, vocab, v_begin, T=1.0, kind="jsd",
+                   beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False, chunk_tokens=0,
+                   stream=None):
+    """kd_vocab_partials (JSD/TVD shards, one token chunk): -> (kj [2, N] this shard's (K, J) partials, state)."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(x, "input") for x in (h_t, W_t_shard, h_s, W_s_shard))
+    N, d_t = h_t.shape
+    V_r, d_s = W_s_shard.shape
+    dev = h_t.device
+    p = make_problem(N, d_t, d_s, vocab, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, v_begin=v_begin, v_end=v_begin + V_r,
+                     chunk_tokens=chunk_tokens or max(N, 1))
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    recs = recs.to(device=dev, dtype=torch.float32).contiguous()
+    kj = torch.empty(2, N, dtype=torch.float32, device=dev)
+    ws = torch.empty(max(workspace_size(p), 256), dtype=torch.uint8, device=dev)
+    _check(lib().kd_vocab_partials(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                   _ptr(mask), _ptr(recs), int(recs.shape[0]), _ptr(kj), _ptr(ws), ws.numel(),
+                                   _stream_handle(stream)))
+    return kj, VocabFixState(p, ws)
+
+
+def vocab_finish(state: VocabFixState, h_t, W_t_shard, h_s, W_s_shard, kj_all, mask=None, *, dW_s=None,
+                 stream=None) -> KDResult:
+    """kd_vocab_finish: sum the [P, 2, N] (K, J) partials in rank order; loss, PARTIAL dh_s, local dW_s."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(x, "input") for x in (h_t, W_t_shard, h_s, W_s_shard))
+    p = state.problem
+    N, d_s = int(p.n_tokens), int(p.d_s)
+    V_r = int(p.v_end - p.v_begin)
+    dev = h_t.device
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    kj_all = kj_all.to(device=dev, dtype=torch.float32).contiguous()
+    loss = torch.empty(N, dtype=torch.float32, device=dev)
+    dh = torch.empty(N, d_s, dtype=torch.float32, device=dev)
+    nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    want_dW = bool(p.want_dW)
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if p.accumulate_dW else torch.empty)(V_r, d_s, dtype=torch.float32, device=dev)
+    _check(lib().kd_vocab_finish(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                 _ptr(mask), _ptr(kj_all), int(kj_all.shape[0]), _ptr(loss), _ptr(dh),
+                                 _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(state.workspace),
+                                 state.workspace.numel(), _stream_handle(stream)))
     return KDResult(loss, dh, dW_s if want_dW else None, nnf)
 
 

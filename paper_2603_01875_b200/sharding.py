@@ -8,9 +8,12 @@ alongside"):
 * vocabulary sharding — rank r owns LM-head rows [v0, v1) (128-row granules; V = 151936 = 128·1187) and
   every token.  Exchanges: (1) all-gather of the per-token pass-1 records (20 B/token/rank), merged in rank
   order by the kernels (deterministic); (2) all-reduce SUM of the partial dL/dh_s.  dW_s rows stay local.
+  JSD/TVD add (1b): all-gather of the per-token (K, J) partials (8 B/token/rank) between the shards'
+  pass 2 and the gradient fix-up, token chunk by token chunk.
 
 The collectives go through ``torch.distributed`` (NCCL over NVLink on the GPU box; gloo in the CPU tests);
-the kernels on either side are the library's (``kd_vocab_stats`` / ``kd_vocab_backward``).
+the kernels on either side are the library's (``kd_vocab_stats`` / ``kd_vocab_backward``, and for JSD/TVD
+``kd_vocab_partials`` / ``kd_vocab_finish``).
 """
 from __future__ import annotations
 
@@ -44,14 +47,73 @@ def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
     return torch.stack(out)
 
 
+def gather_kj(kj: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather this rank's [2, n] (K, J) partials into [P, 2, n] in rank order."""
+    world = dist.get_world_size(group)
+    out = [torch.empty_like(kj) for _ in range(world)]
+    dist.all_gather(out, kj.contiguous(), group=group)
+    return torch.stack(out)
+
+
+class _Result:
+    def __init__(self, loss, dh_s, dW_s):
+        self.loss, self.dh_s, self.dW_s = loss, dh_s, dW_s
+
+
+def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, group, T, kind, beta, loss_scale,
+                       want_dW, accumulate_dW, dW_s, chunk_tokens, stats_fn, partials_fn, finish_fn):
+    """JSD/TVD: per token chunk, records all-gather -> partials -> (K, J) all-gather -> finish."""
+    N = h_t.shape[0]
+    d_s = W_s_shard.shape[1]
+    chunk = chunk_tokens if chunk_tokens > 0 else 2048
+    loss = dh = None
+    for a in range(0, N, chunk):
+        b = min(N, a + chunk)
+        ht_c, hs_c = h_t[a:b], h_s[a:b]
+        m_c = None if mask is None else mask[a:b]
+        rec = stats_fn(ht_c, W_t_shard, hs_c, W_s_shard, m_c, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
+                       chunk_tokens=b - a)
+        recs = gather_records(rec, group)
+        acc = accumulate_dW or a > 0  # later chunks add into the first chunk's dW_s
+        kj, state = partials_fn(ht_c, W_t_shard, hs_c, W_s_shard, recs, m_c, vocab=vocab, v_begin=v_begin, T=T,
+                                kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=acc,
+                                chunk_tokens=b - a)
+        kj_all = gather_kj(kj, group)
+        r = finish_fn(state, ht_c, W_t_shard, hs_c, W_s_shard, kj_all, m_c, dW_s=dW_s)
+        if loss is None:  # outputs in the kernels' dtype (fp32; the CPU test stand-ins return fp64)
+            loss = torch.zeros(N, dtype=r.loss.dtype, device=r.loss.device)
+            dh = torch.zeros(N, d_s, dtype=r.dh_s.dtype, device=r.dh_s.device)
+        loss[a:b] = r.loss
+        dh[a:b] = r.dh_s
+        if want_dW:
+            dW_s = r.dW_s
+    if dh is None:  # no tokens
+        loss = torch.zeros(0, dtype=torch.float32, device=h_t.device)
+        dh = torch.zeros(0, d_s, dtype=torch.float32, device=h_t.device)
+    dist.all_reduce(dh, op=dist.ReduceOp.SUM, group=group)
+    return _Result(loss, dh, dW_s if want_dW else None)
+
+
 def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
-                          T=1.0, kind="fkl", loss_scale=1.0, want_dW=False, accumulate_dW=False, dW_s=None,
-                          chunk_tokens=0, stats_fn: Callable | None = None, backward_fn: Callable | None = None):
+                          T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False,
+                          dW_s=None, chunk_tokens=0, stats_fn: Callable | None = None,
+                          backward_fn: Callable | None = None, partials_fn: Callable | None = None,
+                          finish_fn: Callable | None = None):
     """One vocab-sharded step on this rank; returns a KDResult whose dh_s is the full (all-reduced) gradient.
 
-    ``stats_fn`` / ``backward_fn`` default to the CUDA entry points; tests substitute CPU stand-ins to
+    The kernel-side callables default to the CUDA entry points; tests substitute CPU stand-ins to
     exercise this exchange logic under gloo.
     """
+    if kind in ("jsd", "tvd"):
+        if stats_fn is None or partials_fn is None or finish_fn is None:
+            from . import kdfused
+            stats_fn = stats_fn or kdfused.vocab_stats
+            partials_fn = partials_fn or kdfused.vocab_partials
+            finish_fn = finish_fn or kdfused.vocab_finish
+        return _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, vocab=vocab, v_begin=v_begin, group=group,
+                                  T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                                  accumulate_dW=accumulate_dW, dW_s=dW_s, chunk_tokens=chunk_tokens,
+                                  stats_fn=stats_fn, partials_fn=partials_fn, finish_fn=finish_fn)
     if stats_fn is None or backward_fn is None:
         from . import kdfused
         stats_fn = stats_fn or kdfused.vocab_stats

@@ -97,9 +97,17 @@ def test_vocab_range_and_unsupported():
     p = kd.make_problem(16, 64, 64, 1000, v_begin=0, v_end=500)
     rc = L.kd_fused_fwd_bwd(ctypes.byref(p), *([None] * 10), 0, None)
     assert rc == 2 and b"kd_vocab" in L.kd_last_error()
+    # JSD/TVD shards go through kd_vocab_partials / kd_vocab_finish (the (K, J) exchange), FKL/RKL do not
     pj = kd.make_problem(16, 64, 64, 1000, kind="jsd", v_begin=0, v_end=500)
-    rc = L.kd_vocab_stats(ctypes.byref(pj), *([None] * 7), 0, None)
+    rc = L.kd_vocab_backward(ctypes.byref(pj), *([None] * 6), 1, *([None] * 5), 0, None)
+    assert rc == 4 and b"kd_vocab_partials" in L.kd_last_error()
+    pf = kd.make_problem(16, 64, 64, 1000, kind="fkl", v_begin=0, v_end=500)
+    rc = L.kd_vocab_partials(ctypes.byref(pf), *([None] * 6), 1, None, None, 0, None)
     assert rc == 4
+    # one token chunk per JSD/TVD shard call: more tokens than the chunk is a shape error, before any launch
+    pc = kd.make_problem(4096, 64, 64, 1000, kind="tvd", v_begin=0, v_end=500, chunk_tokens=1024)
+    rc = L.kd_vocab_partials(ctypes.byref(pc), *([None] * 6), 1, None, None, 0, None)
+    assert rc == 2 and b"chunk" in L.kd_last_error()
 
 
 def test_no_cpu_fallback_in_binding():

@@ -293,3 +293,43 @@ def test_vocab_sharded_equals_single(P, kind):
     assert_kd_close("loss", losses[0].cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
     assert_grad_close("dh_s", dh.cpu().numpy(), dh_ref)
     assert_grad_close("dW_s", dW.cpu().numpy(), dW_ref)
+
+
+@pytest.mark.parametrize("P,kind,chunk", [(2, "jsd", 0), (3, "tvd", 0), (4, "jsd", 256)])
+def test_vocab_sharded_jsd_tvd_equals_single(P, kind, chunk):
+    """JSD/TVD vocab shards: per token chunk, records all-gathered -> kd_vocab_partials -> (K, J) partials
+    all-gathered -> kd_vocab_finish (rank-order sums), partial dh summed; equals the oracle.  chunk=256 drives
+    three token chunks (the per-chunk protocol sharding.py runs)."""
+    from paper_2603_01875_b200.sharding import vocab_shard_bounds
+    N, d_t, d_s, V = 520, 256, 128, 5000
+    mask = (np.random.default_rng(P).random(N) > 0.2).astype(np.uint8)
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=40 + P, mask=mask)
+    Ht, Hs, Wt, Ws = dev_bf16(inp.H_t), dev_bf16(inp.H_s), dev_bf16(inp.W_t), dev_bf16(inp.W_s)
+    m = torch.from_numpy(mask).cuda()
+    bounds = vocab_shard_bounds(V, P)
+    step = chunk or N
+    dh = torch.zeros(N, d_s, device="cuda")
+    dW = torch.zeros(V, d_s, device="cuda")
+    loss = torch.zeros(N, device="cuda")
+    for t0 in range(0, N, step):
+        t1 = min(N, t0 + step)
+        sl = slice(t0, t1)
+        recs = torch.stack([kd().vocab_stats(Ht[sl], Wt[a:b], Hs[sl], Ws[a:b], m[sl], vocab=V, v_begin=a, T=2.0,
+                                             kind=kind, chunk_tokens=t1 - t0) for a, b in bounds])
+        parts = [kd().vocab_partials(Ht[sl], Wt[a:b], Hs[sl], Ws[a:b], recs, m[sl], vocab=V, v_begin=a, T=2.0,
+                                     kind=kind, beta=0.5, want_dW=True, accumulate_dW=t0 > 0)
+                 for a, b in bounds]
+        kj_all = torch.stack([kj for kj, _ in parts])
+        losses = []
+        for (a, b), (_, st) in zip(bounds, parts):
+            r = kd().vocab_finish(st, Ht[sl], Wt[a:b], Hs[sl], Ws[a:b], kj_all, m[sl], dW_s=dW[a:b])
+            dh[sl] += r.dh_s
+            losses.append(r.loss)
+        for l in losses[1:]:
+            assert torch.equal(l, losses[0])  # every rank sums the same (K, J) partials in the same order
+        loss[sl] = losses[0]
+    torch.cuda.synchronize()
+    loss_ref, dh_ref, dW_ref = oracle_run(inp, T=2.0, kind=kind, beta=0.5, want_dW=True)
+    assert_kd_close("loss", loss.cpu().numpy(), loss_ref, LOSS_RTOL, LOSS_ATOL)
+    assert_grad_close("dh_s", dh.cpu().numpy(), dh_ref)
+    assert_grad_close("dW_s", dW.cpu().numpy(), dW_ref)

@@ -70,6 +70,68 @@ def _backward_standin(h_t, Wt, h_s, Ws, recs, mask, *, vocab, v_begin, T, kind, 
     return _R(torch.tensor(ell), dh, dW)
 
 
+class _FixState:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def _probs(h_t, Wt, h_s, Ws, recs, mask, T, kind):
+    from oracle.kd_blockwise import merge
+    R = None
+    for r in recs:  # rank order
+        rr = tuple(x.numpy() for x in r)
+        if np.all(rr[2] == 0):
+            continue
+        R = rr if R is None else merge(R, rr)
+    m = np.ones(recs.shape[-1]) if mask is None else mask.numpy().astype(np.float64)
+    live = m > 0
+    m_p, m_q, S_p, S_q, _ = (np.where(live, x, 1.0) for x in R)
+    lse_t, lse_s = m_p + np.log(S_p), m_q + np.log(S_q)
+    lp = h_t.double().numpy() @ Wt.double().numpy().T / T - lse_t[:, None]
+    lq = h_s.double().numpy() @ Ws.double().numpy().T / T - lse_s[:, None]
+    return live, lp, lq
+
+
+def _partials_standin(h_t, Wt, h_s, Ws, recs, mask, *, vocab, v_begin, T, kind, beta, loss_scale, want_dW,
+                      accumulate_dW, chunk_tokens):
+    live, lp, lq = _probs(h_t, Wt, h_s, Ws, recs, mask, T, kind)
+    p, q = np.exp(lp), np.exp(lq)
+    if kind == "jsd":
+        lm = np.log(beta * p + (1 - beta) * q)
+        K = (q * (lq - lm)).sum(1) / np.log(2)   # bits, like the kernels
+        J = (p * (lp - lm)).sum(1) / np.log(2)
+    else:
+        s = np.sign(q - p)
+        K = (q * s).sum(1)
+        J = np.abs(q - p).sum(1)
+    kj = torch.tensor(np.stack([np.where(live, K, 0.0), np.where(live, J, 0.0)]))
+    st = _FixState(live=live, p=p, q=q, lp=lp, lq=lq, beta=beta, T=T, kind=kind, loss_scale=loss_scale,
+                   want_dW=want_dW, accumulate_dW=accumulate_dW)
+    return kj, st
+
+
+def _finish_standin(st, h_t, Wt, h_s, Ws, kj_all, mask, *, dW_s=None):
+    K = kj_all[:, 0].numpy().sum(0)   # rank order
+    J = kj_all[:, 1].numpy().sum(0)
+    c = st.loss_scale / st.T
+    if st.kind == "jsd":
+        lm = np.log(st.beta * st.p + (1 - st.beta) * st.q)
+        G = c * (1 - st.beta) * st.q * ((st.lq - lm) - K[:, None] * np.log(2))
+        ell = np.log(2) * (st.beta * J + (1 - st.beta) * K)
+    else:
+        G = 0.5 * c * st.q * (np.sign(st.q - st.p) - K[:, None])
+        ell = 0.5 * J
+    G = np.where(st.live[:, None], G, 0.0)
+    ell = np.where(st.live, ell, 0.0)
+    dh = torch.tensor(G @ Ws.double().numpy())
+    dW = None
+    if st.want_dW:
+        dW = torch.tensor(G.T @ h_s.double().numpy())
+        if st.accumulate_dW and dW_s is not None:
+            dW = dW_s + dW
+    return _R(torch.tensor(ell), dh, dW)
+
+
 def _worker(rank, world, port, kind, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -83,21 +145,24 @@ def _worker(rank, world, port, kind, q):
         Wt = torch.tensor(KI.bf16_to_f64(inp.W_t))
         Ws = torch.tensor(KI.bf16_to_f64(inp.W_s))
         a, b = vocab_shard_bounds(V, world, granule=16)[rank]
+        # JSD/TVD: chunk_tokens=16 drives three token chunks through the (K, J) exchange
         r = vocab_sharded_fwd_bwd(ht, Wt[a:b], hs, Ws[a:b], torch.tensor(mask), vocab=V, v_begin=a, T=1.3,
-                                  kind=kind, want_dW=True, stats_fn=_stats_standin, backward_fn=_backward_standin)
+                                  kind=kind, beta=0.3, want_dW=True, chunk_tokens=16, stats_fn=_stats_standin,
+                                  backward_fn=_backward_standin, partials_fn=_partials_standin,
+                                  finish_fn=_finish_standin)
         # token-sharded dW: each rank's partial sum over its tokens, reduced
         t0, t1 = token_shard_bounds(N, world)[rank]
         from oracle.kd_oracle import kd_fused_fwd_bwd
         sl = slice(t0, t1)
         _, _, dW_part = kd_fused_fwd_bwd(ht.numpy()[sl], Wt.numpy(), hs.numpy()[sl], Ws.numpy(), mask[sl],
-                                         T=1.3, kind=kind, want_dW=True)
+                                         T=1.3, kind=kind, beta=0.3, want_dW=True)
         dW_tok = token_sharded_dW_reduce(torch.tensor(dW_part))
         q.put((rank, r.loss.numpy(), r.dh_s.numpy(), (a, b, r.dW_s.numpy()), dW_tok.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["fkl", "rkl"])
+@pytest.mark.parametrize("kind", ["fkl", "rkl", "jsd", "tvd"])
 def test_vocab_and_token_sharding_world2(kind):
     import kd_inputs as KI
     from oracle.kd_oracle import kd_fused_fwd_bwd
@@ -117,7 +182,7 @@ def test_vocab_and_token_sharding_world2(kind):
     inp = KI.make_inputs(N, d_t, d_s, V, seed=4, mask=mask)
     f = KI.bf16_to_f64
     loss, dh, dW = kd_fused_fwd_bwd(f(inp.H_t), f(inp.W_t), f(inp.H_s), f(inp.W_s), mask, T=1.3, kind=kind,
-                                    want_dW=True)
+                                    beta=0.3, want_dW=True)
     dW_cat = np.zeros_like(dW)
     for rank, l, d, (a, b, dws), dW_tok in res:
         np.testing.assert_allclose(l, loss, rtol=1e-12, atol=1e-13)
