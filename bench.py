@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(KI.CONFIGS))
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU (default: the config's)")
     ap.add_argument("--dW", action="store_true", help="also compute dL/dW_s")
+    ap.add_argument("--grad-precision", default="split", choices=["split", "bf16"],
+                    help="G fed to the backward GEMMs: split hi+lo bf16 (parity-grade, default) or one bf16 plane "
+                         "(KD_GRAD_BF16, fast, not within the north-star gradient tolerance)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=128)
@@ -61,17 +64,18 @@ def peaks():
     return d
 
 
-def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int):
+def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_precision: str = "split"):
     mask_desc = {"none": "all ones", "prompt_pad": "prompt L_p~U[64,512] + padding beyond L~U[2048,4096] masked",
                  "ragged": "ragged L~U[256,8192], prompt L_p~U[32,min(512,L/2)] masked"}[cfg.mask]
     heads_b = cfg.vocab * (cfg.d_t + cfg.d_s) * 2
     return {
         "workload": f"{cfg.name}: d_t={cfg.d_t} -> d_s={cfg.d_s}, V={cfg.vocab}, {n_tok} tokens/GPU, "
-                    f"{cfg.kind.upper()} T={cfg.temperature:g}" + (" +dW_s" if want_dW else ""),
+                    f"{cfg.kind.upper()} T={cfg.temperature:g}" + (" +dW_s" if want_dW else "")
+                    + (" [G: one bf16 plane]" if grad_precision == "bf16" else ""),
         "baseline_config": cfg.notes,
         "tokens_per_gpu": n_tok, "d_t": cfg.d_t, "d_s": cfg.d_s, "vocab": cfg.vocab, "kind": cfg.kind,
         "temperature": cfg.temperature, "jsd_beta": cfg.jsd_beta if cfg.kind == "jsd" else None,
-        "want_dW": want_dW, "mask": mask_desc,
+        "want_dW": want_dW, "mask": mask_desc, "grad_precision": grad_precision,
         "parallelism": f"token-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU",
         "l2": f"no flush: resident inputs {heads_b / 1e9:.2f} GB heads + {n_tok * (cfg.d_t + cfg.d_s) * 2 / 1e9:.2f} GB "
               f"hidden > {L2_BYTES / 2 ** 20:.0f} MiB L2",
@@ -208,7 +212,7 @@ def main():
     n_eff = int(mask_np.sum()) if mask_np is not None else n_tok
     del W_t, W_s
     kw = dict(T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0, want_dW=want_dW,
-              accumulate_dW=False)
+              accumulate_dW=False, grad_precision=args.grad_precision)
     out = kd.KDResult(torch.empty(n_tok, dtype=torch.float32, device=dev),
                       torch.empty(n_tok, cfg.d_s, dtype=torch.float32, device=dev), None,
                       torch.zeros(1, dtype=torch.int64, device=dev))
@@ -262,7 +266,8 @@ def main():
     flops_pass = 2.0 * n_eff * cfg.vocab * (cfg.d_t + cfg.d_s)  # both LM-head GEMMs, one vocab sweep
     flops_g = 2.0 * n_eff * cfg.vocab * cfg.d_s                   # G · W_s  (or Gᵀ · H_s)
     algo = {"pass1": flops_pass, "pass2": flops_pass, "gemm_dh": flops_g, "gemm_dW": flops_g}
-    exec_mult = {"pass1": 1.0, "pass2": 1.0, "gemm_dh": 2.0, "gemm_dW": 2.0}   # split-bf16 G: 2 MMAs
+    gm = 2.0 if args.grad_precision == "split" else 1.0                 # split-bf16 G: 2 MMAs per product
+    exec_mult = {"pass1": 1.0, "pass2": 1.0, "gemm_dh": gm, "gemm_dW": gm}
     kernels = {}
     total_ms = sum(t for _, t in prof.values()) or 1.0
     for name, (n, t) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
@@ -361,7 +366,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kd_inputs recipe, seeded)",
-                "config": workload_desc(cfg, n_tok, want_dW, world), "clocks": clocks, "e2e": e2e,
+                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision), "clocks": clocks, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "roofline": roofline, "cpu_baseline": cpu,
                 "useful_flop_frac": useful_frac, "kernels": kernels, "nonfinite_tokens": nonfinite,
                 "tokens_loss_bearing_per_gpu": n_eff}

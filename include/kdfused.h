@@ -55,6 +55,14 @@ typedef enum {
   KD_ERR_CUDA = 6                 /* a CUDA runtime/driver call failed (message in kd_last_error) */
 } kd_status;
 
+/* Precision of the logit gradient G fed to the backward GEMMs.
+ *   KD_GRAD_SPLIT_BF16 (default, parity-grade): G = hi + lo, two bf16 planes (<= 2^-16 relative) and two MMAs
+ *     per product; the largest entries' exact residuals are added back (R11).
+ *   KD_GRAD_BF16 (fast): one bf16 plane (<= 2^-8 relative per element; the residual fix still restores the
+ *     largest entries exactly), half the backward tensor work.  NOT within the north-star gradient
+ *     tolerance in general (tests/test_gpu_full.py measures it against the oracle with its own bound). */
+typedef enum { KD_GRAD_SPLIT_BF16 = 0, KD_GRAD_BF16 = 1 } kd_grad_precision;
+
 /* Problem description (plain data, no pointers). */
 typedef struct {
   int64_t n_tokens;      /* N: packed token rows (ragged sequences concatenated by the caller), >= 0 */
@@ -71,7 +79,8 @@ typedef struct {
   int32_t accumulate_dW; /* 1: dW_s += (gradient accumulation, P:210 GA=8); 0: dW_s = */
   int32_t chunk_tokens;  /* token chunk Nc bounding the G scratch (0 = default: ~24 MiB of H_t|H_s rows, clamped to
                             [1024, 8192], so the chunk stays L2-resident; rounded up to the 256-row pair tile) */
-  int32_t reserved[5];   /* must be zero */
+  int32_t grad_precision;/* kd_grad_precision: how G reaches the backward GEMMs */
+  int32_t reserved[4];   /* must be zero */
 } kd_problem;
 
 /* Host-only validation of `p` (no CUDA call): the status kd_fused_fwd_bwd / kd_vocab_* would return for

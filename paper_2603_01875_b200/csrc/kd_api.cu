@@ -192,6 +192,7 @@ struct Plan {
   int cg;  // CTA group of the fused passes: 2 = SM pairs (UMMA M=256), 1 = single SMs
   int bn;  // vocab tile of the fused passes (UMMA N): 256 or 128
   bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
+  int g_planes;  // bf16 planes of G fed to the backward GEMMs: 2 (split hi + lo) or 1 (KD_GRAD_BF16)
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
       off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, off_zscr, total;
 };
@@ -242,8 +243,10 @@ static int choose_k_split(int m_tiles, int n_tiles, int kbs, int workers, long l
 
 static kd_status validate(const kd_problem* p, bool require_full_vocab) {
   if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
-  for (int i = 0; i < 5; ++i)
+  for (int i = 0; i < 4; ++i)
     if (p->reserved[i] != 0) return fail(KD_ERR_INVALID_ARG, "reserved fields must be zero");
+  if (p->grad_precision != KD_GRAD_SPLIT_BF16 && p->grad_precision != KD_GRAD_BF16)
+    return fail(KD_ERR_INVALID_ARG, "unknown grad_precision %d", p->grad_precision);
   if (!(p->temperature > 0.f) || !std::isfinite(p->temperature))
     return fail(KD_ERR_INVALID_ARG, "temperature must be finite and > 0 (got %g)", (double)p->temperature);
   if (p->kind < KD_FKL || p->kind > KD_TVD) return fail(KD_ERR_INVALID_ARG, "unknown divergence kind %d", p->kind);
@@ -271,6 +274,7 @@ static Plan make_plan(const kd_problem* p) {
   P.V_r = (int)(p->v_end - p->v_begin);
   P.kind = p->kind;
   P.fix = (p->kind == KD_JSD || p->kind == KD_TVD);
+  P.g_planes = p->grad_precision == KD_GRAD_BF16 ? 1 : 2;
   P.num_sms = device_sms();
   P.cg = cta_group();
   P.bn = pass_bn();
@@ -308,7 +312,7 @@ static Plan make_plan(const kd_problem* p) {
   P.off_kpart = take((P.fix || P.kind == KD_FKL) ? (size_t)2 * P.n_split * epi_parts(2, P.kind) * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
   P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
-  P.off_glo = take((size_t)P.Nc * P.g_ld * 2);
+  P.off_glo = take(P.g_planes == 2 ? (size_t)P.Nc * P.g_ld * 2 : 0);
   P.off_ga = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_gb = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
@@ -393,7 +397,7 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.gscale = (float)(p->kind == KD_RKL ? cscale * 0.6931471805599453 : cscale);
   pp.beta = p->jsd_beta;
   pp.g_hi = ws_at<__nv_bfloat16>(c.ws, P.off_ghi);
-  pp.g_lo = ws_at<__nv_bfloat16>(c.ws, P.off_glo);
+  pp.g_lo = P.g_planes == 2 ? ws_at<__nv_bfloat16>(c.ws, P.off_glo) : nullptr;
   pp.g_a = P.fix ? ws_at<float>(c.ws, P.off_ga) : nullptr;
   pp.g_b = P.fix ? ws_at<float>(c.ws, P.off_gb) : nullptr;
   pp.g_ld = P.g_ld;
@@ -443,7 +447,8 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
   CUtensorMap mg_hi, mg_lo, mw;
   kd_status st;
   if ((st = make_map(&mg_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK) return st;
-  if ((st = make_map(&mg_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK) return st;
+  if (P.g_planes == 2 && (st = make_map(&mg_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK)
+    return st;
   if ((st = make_map(&mw, c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK) return st;
   GemmParams gp{};
   gp.M = P.Nc;
@@ -457,7 +462,8 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
   gp.out = ws_at<float>(c.ws, P.off_dhp);
   gp.out_ld = P.d_s;
   gp.out_split_stride = (long long)P.Nc * P.d_s;
-  KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, 2, EPI_STORE, gemm_cg(), &mg_hi, &mg_lo, &mw, gp, P.num_sms, c.s));
+  KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, P.g_planes, EPI_STORE, gemm_cg(), &mg_hi,
+                                   P.g_planes == 2 ? &mg_lo : nullptr, &mw, gp, P.num_sms, c.s));
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                                           P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
                                           P.n_split * epi_parts(2, P.kind) * kCorrSlots, c.Ws, c.s));
@@ -465,7 +471,8 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
     CUtensorMap ma_hi, ma_lo, mh;
     // dW_s += Gᵀ · H_s: A = Gᵀ [g_ld][Nc] is K-major (K = tokens), B = H_s chunk MN-major
     if ((st = make_map(&ma_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, kBK, kBM)) != KD_OK) return st;
-    if ((st = make_map(&ma_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, kBK, kBM)) != KD_OK) return st;
+    if (P.g_planes == 2 && (st = make_map(&ma_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, kBK, kBM)) != KD_OK)
+      return st;
     const int rows_left = P.N - row0;
     if ((st = make_map(&mh, c.hs + (size_t)row0 * P.d_s, P.d_s, rows_left, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK)
       return st;
@@ -481,7 +488,8 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
     wp.out = dW;
     wp.out_ld = P.d_s;
     wp.out_split_stride = 0;
-    KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, 2, EPI_ACCUM, gemm_cg(), &ma_hi, &ma_lo, &mh, wp, P.num_sms, c.s));
+    KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, P.g_planes, EPI_ACCUM, gemm_cg(), &ma_hi,
+                                     P.g_planes == 2 ? &ma_lo : nullptr, &mh, wp, P.num_sms, c.s));
   }
   return KD_OK;
 }

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256) k_kfix_apply(const float* __restrict__ ga
     split2(scale * (a.x - K.x * b.x), scale * (a.y - K.y * b.y), h0, l0);
     split2(scale * (a.z - K.z * b.z), scale * (a.w - K.w * b.w), h1, l1);
     *reinterpret_cast<uint2*>(ghi + e) = make_uint2(h0, h1);
-    *reinterpret_cast<uint2*>(glo + e) = make_uint2(l0, l1);
+    if (glo) *reinterpret_cast<uint2*>(glo + e) = make_uint2(l0, l1);  // NULL: KD_GRAD_BF16
   }
 }
 

@@ -289,6 +289,7 @@ cudaError_t launch_gemm(bool a_mn, bool b_mn, int num_a, int epi, int cg, const 
   KD_GEMM_CASE(true, true, 2, EPI_STORE)    // dh = [G_hi|G_lo] · W_s    (scratch holds Gᵀ: A MN-major)
   KD_GEMM_CASE(false, true, 2, EPI_ACCUM)   // dW += [G_hi|G_lo]ᵀ · H_s  (Gᵀ: A K-major)
   KD_GEMM_CASE(true, true, 1, EPI_ACCUM)
+  KD_GEMM_CASE(false, true, 1, EPI_ACCUM)   // dW with a single bf16 G plane (KD_GRAD_BF16)
 #undef KD_GEMM_CASE
   return cudaErrorNotSupported;
 }

@@ -40,7 +40,7 @@ struct PassParams {
   float gscale;         // c = loss_scale / T (FKL/RKL already folded with ln2 where needed)
   float beta;           // JSD beta
   __nv_bfloat16* g_hi;  // Gᵀ: [g_ld][n_rows] (vocab-major, token rows contiguous)
-  __nv_bfloat16* g_lo;
+  __nv_bfloat16* g_lo;  // NULL: KD_GRAD_BF16 (one plane)
   float* g_a;           // JSD/TVD: [g_ld][n_rows] fp32 planes
   float* g_b;
   int g_ld;             // vocab rows of the scratch: multiple of 64, >= V_r
@@ -51,7 +51,7 @@ struct PassParams {
   float* corr_r;
   float* zscr;          // decoupled pass 2: per-CTA [BN][128] fp32 staging of the teacher half-tile
   int l2_hints;         // bit 0: TMA loads of H evict_last, of W evict_first; bit 1: discard staged z_t lines;
-                        // bit 2: streaming G stores; bit 3: L2 prefetch of the next vocab tile's head rows
+                        // bit 3: L2 prefetch of the next vocab tile's head rows
   unsigned long long* dbg;  // KD_EPI_TIMING builds only: epilogue cycle counters (see kd_pass.cu)
 };
 

@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             if (KIND == KIND_FKL) kahan_add(Lacc, cL, la);
           }
           uint32_t hi[16], lo[16];
+          const bool two = p.g_lo != nullptr;  // split hi + lo planes (default) or hi only (KD_GRAD_BF16)
 #pragma unroll
           for (int i = 0; i < 16; ++i) split2_fast(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
           // exact residuals of the split for the largest entries (added back by k_reduce_dh); the per-chunk
@@ -498,8 +499,9 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               for (int h = 0; h < 2; ++h) {
                 const float gv = g[2 * i + h];
                 if (fabsf(gv) > kCorrThresh) {
-                  const float rep = h ? bf16hi_to_f32(hi[i]) + bf16hi_to_f32(lo[i])
-                                      : bf16lo_to_f32(hi[i]) + bf16lo_to_f32(lo[i]);
+                  // represented value: hi + lo (split planes) or hi alone (KD_GRAD_BF16)
+                  const float rep = h ? bf16hi_to_f32(hi[i]) + (two ? bf16hi_to_f32(lo[i]) : 0.f)
+                                      : bf16lo_to_f32(hi[i]) + (two ? bf16lo_to_f32(lo[i]) : 0.f);
                   const float rr = gv - rep;
                   if (fabsf(rr) > fabsf(cr1)) {
                     if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
@@ -511,20 +513,6 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           }
           __nv_bfloat16* ph = p.g_hi + col0;
           __nv_bfloat16* pl = p.g_lo + col0;
-          if (p.l2_hints & 4) {  // G is consumed by the next kernel: stream it past L2's operand working set
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              st_global_b16_cs(ph, (uint16_t)(hi[i] & 0xFFFFu));
-              st_global_b16_cs(pl, (uint16_t)(lo[i] & 0xFFFFu));
-              ph += p.n_rows;
-              pl += p.n_rows;
-              st_global_b16_cs(ph, (uint16_t)(hi[i] >> 16));
-              st_global_b16_cs(pl, (uint16_t)(lo[i] >> 16));
-              ph += p.n_rows;
-              pl += p.n_rows;
-            }
-            return;
-          }
 #ifdef KD_X_NOGSTORE  // experiment builds only: G computed but not stored
           {
             uint32_t x = 0;
@@ -534,16 +522,26 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             return;
           }
 #endif
+          if (two) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
-            st_global_b16(pl, (uint16_t)(lo[i] & 0xFFFFu));
-            ph += p.n_rows;
-            pl += p.n_rows;
-            st_global_b16(ph, (uint16_t)(hi[i] >> 16));
-            st_global_b16(pl, (uint16_t)(lo[i] >> 16));
-            ph += p.n_rows;
-            pl += p.n_rows;
+            for (int i = 0; i < 16; ++i) {
+              st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
+              st_global_b16(pl, (uint16_t)(lo[i] & 0xFFFFu));
+              ph += p.n_rows;
+              pl += p.n_rows;
+              st_global_b16(ph, (uint16_t)(hi[i] >> 16));
+              st_global_b16(pl, (uint16_t)(lo[i] >> 16));
+              ph += p.n_rows;
+              pl += p.n_rows;
+            }
+          } else {  // KD_GRAD_BF16: the hi plane only
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
+              ph += p.n_rows;
+              st_global_b16(ph, (uint16_t)(hi[i] >> 16));
+              ph += p.n_rows;
+            }
           }
         } else {
           float g[32], gb[32];

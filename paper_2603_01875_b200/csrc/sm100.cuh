@@ -396,9 +396,6 @@ __device__ __forceinline__ void split2_fast(float a, float b, uint32_t& hi, uint
 }
 
 
-__device__ __forceinline__ void st_global_b16_cs(void* p, uint16_t v) {  // streaming (evict-first) store
-  asm volatile("st.global.cs.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
-}
 __device__ __forceinline__ void st_global_b16(void* p, uint16_t v) {
   asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
 }

@@ -1,6 +1,8 @@
 """Shared helpers for the parity tests: upload generator bit patterns, run the oracle, compare."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -30,10 +32,26 @@ def oracle_run(inp: KI.KDInputs, *, T, kind, beta=0.5, loss_scale=1.0, want_dW=F
                             loss_scale=loss_scale, want_dW=want_dW)
 
 
+def _parity_log(name, got, ref, strict_tol, floor_used, n_strict):
+    """KD_PARITY_LOG=path: append one JSON line per comparison (summarised in profiles/r01_parity.md)."""
+    path = os.environ.get("KD_PARITY_LOG")
+    if not path or got.size == 0:
+        return
+    import json
+    d = np.abs(got - ref)
+    rec = {"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "name": name, "n": int(got.size),
+           "max_abs_err": float(d.max()), "max_err_over_strict_tol": float((d / strict_tol).max()),
+           "strict_violations": int(n_strict), "floor_used": bool(floor_used)}
+    with open(path, "a") as fh:
+        fh.write(json.dumps(rec) + "\n")
+
+
 def assert_kd_close(name, got, ref, rtol, atol, max_report=5):
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, (name, got.shape, ref.shape)
+    _parity_log(name, got, ref, atol + rtol * np.abs(ref), False,
+                int((np.abs(got - ref) > atol + rtol * np.abs(ref)).sum()))
     bad = ~(np.abs(got - ref) <= atol + rtol * np.abs(ref))
     if bad.any():
         idx = np.argwhere(bad)[:max_report]
@@ -103,6 +121,7 @@ def assert_grad_close(name, got, ref, floor=None, rtol=GRAD_RTOL, atol=GRAD_ATOL
                              f"{FLOOR_SIGMAS}*floor; first: "
                              f"{[(tuple(i), float(got[tuple(i)]), float(ref[tuple(i)])) for i in idx]}")
     strict = d > strict_tol
+    _parity_log(name, got, ref, strict_tol, floor is not None, int(strict.sum()))
     frac = strict.mean()
     assert frac <= STRICT_FRACTION_MAX, f"{name}: strict element-wise violations {strict.sum()} ({frac:.2e})"
     return int(strict.sum())

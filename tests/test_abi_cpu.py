@@ -37,9 +37,9 @@ def test_struct_layout_matches_header():
 #include <stddef.h>
 #include "kdfused.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(kd_problem), offsetof(kd_problem, vocab),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(kd_problem), offsetof(kd_problem, vocab),
          offsetof(kd_problem, temperature), offsetof(kd_problem, loss_scale), offsetof(kd_problem, want_dW),
-         offsetof(kd_problem, chunk_tokens), offsetof(kd_problem, reserved));
+         offsetof(kd_problem, chunk_tokens), offsetof(kd_problem, grad_precision), offsetof(kd_problem, reserved));
   return 0;
 }
 '''
@@ -51,7 +51,7 @@ int main(void) {
         got = [int(x) for x in subprocess.check_output([exe]).split()]
     P = kdfused.KDProblem
     want = [ctypes.sizeof(P), P.vocab.offset, P.temperature.offset, P.loss_scale.offset, P.want_dW.offset,
-            P.chunk_tokens.offset, P.reserved.offset]
+            P.chunk_tokens.offset, P.grad_precision.offset, P.reserved.offset]
     assert got == want
 
 
