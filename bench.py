@@ -8,9 +8,11 @@ Qwen3-8B d_t=4096 -> Qwen3-1.7B d_s=2048, 8 x 4096 tokens, FKL, T = 1).
     python bench.py [--gpus N --steps K --warmup W] [--config c2|c3_rkl|c3_jsd|c4|c5] [--dW]
     python bench.py --impl reference ...      # the fp64 CPU oracle on this box's host cores
 
-Multi-GPU (torchrun): token sharding with no data-path collective — every rank owns its own 32768 tokens
-and a full copy of both heads (weak scaling); the only collectives are the timing barrier / max.
-Prints ONE JSON line on rank 0.
+Multi-GPU (torchrun): the headline value is token sharding with no data-path collective — every rank owns its
+own 32768 tokens and a full copy of both heads (weak scaling); the only collectives are the timing barrier / max.
+The north star's vocabulary sharding (LM-head rows split over the ranks, every rank sees all N·P tokens, NCCL
+all-gather of the per-token records + all-reduce of dh) is measured in the same run and reported alongside under
+"vocab_sharded" (``--shard vocab`` swaps the two).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -47,6 +49,14 @@ def parse():
     ap.add_argument("--grad-precision", default="split", choices=["split", "bf16"],
                     help="G fed to the backward GEMMs: split hi+lo bf16 (parity-grade, default) or one bf16 plane "
                          "(KD_GRAD_BF16, fast, not within the north-star gradient tolerance)")
+    ap.add_argument("--shard", default="token", choices=["token", "vocab"],
+                    help="layout of the headline value at N>1: token sharding (default, no data-path collective) or "
+                         "vocab sharding (north star: LM-head rows split over ranks, record all-gather + dh "
+                         "all-reduce over NCCL).  At N>1 the other layout is measured too and reported alongside.")
+    ap.add_argument("--teacher-lse", action="store_true",
+                    help="SURVEY §8(f) NEXT-2(i): the teacher ships its per-token LSE record with H_t (computed once by "
+                         "kd_teacher_lse outside the timed region, as the teacher side would); the timed step is "
+                         "kd_fused_fwd_bwd_lse, whose pass 1 sweeps the student head only (FKL/JSD/TVD)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=128)
@@ -64,14 +74,16 @@ def peaks():
     return d
 
 
-def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_precision: str = "split"):
+def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_precision: str = "split",
+                  teacher_lse: bool = False):
     mask_desc = {"none": "all ones", "prompt_pad": "prompt L_p~U[64,512] + padding beyond L~U[2048,4096] masked",
                  "ragged": "ragged L~U[256,8192], prompt L_p~U[32,min(512,L/2)] masked"}[cfg.mask]
     heads_b = cfg.vocab * (cfg.d_t + cfg.d_s) * 2
     return {
         "workload": f"{cfg.name}: d_t={cfg.d_t} -> d_s={cfg.d_s}, V={cfg.vocab}, {n_tok} tokens/GPU, "
                     f"{cfg.kind.upper()} T={cfg.temperature:g}" + (" +dW_s" if want_dW else "")
-                    + (" [G: one bf16 plane]" if grad_precision == "bf16" else ""),
+                    + (" [G: one bf16 plane]" if grad_precision == "bf16" else "")
+                    + (" [teacher-shipped LSE record: pass 1 sweeps W_s only]" if teacher_lse else ""),
         "baseline_config": cfg.notes,
         "tokens_per_gpu": n_tok, "d_t": cfg.d_t, "d_s": cfg.d_s, "vocab": cfg.vocab, "kind": cfg.kind,
         "temperature": cfg.temperature, "jsd_beta": cfg.jsd_beta if cfg.kind == "jsd" else None,
@@ -173,6 +185,72 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------------- vocab-sharded leg
+def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, want_dW):
+    """Vocabulary sharding (BASELINE.json north_star): rank r keeps LM-head rows [v0, v1) of both
+    heads and sees EVERY rank's tokens (the per-rank token slices are all-gathered once, outside the timed region),
+    so per-GPU work stays that of one GPU (weak scaling in N·P tokens).  One step = ``sharding.vocab_sharded_fwd_bwd``:
+    kd_vocab_stats -> NCCL all-gather of the 20 B/token records -> kd_vocab_backward (rank-order merge, pass 2, partial
+    dh, local dW rows) -> NCCL all-reduce of dh (JSD/TVD add the (K, J) all-gather per token chunk)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_01875_b200 import sharding
+
+    bounds = sharding.vocab_shard_bounds(cfg.vocab, world)
+    v0, v1 = bounds[rank]
+    Wt_sh, Ws_sh = Wt[v0:v1].contiguous(), Ws[v0:v1].contiguous()
+    if world > 1:
+        def gather(x):
+            parts = [torch.empty_like(x) for _ in range(world)]
+            dist.all_gather(parts, x.contiguous())
+            return torch.cat(parts)
+        Ht_all, Hs_all = gather(Ht), gather(Hs)
+        mask_all = gather(mask) if mask is not None else None
+    else:
+        Ht_all, Hs_all, mask_all = Ht, Hs, mask
+    n_all = Ht_all.shape[0]
+    n_eff_all = int(mask_all.sum().item()) if mask_all is not None else n_all
+    dW = torch.empty(v1 - v0, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
+    kw = dict(vocab=cfg.vocab, v_begin=v0, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0,
+              want_dW=want_dW, accumulate_dW=False)
+    def step():
+        return sharding.vocab_sharded_fwd_bwd(Ht_all, Wt_sh, Hs_all, Ws_sh, mask_all, dW_s=dW, **kw)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        r = step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        r = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rec_bytes = 20 * n_all * world
+    kj_bytes = 8 * n_all * world if cfg.kind in ("jsd", "tvd") else 0
+    return {"value": n_eff_all * args.steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
+            "scaling": "weak", "tokens_per_step": n_all, "vocab_rows_per_gpu": v1 - v0,
+            "layout": f"vocab-sharded x{world}: LM-head rows split in 128-row granules, every rank sees all "
+                      f"{n_all} tokens",
+            "exchange_bytes_per_step_per_rank": {"records_allgather": rec_bytes, "kj_allgather": kj_bytes,
+                                                 "dh_allreduce": 4 * n_all * cfg.d_s},
+            "loss_finite": bool(torch.isfinite(r.loss).all().item())}
+
+
 # ------------------------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -187,9 +265,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only in the gloo test of the vocab leg
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("KD_DIST_BACKEND", "nccl")  # gloo: 2 ranks on one GPU (tests of the exchange)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     kd.lib()
     cfg = KI.CONFIGS[args.config]
@@ -219,7 +302,14 @@ def main():
     dW = torch.empty(cfg.vocab, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
     stream = torch.cuda.current_stream()
 
+    lse_t = None
+    if args.teacher_lse:
+        # the teacher side's record, produced once per batch by the teacher (not student work: outside the timing)
+        lse_t = kd.teacher_lse(Ht, Wt, mask, d_s=cfg.d_s, T=cfg.temperature, kind=cfg.kind)
+
     def step():
+        if lse_t is not None:
+            return kd.fused_fwd_bwd_lse(Ht, Wt, Hs, Ws, lse_t, mask, dW_s=dW, out=out, **kw)
         return kd.fused_fwd_bwd(Ht, Wt, Hs, Ws, mask, dW_s=dW, out=out, **kw)
 
     def barrier():
@@ -265,7 +355,8 @@ def main():
     pk = peaks()
     flops_pass = 2.0 * n_eff * cfg.vocab * (cfg.d_t + cfg.d_s)  # both LM-head GEMMs, one vocab sweep
     flops_g = 2.0 * n_eff * cfg.vocab * cfg.d_s                   # G · W_s  (or Gᵀ · H_s)
-    algo = {"pass1": flops_pass, "pass2": flops_pass, "gemm_dh": flops_g, "gemm_dW": flops_g}
+    flops_p1 = 2.0 * n_eff * cfg.vocab * cfg.d_s if args.teacher_lse else flops_pass  # student head only
+    algo = {"pass1": flops_p1, "pass2": flops_pass, "gemm_dh": flops_g, "gemm_dW": flops_g}
     gm = 2.0 if args.grad_precision == "split" else 1.0                 # split-bf16 G: 2 MMAs per product
     exec_mult = {"pass1": 1.0, "pass2": 1.0, "gemm_dh": gm, "gemm_dW": gm}
     kernels = {}
@@ -289,7 +380,9 @@ def main():
                 "traffic": traffic,
                 "peak_note": f"bf16 dense, {pk['source']}, sustained (kernel timed inside a long step); "
                              f"burst {pk['bf16_tflops']}",
-                "algorithmic_per_launch": f"2*tokens*V*(d_t+d_s) flop = {algo[dom] * args.steps / n_l:.4g}"}
+                "algorithmic_per_launch": (f"2*tokens*V*d_s flop = " if dom == "pass1" and args.teacher_lse else
+                                           f"2*tokens*V*(d_t+d_s) flop = " if dom.startswith("pass") else
+                                           f"2*tokens*V*d_s flop = ") + f"{algo[dom] * args.steps / n_l:.4g}"}
     step_useful = 2.0 * n_eff * cfg.vocab * (cfg.d_t + 2 * cfg.d_s + (cfg.d_s if want_dW else 0))
     useful_frac = step_useful * args.steps / (ms_max / 1e3) / 1e12 / peak_sust
 
@@ -301,10 +394,11 @@ def main():
         hHt = Ht.cpu().pin_memory()
         hHs = Hs.cpu().pin_memory()
         hmask = mask.cpu().pin_memory() if mask is not None else None
+        hlse = lse_t.cpu().pin_memory() if lse_t is not None else None
         hloss = [torch.empty(n_tok, dtype=torch.float32).pin_memory() for _ in range(2)]
         hdh = [torch.empty(n_tok, cfg.d_s, dtype=torch.float32).pin_memory() for _ in range(2)]
-        dH = [(torch.empty_like(Ht), torch.empty_like(Hs), torch.empty_like(mask) if mask is not None else None)
-              for _ in range(2)]
+        dH = [(torch.empty_like(Ht), torch.empty_like(Hs), torch.empty_like(mask) if mask is not None else None,
+               torch.empty_like(lse_t) if lse_t is not None else None) for _ in range(2)]
         outs = [kd.KDResult(torch.empty(n_tok, dtype=torch.float32, device=dev),
                             torch.empty(n_tok, cfg.d_s, dtype=torch.float32, device=dev), None,
                             torch.zeros(1, dtype=torch.int64, device=dev)) for _ in range(2)]
@@ -318,6 +412,8 @@ def main():
                 dH[b][1].copy_(hHs, non_blocking=True)
                 if hmask is not None:
                     dH[b][2].copy_(hmask, non_blocking=True)
+                if hlse is not None:
+                    dH[b][3].copy_(hlse, non_blocking=True)
                 in_ready[b].record(cs)
 
         def run_pipeline(n):
@@ -329,7 +425,10 @@ def main():
                         cs.wait_event(done[b ^ 1])  # buffer b^1 was read by step i-1
                     upload(b ^ 1)
                 stream.wait_event(in_ready[b])
-                kd.fused_fwd_bwd(dH[b][0], Wt, dH[b][1], Ws, dH[b][2], dW_s=dW, out=outs[b], **kw)
+                if hlse is not None:
+                    kd.fused_fwd_bwd_lse(dH[b][0], Wt, dH[b][1], Ws, dH[b][3], dH[b][2], dW_s=dW, out=outs[b], **kw)
+                else:
+                    kd.fused_fwd_bwd(dH[b][0], Wt, dH[b][1], Ws, dH[b][2], dW_s=dW, out=outs[b], **kw)
                 done[b].record(stream)
                 with torch.cuda.stream(cs):
                     cs.wait_event(done[b])
@@ -348,7 +447,7 @@ def main():
         torch.cuda.synchronize()
         ms_e2e = max_over_ranks(t0.elapsed_time(t1))
         assert torch.equal(hloss[(args.steps - 1) & 1], outs[(args.steps - 1) & 1].loss.cpu())
-        h2d = n_tok * (cfg.d_t + cfg.d_s) * 2 + (n_tok if mask is not None else 0)
+        h2d = n_tok * (cfg.d_t + cfg.d_s) * 2 + (n_tok if mask is not None else 0) + (8 * n_tok if hlse is not None else 0)
         d2h = n_tok * 4 + n_tok * cfg.d_s * 4
         e2e = {"value": world * n_eff * args.steps / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
@@ -362,14 +461,30 @@ def main():
                "sample": f"{args.cpu_sample_tokens} tokens at full {cfg.name} shapes, fp64 numpy "
                          f"({dt:.1f} s; BLAS threads = all {cores} affinity cores)"}
 
+    # ---- the other layout, measured in the same run (north star: vocab sharding, token sharding alongside)
+    alongside = {}
+    if world > 1 or args.shard == "vocab":
+        vleg = vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, want_dW)
+        tleg = {"value": value, "unit": UNIT, "ms_per_step": ms_max / args.steps, "scaling": "weak",
+                "tokens_per_step": n_tok * world, "layout": f"token-sharded x{world}, full heads per rank"}
+        if args.shard == "vocab":
+            value, ms_max = vleg["value"], vleg["ms_per_step"] * args.steps
+            alongside["token_sharded"] = tleg
+        else:
+            alongside["vocab_sharded"] = vleg
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kd_inputs recipe, seeded)",
-                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision), "clocks": clocks, "e2e": e2e,
+                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision, args.teacher_lse),
+                "clocks": clocks, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "roofline": roofline, "cpu_baseline": cpu,
                 "useful_flop_frac": useful_frac, "kernels": kernels, "nonfinite_tokens": nonfinite,
-                "tokens_loss_bearing_per_gpu": n_eff}
+                "tokens_loss_bearing_per_gpu": n_eff, **alongside}
+        if args.shard == "vocab":
+            line["config"]["parallelism"] = vleg["layout"]
+            line["config"]["tokens_per_step"] = vleg["tokens_per_step"]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -107,6 +107,32 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
                            const void* W_s, const uint8_t* mask, float* loss, float* dh_s, float* dW_s,
                            int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- teacher-shipped LSE (the recompute-reduced variant).  The paper's teacher
+ * ships only H_t and the student recomputes everything, so pass 1 sweeps BOTH heads just to
+ * learn the two log-sum-exps.  If the teacher side also ships its per-token LSE record (8 B/token next to
+ * the 2·d_t B/token of H_t), the student's pass 1 sweeps the student head only: at BASELINE config 2 the
+ * executed tensor work drops from 2V(2d_t+3d_s) to 2V(d_t+4d_s) flop/token (split-bf16 G).  Same results:
+ * the record is the one the fused call computes for itself, so
+ * kd_teacher_lse + kd_fused_fwd_bwd_lse reproduce kd_fused_fwd_bwd bit for bit for the same problem.
+ *
+ * kd_teacher_lse (teacher side; full vocabulary, v_begin = 0, v_end = vocab; d_s / kind are only used to size
+ *   the workspace, so pass the student's problem unchanged):
+ *   h_t  [N, d_t] bf16, W_t [V, d_t] bf16, mask [N] u8 or NULL (rows with mask = 0 are not written)
+ *   lse_t [2][N] f32 out: lse_t[0][n] = M_t = max_v z_v·log2(e)/T, lse_t[1][n] = log2 Σ_v 2^{z_v·log2(e)/T − M_t}
+ *         (the base-2 LSE of Z_t/T as two numbers; ln-LSE = ln2·(M_t + lse_t[1][n])).  Kept apart because
+ *         one fp32 number (ulp 2e-6 at |LSE| ~ 30) would cancel in q − p for peaked rows.
+ *   workspace >= kd_workspace_size(p).
+ * kd_fused_fwd_bwd_lse: kd_fused_fwd_bwd with the teacher record `lse_t` [2][N] (as above; rows with
+ *   mask = 0 are not read) supplied; pass 1 reads W_t not at all.  FKL, JSD and TVD; RKL returns
+ *   KD_ERR_UNSUPPORTED (its gradient needs the RKL value, a cross term of both heads, before pass 2).
+ *   Errors otherwise as kd_fused_fwd_bwd; lse_t NULL with N > 0 is KD_ERR_INVALID_ARG. */
+kd_status kd_teacher_lse(const kd_problem* p, const void* h_t, const void* W_t, const uint8_t* mask, float* lse_t,
+                         void* workspace, size_t workspace_bytes, void* stream);
+kd_status kd_fused_fwd_bwd_lse(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                               const void* W_s, const uint8_t* mask, const float* lse_t, float* loss, float* dh_s,
+                               float* dW_s, int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
 /* ---- vocabulary-sharded execution (north_star: "vocabulary sharding of W_t/W_s, with a tiny
  * all-reduce of per-token stats").  Rank r owns rows [v_begin, v_end) of both heads.
  * FKL/RKL: kd_vocab_stats -> exchange -> kd_vocab_backward.  JSD/TVD: see kd_vocab_partials below.

@@ -32,7 +32,7 @@ cudaError_t launch_zero_masked(const uint8_t* mask, int N, float* loss, float* d
 cudaError_t launch_merge(const float* part, long long plane, long long split_stride, int n_split, int n_rows,
                          int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
                          long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, int write_loss,
-                         cudaStream_t s);
+                         cudaStream_t s, const float* tstats_in = nullptr);
 cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, float* loss,
                              const int* idx, long long* nonfinite, cudaStream_t s);
 cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, int kind, float beta,
@@ -345,8 +345,9 @@ struct Ctx {
 };
 }  // namespace
 
+// teacher_only (kd_teacher_lse): h_s / W_s are absent; the student maps alias the teacher's and are never read.
 static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
-                          const uint8_t* mask, int64_t* n_nonfinite) {
+                          const uint8_t* mask, int64_t* n_nonfinite, bool teacher_only = false) {
   const Plan& P = c.P;
   c.n_eff = ws_at<int>(c.ws, P.off_neff);
   c.nonfinite = n_nonfinite ? reinterpret_cast<long long*>(n_nonfinite) : ws_at<long long>(c.ws, P.off_nonfinite);
@@ -359,7 +360,8 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
     auto* pt = ws_at<__nv_bfloat16>(c.ws, P.off_ht);
     auto* ps = ws_at<__nv_bfloat16>(c.ws, P.off_hs);
     KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_t), P.d_t, pt, P.d_t, P.N, idx, c.n_eff, c.s));
-    KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_s), P.d_s, ps, P.d_s, P.N, idx, c.n_eff, c.s));
+    if (!teacher_only)
+      KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_s), P.d_s, ps, P.d_s, P.N, idx, c.n_eff, c.s));
     c.ht = pt;
     c.hs = ps;
     c.idx = idx;
@@ -372,6 +374,11 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
   kd_status st;
   if ((st = make_map(&c.maps[0], c.ht, P.d_t, P.N, (uint64_t)P.d_t * 2, kBK, kBM)) != KD_OK) return st;
   if ((st = make_map(&c.maps[1], c.Wt, P.d_t, P.V_r, (uint64_t)P.d_t * 2, kBK, P.bn / P.cg)) != KD_OK) return st;
+  if (teacher_only) {
+    c.maps[2] = c.maps[0];
+    c.maps[3] = c.maps[1];
+    return KD_OK;
+  }
   if ((st = make_map(&c.maps[2], c.hs, P.d_s, P.N, (uint64_t)P.d_s * 2, kBK, kBM)) != KD_OK) return st;
   if ((st = make_map(&c.maps[3], c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, kBK, P.bn / P.cg)) != KD_OK) return st;
   return KD_OK;
@@ -408,6 +415,8 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.dbg = reinterpret_cast<unsigned long long*>(g_dbg_ptr);
   static const int l2_hints = env_int("KD_L2_HINTS", 0);  // measured neutral-to-negative (profiles/r01_ncu_pass_pair256.md)
   pp.l2_hints = l2_hints;
+  pp.side_lo = 0;
+  pp.side_hi = 2;
   return pp;
 }
 
@@ -525,13 +534,19 @@ size_t kd_workspace_size(const kd_problem* p) {
   return make_plan(p).total;
 }
 
-kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
-                           const void* W_s, const uint8_t* mask, float* loss, float* dh_s, float* dW_s,
-                           int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
+// The whole path on one GPU.  lse_t != NULL: the teacher's per-token base-2 LSE record [2][N] (kd_teacher_lse) is
+// supplied, so pass 1 sweeps the student head only.
+static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                            const uint8_t* mask, const float* lse_t, float* loss, float* dh_s, float* dW_s,
+                            int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = validate(p, true);
   if (st != KD_OK) return st;
+  if (lse_t && p->kind == KD_RKL)
+    return fail(KD_ERR_UNSUPPORTED, "kd_fused_fwd_bwd_lse: RKL's gradient needs its loss (a cross term of both heads) "
+                                    "before pass 2, so pass 1 cannot skip the teacher head");
+  if (lse_t && !aligned16(lse_t)) return fail(KD_ERR_ALIGNMENT, "lse_t must be 16-byte aligned");
   Ctx c{};
   c.p = p;
   c.P = make_plan(p);
@@ -553,14 +568,64 @@ kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t
     PassParams pp = pass_params(c, row0);
     // decoupled pass 1 (independent teacher / student LSEs) for FKL/JSD/TVD; RKL needs its loss in pass 2
     const bool coupled = P.kind == KD_RKL;
+    if (lse_t) pp.side_lo = 1;  // student half-tiles only
     KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 0,
-                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0, c.nonfinite, coupled ? 1 : 0,
-                           c.s));
+                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, (long long)P.N, c.idx, 0, c.nonfinite,
+                           coupled ? 1 : 0, c.s, lse_t));
     if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
     if (P.kind == KD_FKL)
       KD_LAUNCH(K_MERGE, launch_loss_rows(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, row0, c.n_eff, loss, c.idx,
                                           c.nonfinite, c.s));
+  }
+  return KD_OK;
+}
+
+kd_status kd_fused_fwd_bwd(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                           const void* W_s, const uint8_t* mask, float* loss, float* dh_s, float* dW_s,
+                           int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
+  return fused_impl(p, h_t, W_t, h_s, W_s, mask, nullptr, loss, dh_s, dW_s, n_nonfinite, workspace, workspace_bytes,
+                    stream);
+}
+
+kd_status kd_fused_fwd_bwd_lse(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                               const void* W_s, const uint8_t* mask, const float* lse_t, float* loss, float* dh_s,
+                               float* dW_s, int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (p && p->n_tokens > 0 && !lse_t) return fail(KD_ERR_INVALID_ARG, "lse_t is NULL");
+  return fused_impl(p, h_t, W_t, h_s, W_s, mask, p && p->n_tokens > 0 ? lse_t : nullptr, loss, dh_s, dW_s,
+                    n_nonfinite, workspace, workspace_bytes, stream);
+}
+
+kd_status kd_teacher_lse(const kd_problem* p, const void* h_t, const void* W_t, const uint8_t* mask, float* lse_t,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = validate(p, true);
+  if (st != KD_OK) return st;
+  Ctx c{};
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  const Plan& P = c.P;
+  if (P.N > 0 && (!h_t || !lse_t)) return fail(KD_ERR_INVALID_ARG, "NULL h_t / lse_t");
+  if (!W_t) return fail(KD_ERR_INVALID_ARG, "NULL W_t");
+  const void* ptrs[] = {h_t, W_t, lse_t};
+  for (const void* x : ptrs)
+    if (x && !aligned16(x)) return fail(KD_ERR_ALIGNMENT, "pointers must be 16-byte aligned");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255) || workspace_bytes < P.total)
+    return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace must be 256-byte aligned and >= %zu bytes", P.total);
+  if (P.N == 0) return KD_OK;
+  if ((st = prologue(c, h_t, W_t, nullptr, nullptr, mask, nullptr, true)) != KD_OK) return st;
+  for (int ch = 0; ch < P.n_chunks; ++ch) {
+    const int row0 = ch * P.Nc;
+    PassParams pp = pass_params(c, row0);
+    pp.side_hi = 1;  // teacher half-tiles only (the same sweep as the teacher side of the fused decoupled pass 1)
+    KD_LAUNCH(K_PASS1, launch_pass(1, KD_FKL, false, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, KD_FKL), P.Nc, row0,
+                                    c.n_eff, KD_FKL, 2, nullptr, nullptr, lse_t, (long long)P.N, c.idx, 0,
+                                    c.nonfinite, 0, c.s));
   }
   return KD_OK;
 }

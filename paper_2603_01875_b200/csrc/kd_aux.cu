@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
                                                      float* __restrict__ fstats, float* __restrict__ loss,
                                                      float* __restrict__ rec, long long rec_plane,
                                                      const int* __restrict__ idx, int orig_rows,
-                                                     long long* __restrict__ nonfinite, int write_loss) {
+                                                     long long* __restrict__ nonfinite, int write_loss,
+                                                     const float* __restrict__ tstats_in) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int valid = min(n_rows, *n_eff - row0);
@@ -156,6 +157,13 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
     rec[4 * rec_plane + orow] = (float)A.U;
     return;
   }
+  if (mode == 2) {
+    // kd_teacher_lse: the teacher's base-2 LSE as (M_t, log2 S_t) per ORIGINAL row — the same two fp32 numbers
+    // mode 0 leaves in fstats, so a caller-supplied record reproduces the fused path exactly
+    rec[orow] = (float)A.Mp;
+    rec[rec_plane + orow] = (float)log2(A.Sp);
+    return;
+  }
   const float lp = (float)log2(A.Sp), lq = (float)log2(A.Sq);
   const float ell2 = (float)__dadd_rn(__dsub_rn(__ddiv_rn(A.U, A.Sp), log2(A.Sp)), log2(A.Sq));  // FKL / RKL, bits
   const bool rkl = kind == KIND_RKL;
@@ -165,6 +173,10 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
   fstats[2 * n_rows + r] = (float)(rkl ? A.Mp : A.Mq);  // M_s
   fstats[3 * n_rows + r] = rkl ? lp : lq;        // log2 S_s
   fstats[4 * n_rows + r] = ell2;
+  if (tstats_in) {  // teacher LSE supplied by the caller (kd_fused_fwd_bwd_lse): pass 1 swept the student only
+    fstats[r] = tstats_in[orow];
+    fstats[n_rows + r] = tstats_in[rec_plane + orow];
+  }
   if (write_loss && (kind == KIND_FKL || kind == KIND_RKL)) {
     const float ell = ell2 * kLn2;
     loss[orow] = ell;
@@ -352,10 +364,10 @@ cudaError_t launch_zero_masked(const uint8_t* mask, int N, float* loss, float* d
 cudaError_t launch_merge(const float* part, long long plane, long long split_stride, int n_split, int n_rows,
                          int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
                          long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, int write_loss,
-                         cudaStream_t s) {
+                         cudaStream_t s, const float* tstats_in) {
   k_merge_stats<<<(n_rows + 7) / 8, 256, 0, s>>>(part, plane, split_stride, n_split, n_rows, row0, n_eff, kind,
                                                       mode, fstats, loss, rec, rec_plane, idx, orig_rows, nonfinite,
-                                                      write_loss);
+                                                      write_loss, tstats_in);
   return cudaGetLastError();
 }
 

@@ -53,6 +53,10 @@ struct PassParams {
   int l2_hints;         // bit 0: TMA loads of H evict_last, of W evict_first; bit 1: discard staged z_t lines;
                         // bit 3: L2 prefetch of the next vocab tile's head rows
   unsigned long long* dbg;  // KD_EPI_TIMING builds only: epilogue cycle counters (see kd_pass.cu)
+  // decoupled pass 1 only: the half-tile sides swept, [side_lo, side_hi) of {0 = teacher, 1 = student}.
+  // (0, 2) = both (default); (1, 2) = student only (teacher LSE supplied by the caller);
+  // (0, 1) = teacher only (kd_teacher_lse).
+  int side_lo, side_hi;
 };
 
 // Generic bf16 GEMM with fp32 TMEM accumulation: D[M, N] = sum_{a < NUM_A} A_a[M, K] * B[N, K]^T.

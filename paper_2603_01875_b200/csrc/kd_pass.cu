@@ -151,7 +151,10 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       const int row = p.row0 + ur.m_tile * kBMt + rank * kBM;  // this CTA's 128 token rows
       for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
         const int vrow = vt * BN + rank * (BN / CG);           // this CTA's share of the vocab tile
-        for (int kb = 0; kb < p.kb_t + p.kb_s; ++kb, ++kit) {
+        // decoupled pass 1 may sweep one side only: teacher K blocks are [0, kb_t), student [kb_t, kb_t + kb_s)
+        const int kb_lo = (DEC && PASS == 1 && p.side_lo == 1) ? p.kb_t : 0;
+        const int kb_hi = (DEC && PASS == 1 && p.side_hi == 1) ? p.kb_t : p.kb_t + p.kb_s;
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++kit) {
           const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
           mbar_wait(&empty[st], ph ^ 1);
           if (lane == 0) {
@@ -195,7 +198,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       for (int u = worker; u < n_units; u += n_workers) {
         const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
-          for (int side = 0; side < 2; ++side, ++it) {
+          const int s_lo = PASS == 1 ? p.side_lo : 0, s_hi = PASS == 1 ? p.side_hi : 2;
+          for (int side = s_lo; side < s_hi; ++side, ++it) {
             const uint32_t buf = it & 1, tph = (it >> 1) & 1;
 #ifdef KD_EPI_TIMING
             const long long m0 = clock64();
@@ -340,8 +344,11 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         const int rslot = (u / m_tiles) * EP + part;
         float M2[2] = {-INFINITY, -INFINITY}, S2[2] = {0.f, 0.f}, cS2[2] = {0.f, 0.f};  // teacher, student
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
-          for (int side = 0; side < 2; ++side, ++it) {
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            if (side < p.side_lo || side >= p.side_hi) continue;  // one-sided sweep (side index stays static)
             const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+            ++it;
             mbar_wait(&tfull[buf], tph);
             tc_fence_after();
             const uint32_t t_addr = tmem_base + lane_addr + buf * BN;
@@ -396,11 +403,14 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           }
         }
         if (row_ok) {
+          // a one-sided sweep writes its side into both halves of the record (a symmetric record: the merge's
+          // empty-record test and its cross term stay well defined; the caller uses one half)
+          const bool sp = p.side_lo == 1, sq = p.side_hi == 2;
           const size_t idx = (size_t)rslot * p.n_rows + r_local;
-          p.part[idx] = M2[0];
-          p.part[p.part_plane + idx] = M2[1];
-          p.part[2 * p.part_plane + idx] = S2[0] - cS2[0];
-          p.part[3 * p.part_plane + idx] = S2[1] - cS2[1];
+          p.part[idx] = sp ? M2[1] : M2[0];
+          p.part[p.part_plane + idx] = sq ? M2[1] : M2[0];
+          p.part[2 * p.part_plane + idx] = sp ? S2[1] - cS2[1] : S2[0] - cS2[0];
+          p.part[3 * p.part_plane + idx] = sq ? S2[1] - cS2[1] : S2[0] - cS2[0];
           p.part[4 * p.part_plane + idx] = 0.f;  // no cross term: the FKL loss is accumulated in pass 2
         }
       }

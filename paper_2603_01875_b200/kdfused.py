@@ -19,7 +19,8 @@ LIB_PATH = os.environ.get("KD_LIB_PATH") or os.path.join(_HERE, "libkdfused.so")
 KINDS = {"fkl": 0, "rkl": 1, "jsd": 2, "tvd": 3}
 STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALIGNMENT", 4: "KD_ERR_UNSUPPORTED",
           5: "KD_ERR_WORKSPACE_TOO_SMALL", 6: "KD_ERR_CUDA"}
-EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_vocab_stats", "kd_vocab_backward",
+EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_teacher_lse", "kd_fused_fwd_bwd_lse",
+            "kd_vocab_stats", "kd_vocab_backward",
             "kd_vocab_partials", "kd_vocab_finish", "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
             "kd_last_error", "kd_abi_version")
@@ -60,6 +61,10 @@ def lib() -> ctypes.CDLL:
     L.kd_workspace_size.restype = sz
     L.kd_fused_fwd_bwd.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, i64p, vp, sz, vp]
     L.kd_fused_fwd_bwd.restype = ctypes.c_int
+    L.kd_teacher_lse.argtypes = [P, vp, vp, vp, vp, vp, sz, vp]
+    L.kd_teacher_lse.restype = ctypes.c_int
+    L.kd_fused_fwd_bwd_lse.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64p, vp, sz, vp]
+    L.kd_fused_fwd_bwd_lse.restype = ctypes.c_int
     L.kd_vocab_stats.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.kd_vocab_stats.restype = ctypes.c_int
     L.kd_vocab_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
@@ -197,6 +202,55 @@ def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5,
     _check(lib().kd_fused_fwd_bwd(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(h_s), _ptr(W_s), _ptr(mask),
                                   _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws),
                                   ws.numel(), _stream_handle(stream)))
+    return KDResult(loss, dh, dW_s if want_dW else None, nnf)
+
+
+def teacher_lse(h_t, W_t, mask=None, *, d_s, T=1.0, kind="fkl", chunk_tokens=0, out=None,
+                stream=None) -> torch.Tensor:
+    """kd_teacher_lse: the teacher's per-token base-2 LSE record [2, N] (M_t, log2 S_t) at temperature T.
+
+    ``d_s`` / ``kind`` / ``chunk_tokens`` must match the student call that consumes the record (they size the
+    workspace and fix the token chunking, which the record reproduces bit for bit)."""
+    h_t, W_t = _as_bf16(h_t, "h_t"), _as_bf16(W_t, "W_t")
+    N, d_t = h_t.shape
+    V = W_t.shape[0]
+    p = make_problem(N, d_t, d_s, V, T=T, kind=kind, chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
+    lse = out if out is not None else torch.zeros(2, N, dtype=torch.float32, device=h_t.device)
+    ws = _workspace(workspace_size(p), h_t.device)
+    _check(lib().kd_teacher_lse(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(mask), _ptr(lse), _ptr(ws), ws.numel(),
+                                _stream_handle(stream)))
+    return lse
+
+
+def fused_fwd_bwd_lse(h_t, W_t, h_s, W_s, lse_t, mask=None, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0,
+                      want_dW=False, accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split",
+                      out=None, stream=None) -> KDResult:
+    """kd_fused_fwd_bwd_lse: kd_fused_fwd_bwd with the teacher's LSE record supplied (pass 1: student head only)."""
+    h_t, W_t, h_s, W_s = (_as_bf16(x, n) for x, n in ((h_t, "h_t"), (W_t, "W_t"), (h_s, "h_s"), (W_s, "W_s")))
+    N, d_t = h_t.shape
+    V, d_s = W_s.shape
+    dev = h_t.device
+    if not lse_t.is_cuda or lse_t.dtype != torch.float32 or tuple(lse_t.shape) != (2, N):
+        raise ValueError("lse_t must be a CUDA float32 tensor of shape [2, N]")
+    lse_t = lse_t.contiguous()
+    p = make_problem(N, d_t, d_s, V, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, chunk_tokens=chunk_tokens, grad_precision=grad_precision)
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    if out is None:
+        loss = torch.empty(N, dtype=torch.float32, device=dev)
+        dh = torch.empty(N, d_s, dtype=torch.float32, device=dev)
+        nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        loss, dh, nnf = out.loss, out.dh_s, out.n_nonfinite
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if accumulate_dW else torch.empty)(V, d_s, dtype=torch.float32, device=dev)
+    ws = _workspace(workspace_size(p), dev)
+    _check(lib().kd_fused_fwd_bwd_lse(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(h_s), _ptr(W_s), _ptr(mask),
+                                      _ptr(lse_t), _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf),
+                                      _ptr(ws), ws.numel(), _stream_handle(stream)))
     return KDResult(loss, dh, dW_s if want_dW else None, nnf)
 
 

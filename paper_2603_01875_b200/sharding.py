@@ -39,8 +39,15 @@ def token_shard_bounds(n_tokens: int, world: int) -> list[tuple[int, int]]:
     return [(edges[i], edges[i + 1]) for i in range(world)]
 
 
+def _distributed() -> bool:
+    """False when no process group exists: a one-rank job runs the same protocol with identity exchanges."""
+    return dist.is_available() and dist.is_initialized()
+
+
 def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather this rank's [5, N] record into [P, 5, N] in rank order."""
+    if not _distributed():
+        return rec.contiguous()[None]
     world = dist.get_world_size(group)
     out = [torch.empty_like(rec) for _ in range(world)]
     dist.all_gather(out, rec.contiguous(), group=group)
@@ -49,10 +56,17 @@ def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
 
 def gather_kj(kj: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather this rank's [2, n] (K, J) partials into [P, 2, n] in rank order."""
+    if not _distributed():
+        return kj.contiguous()[None]
     world = dist.get_world_size(group)
     out = [torch.empty_like(kj) for _ in range(world)]
     dist.all_gather(out, kj.contiguous(), group=group)
     return torch.stack(out)
+
+
+def _all_reduce_sum(t: torch.Tensor, group=None):
+    if _distributed():
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
 
 class _Result:
@@ -90,7 +104,7 @@ def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, 
     if dh is None:  # no tokens
         loss = torch.zeros(0, dtype=torch.float32, device=h_t.device)
         dh = torch.zeros(0, d_s, dtype=torch.float32, device=h_t.device)
-    dist.all_reduce(dh, op=dist.ReduceOp.SUM, group=group)
+    _all_reduce_sum(dh, group)
     return _Result(loss, dh, dW_s if want_dW else None)
 
 
@@ -124,11 +138,11 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
     r = backward_fn(h_t, W_t_shard, h_s, W_s_shard, recs, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
                     loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
                     chunk_tokens=chunk_tokens)
-    dist.all_reduce(r.dh_s, op=dist.ReduceOp.SUM, group=group)
+    _all_reduce_sum(r.dh_s, group)
     return r
 
 
 def token_sharded_dW_reduce(dW_s: torch.Tensor, group=None) -> torch.Tensor:
     """Token sharding with dW_s: the only exchange is the sum of the per-rank dW_s."""
-    dist.all_reduce(dW_s, op=dist.ReduceOp.SUM, group=group)
+    _all_reduce_sum(dW_s, group)
     return dW_s

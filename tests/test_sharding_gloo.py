@@ -198,3 +198,23 @@ def test_bounds():
     assert sorted({y - x for x, y in b}) == [18944, 19072]   # 148 / 149 granules
     assert vocab_shard_bounds(100, 3, granule=128) == [(0, 0), (0, 0), (0, 100)]
     assert token_shard_bounds(10, 3) == [(0, 3), (3, 6), (6, 10)]
+
+
+@pytest.mark.parametrize("kind", ["fkl", "jsd"])
+def test_one_rank_without_process_group(kind):
+    """A one-rank job (bench.py --shard vocab at N=1) runs the same protocol with identity exchanges."""
+    import kd_inputs as KI
+    from oracle.kd_oracle import kd_fused_fwd_bwd
+    assert not dist.is_initialized()
+    N, d_t, d_s, V = 24, 32, 16, 200
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=6)
+    f = KI.bf16_to_f64
+    ht, hs, Wt, Ws = (torch.tensor(f(x)) for x in (inp.H_t, inp.H_s, inp.W_t, inp.W_s))
+    r = vocab_sharded_fwd_bwd(ht, Wt, hs, Ws, None, vocab=V, v_begin=0, T=1.1, kind=kind, beta=0.5, want_dW=True,
+                              chunk_tokens=16, stats_fn=_stats_standin, backward_fn=_backward_standin,
+                              partials_fn=_partials_standin, finish_fn=_finish_standin)
+    loss, dh, dW = kd_fused_fwd_bwd(f(inp.H_t), f(inp.W_t), f(inp.H_s), f(inp.W_s), None, T=1.1, kind=kind,
+                                    beta=0.5, want_dW=True)
+    np.testing.assert_allclose(r.loss.numpy(), loss, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(r.dh_s.numpy(), dh, rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(r.dW_s.numpy(), dW, rtol=1e-11, atol=1e-13)
