@@ -57,6 +57,9 @@ def parse():
                     help="SURVEY §8(f) NEXT-2(i): the teacher ships its per-token LSE record with H_t (computed once by "
                          "kd_teacher_lse outside the timed region, as the teacher side would); the timed step is "
                          "kd_fused_fwd_bwd_lse, whose pass 1 sweeps the student head only (FKL/JSD/TVD)")
+    ap.add_argument("--vocab-ranks", type=int, default=0,
+                    help="vocab-sharded leg on a 2-D grid: ranks per vocab group (P_voc; default all ranks). "
+                         "world / P_voc token groups (BASELINE config 4: 8x1, 4x2, 2x4, 1x8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=128)
@@ -187,33 +190,51 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------------------- vocab-sharded leg
 def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, want_dW):
-    """Vocabulary sharding (BASELINE.json north_star): rank r keeps LM-head rows [v0, v1) of both
-    heads and sees EVERY rank's tokens (the per-rank token slices are all-gathered once, outside the timed region),
-    so per-GPU work stays that of one GPU (weak scaling in N·P tokens).  One step = ``sharding.vocab_sharded_fwd_bwd``:
-    kd_vocab_stats -> NCCL all-gather of the 20 B/token records -> kd_vocab_backward (rank-order merge, pass 2, partial
-    dh, local dW rows) -> NCCL all-reduce of dh (JSD/TVD add the (K, J) all-gather per token chunk)."""
+    """Vocabulary sharding (BASELINE.json north_star), optionally on a 2-D grid (config 4:
+    P_tok x P_voc).  The ranks form world / P_voc vocab groups of P_voc consecutive ranks; inside a group rank j keeps
+    LM-head rows [v0, v1) of both heads (128-row granules) and sees every token of the group (the members' token
+    slices are all-gathered once, outside the timed region), so per-GPU work stays that of one GPU (weak scaling).
+    One step = ``sharding.vocab_sharded_fwd_bwd`` on the group: kd_vocab_stats -> NCCL all-gather of the 20 B/token
+    records -> kd_vocab_backward (rank-order merge, pass 2, partial dh, local dW rows) -> NCCL all-reduce of dh
+    (JSD/TVD add the (K, J) all-gather per token chunk)."""
     import torch
     import torch.distributed as dist
 
     from paper_2603_01875_b200 import sharding
 
-    bounds = sharding.vocab_shard_bounds(cfg.vocab, world)
-    v0, v1 = bounds[rank]
+    pv = args.vocab_ranks if args.vocab_ranks > 0 else world
+    if world % pv:
+        raise SystemExit(f"--vocab-ranks {pv} must divide the world size {world}")
+    group, g0 = None, (rank // pv) * pv
+    if world > 1 and pv < world:
+        for t in range(world // pv):  # every rank creates every group, in the same order
+            g = dist.new_group(list(range(t * pv, (t + 1) * pv)))
+            if t == rank // pv:
+                group = g
+    j = rank - g0  # position inside the vocab group
+    bounds = sharding.vocab_shard_bounds(cfg.vocab, pv)
+    v0, v1 = bounds[j]
     Wt_sh, Ws_sh = Wt[v0:v1].contiguous(), Ws[v0:v1].contiguous()
-    if world > 1:
+    if pv > 1:
         def gather(x):
-            parts = [torch.empty_like(x) for _ in range(world)]
-            dist.all_gather(parts, x.contiguous())
+            parts = [torch.empty_like(x) for _ in range(pv)]
+            dist.all_gather(parts, x.contiguous(), group=group)
             return torch.cat(parts)
         Ht_all, Hs_all = gather(Ht), gather(Hs)
         mask_all = gather(mask) if mask is not None else None
     else:
         Ht_all, Hs_all, mask_all = Ht, Hs, mask
     n_all = Ht_all.shape[0]
-    n_eff_all = int(mask_all.sum().item()) if mask_all is not None else n_all
+    n_eff_own = int(mask.sum().item()) if mask is not None else Ht.shape[0]
+    n_eff_job = n_eff_own
+    if world > 1:
+        t = torch.tensor([n_eff_own], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        n_eff_job = int(t.item())
     dW = torch.empty(v1 - v0, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
     kw = dict(vocab=cfg.vocab, v_begin=v0, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0,
-              want_dW=want_dW, accumulate_dW=False)
+              want_dW=want_dW, accumulate_dW=False, group=group)
+
     def step():
         return sharding.vocab_sharded_fwd_bwd(Ht_all, Wt_sh, Hs_all, Ws_sh, mask_all, dW_s=dW, **kw)
 
@@ -240,12 +261,14 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    rec_bytes = 20 * n_all * world
-    kj_bytes = 8 * n_all * world if cfg.kind in ("jsd", "tvd") else 0
-    return {"value": n_eff_all * args.steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
-            "scaling": "weak", "tokens_per_step": n_all, "vocab_rows_per_gpu": v1 - v0,
-            "layout": f"vocab-sharded x{world}: LM-head rows split in 128-row granules, every rank sees all "
-                      f"{n_all} tokens",
+    rec_bytes = 20 * n_all * pv
+    kj_bytes = 8 * n_all * pv if cfg.kind in ("jsd", "tvd") else 0
+    grid = f"{world // pv} token groups x {pv} vocab shards"
+    return {"value": n_eff_job * args.steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
+            "scaling": "weak", "tokens_per_step": n_all * (world // pv), "vocab_rows_per_gpu": v1 - v0,
+            "grid": grid,
+            "layout": f"vocab-sharded ({grid}): LM-head rows split in 128-row granules over each group of {pv} "
+                      f"ranks, every rank of a group sees its {n_all} tokens",
             "exchange_bytes_per_step_per_rank": {"records_allgather": rec_bytes, "kj_allgather": kj_bytes,
                                                  "dh_allreduce": 4 * n_all * cfg.d_s},
             "loss_finite": bool(torch.isfinite(r.loss).all().item())}

@@ -17,6 +17,11 @@ Contents
                  simulated vocab shards).  It is NOT used as the reference;
                  tests pin it to ``kd_oracle`` (<= 1e-12) so that the merge
                  algebra the multi-GPU exchange relies on is checked on CPU.
+``kd_topk``      the prior-art top-k teacher transfer (SURVEY §8(f) NEXT-3,
+                 SPEC S:267-275 kd_loss_topk): teacher top-k selection, the
+                 renormalised truncated teacher p̂, FKL against the full
+                 student softmax and its student-side composition — the
+                 negative control for P:37 / P:130.
 
 Citations: ``P:n`` = /root/reference/PAPER.md line n, ``S:n`` = SPEC.md line n
 (SPEC is an interface donor only).  Readings of silent/garbled points are
