@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--vocab-ranks", type=int, default=0,
                     help="vocab-sharded leg on a 2-D grid: ranks per vocab group (P_voc; default all ranks). "
                          "world / P_voc token groups (BASELINE config 4: 8x1, 4x2, 2x4, 1x8)")
+    ap.add_argument("--topk", type=int, default=0,
+                    help="SURVEY §8(f) NEXT-3 negative control: the prior-art top-k teacher transfer (k <= 32).  The "
+                         "teacher's (idx, logit) top-k is produced once by kd_teacher_topk outside the timed region; "
+                         "the timed step is kd_topk_fwd_bwd (student head only, FKL against the truncated teacher)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=128)
@@ -78,7 +82,7 @@ def peaks():
 
 
 def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_precision: str = "split",
-                  teacher_lse: bool = False):
+                  teacher_lse: bool = False, topk: int = 0):
     mask_desc = {"none": "all ones", "prompt_pad": "prompt L_p~U[64,512] + padding beyond L~U[2048,4096] masked",
                  "ragged": "ragged L~U[256,8192], prompt L_p~U[32,min(512,L/2)] masked"}[cfg.mask]
     heads_b = cfg.vocab * (cfg.d_t + cfg.d_s) * 2
@@ -86,7 +90,8 @@ def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_
         "workload": f"{cfg.name}: d_t={cfg.d_t} -> d_s={cfg.d_s}, V={cfg.vocab}, {n_tok} tokens/GPU, "
                     f"{cfg.kind.upper()} T={cfg.temperature:g}" + (" +dW_s" if want_dW else "")
                     + (" [G: one bf16 plane]" if grad_precision == "bf16" else "")
-                    + (" [teacher-shipped LSE record: pass 1 sweeps W_s only]" if teacher_lse else ""),
+                    + (" [teacher-shipped LSE record: pass 1 sweeps W_s only]" if teacher_lse else "")
+                    + (f" [NEGATIVE CONTROL: top-{topk} teacher transfer, student head only]" if topk else ""),
         "baseline_config": cfg.notes,
         "tokens_per_gpu": n_tok, "d_t": cfg.d_t, "d_s": cfg.d_s, "vocab": cfg.vocab, "kind": cfg.kind,
         "temperature": cfg.temperature, "jsd_beta": cfg.jsd_beta if cfg.kind == "jsd" else None,
@@ -325,12 +330,19 @@ def main():
     dW = torch.empty(cfg.vocab, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
     stream = torch.cuda.current_stream()
 
-    lse_t = None
+    lse_t = tk = None
+    if args.topk:
+        if cfg.kind != "fkl":
+            raise SystemExit("--topk is forward KL only (kd_topk_fwd_bwd)")
+        tk = kd.teacher_topk(Ht, Wt, mask, k=args.topk, d_s=cfg.d_s, T=cfg.temperature)
     if args.teacher_lse:
         # the teacher side's record, produced once per batch by the teacher (not student work: outside the timing)
         lse_t = kd.teacher_lse(Ht, Wt, mask, d_s=cfg.d_s, T=cfg.temperature, kind=cfg.kind)
 
     def step():
+        if tk is not None:
+            return kd.topk_fwd_bwd(Hs, Ws, tk[0], tk[1], mask, d_t=cfg.d_t, T=cfg.temperature, loss_scale=1.0,
+                                   want_dW=want_dW, dW_s=dW, grad_precision=args.grad_precision, out=out)
         if lse_t is not None:
             return kd.fused_fwd_bwd_lse(Ht, Wt, Hs, Ws, lse_t, mask, dW_s=dW, out=out, **kw)
         return kd.fused_fwd_bwd(Ht, Wt, Hs, Ws, mask, dW_s=dW, out=out, **kw)
@@ -378,8 +390,9 @@ def main():
     pk = peaks()
     flops_pass = 2.0 * n_eff * cfg.vocab * (cfg.d_t + cfg.d_s)  # both LM-head GEMMs, one vocab sweep
     flops_g = 2.0 * n_eff * cfg.vocab * cfg.d_s                   # G · W_s  (or Gᵀ · H_s)
-    flops_p1 = 2.0 * n_eff * cfg.vocab * cfg.d_s if args.teacher_lse else flops_pass  # student head only
-    algo = {"pass1": flops_p1, "pass2": flops_pass, "gemm_dh": flops_g, "gemm_dW": flops_g}
+    flops_p1 = 2.0 * n_eff * cfg.vocab * cfg.d_s if (args.teacher_lse or args.topk) else flops_pass  # student only
+    flops_p2 = 2.0 * n_eff * cfg.vocab * cfg.d_s if args.topk else flops_pass
+    algo = {"pass1": flops_p1, "pass2": flops_p2, "gemm_dh": flops_g, "gemm_dW": flops_g}
     gm = 2.0 if args.grad_precision == "split" else 1.0                 # split-bf16 G: 2 MMAs per product
     exec_mult = {"pass1": 1.0, "pass2": 1.0, "gemm_dh": gm, "gemm_dW": gm}
     kernels = {}
@@ -403,10 +416,11 @@ def main():
                 "traffic": traffic,
                 "peak_note": f"bf16 dense, {pk['source']}, sustained (kernel timed inside a long step); "
                              f"burst {pk['bf16_tflops']}",
-                "algorithmic_per_launch": (f"2*tokens*V*d_s flop = " if dom == "pass1" and args.teacher_lse else
+                "algorithmic_per_launch": (f"2*tokens*V*d_s flop = " if (dom == "pass1" and args.teacher_lse)
+                                           or args.topk else
                                            f"2*tokens*V*(d_t+d_s) flop = " if dom.startswith("pass") else
                                            f"2*tokens*V*d_s flop = ") + f"{algo[dom] * args.steps / n_l:.4g}"}
-    step_useful = 2.0 * n_eff * cfg.vocab * (cfg.d_t + 2 * cfg.d_s + (cfg.d_s if want_dW else 0))
+    step_useful = 2.0 * n_eff * cfg.vocab * ((0 if args.topk else cfg.d_t) + 2 * cfg.d_s + (cfg.d_s if want_dW else 0))
     useful_frac = step_useful * args.steps / (ms_max / 1e3) / 1e12 / peak_sust
 
     # ---- e2e: same metric through the C-ABI with host buffers (pinned), every step's H2D of its inputs and D2H of
@@ -418,10 +432,12 @@ def main():
         hHs = Hs.cpu().pin_memory()
         hmask = mask.cpu().pin_memory() if mask is not None else None
         hlse = lse_t.cpu().pin_memory() if lse_t is not None else None
+        htk = (tk[0].cpu().pin_memory(), tk[1].cpu().pin_memory()) if tk is not None else None
         hloss = [torch.empty(n_tok, dtype=torch.float32).pin_memory() for _ in range(2)]
         hdh = [torch.empty(n_tok, cfg.d_s, dtype=torch.float32).pin_memory() for _ in range(2)]
         dH = [(torch.empty_like(Ht), torch.empty_like(Hs), torch.empty_like(mask) if mask is not None else None,
-               torch.empty_like(lse_t) if lse_t is not None else None) for _ in range(2)]
+               torch.empty_like(lse_t) if lse_t is not None else None,
+               (torch.empty_like(tk[0]), torch.empty_like(tk[1])) if tk is not None else None) for _ in range(2)]
         outs = [kd.KDResult(torch.empty(n_tok, dtype=torch.float32, device=dev),
                             torch.empty(n_tok, cfg.d_s, dtype=torch.float32, device=dev), None,
                             torch.zeros(1, dtype=torch.int64, device=dev)) for _ in range(2)]
@@ -431,7 +447,11 @@ def main():
 
         def upload(b):
             with torch.cuda.stream(cs):
-                dH[b][0].copy_(hHt, non_blocking=True)
+                if htk is None:  # the top-k student never sees H_t: the teacher ships (idx, logit) pairs instead
+                    dH[b][0].copy_(hHt, non_blocking=True)
+                else:
+                    dH[b][4][0].copy_(htk[0], non_blocking=True)
+                    dH[b][4][1].copy_(htk[1], non_blocking=True)
                 dH[b][1].copy_(hHs, non_blocking=True)
                 if hmask is not None:
                     dH[b][2].copy_(hmask, non_blocking=True)
@@ -448,7 +468,11 @@ def main():
                         cs.wait_event(done[b ^ 1])  # buffer b^1 was read by step i-1
                     upload(b ^ 1)
                 stream.wait_event(in_ready[b])
-                if hlse is not None:
+                if htk is not None:
+                    kd.topk_fwd_bwd(dH[b][1], Ws, dH[b][4][0], dH[b][4][1], dH[b][2], d_t=cfg.d_t, T=cfg.temperature,
+                                    loss_scale=1.0, want_dW=want_dW, dW_s=dW, grad_precision=args.grad_precision,
+                                    out=outs[b])
+                elif hlse is not None:
                     kd.fused_fwd_bwd_lse(dH[b][0], Wt, dH[b][1], Ws, dH[b][3], dH[b][2], dW_s=dW, out=outs[b], **kw)
                 else:
                     kd.fused_fwd_bwd(dH[b][0], Wt, dH[b][1], Ws, dH[b][2], dW_s=dW, out=outs[b], **kw)
@@ -470,12 +494,16 @@ def main():
         torch.cuda.synchronize()
         ms_e2e = max_over_ranks(t0.elapsed_time(t1))
         assert torch.equal(hloss[(args.steps - 1) & 1], outs[(args.steps - 1) & 1].loss.cpu())
-        h2d = n_tok * (cfg.d_t + cfg.d_s) * 2 + (n_tok if mask is not None else 0) + (8 * n_tok if hlse is not None else 0)
+        h2d = n_tok * ((0 if htk else cfg.d_t) + cfg.d_s) * 2 + (n_tok if mask is not None else 0) \
+            + (8 * n_tok if hlse is not None else 0) + (8 * args.topk * n_tok if htk else 0)
         d2h = n_tok * 4 + n_tok * cfg.d_s * 4
         e2e = {"value": world * n_eff * args.steps / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
-               "note": "heads resident in HBM (weights); per step: H_t/H_s (+mask) pinned-host->device and "
-                       "loss/dh_s device->pinned-host, on a copy stream overlapped with the neighbouring steps"}
+               "note": "heads resident in HBM (weights); per step: " +
+                       ("H_s + the teacher's top-k (idx, logit) pairs" if htk else
+                        "H_t/H_s + the teacher's LSE record" if hlse is not None else "H_t/H_s") +
+                       " (+mask) pinned-host->device and loss/dh_s device->pinned-host, on a copy stream overlapped "
+                       "with the neighbouring steps"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -500,7 +528,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kd_inputs recipe, seeded)",
-                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision, args.teacher_lse),
+                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision, args.teacher_lse, args.topk),
                 "clocks": clocks, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "roofline": roofline, "cpu_baseline": cpu,
                 "useful_flop_frac": useful_frac, "kernels": kernels, "nonfinite_tokens": nonfinite,

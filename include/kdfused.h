@@ -133,6 +133,29 @@ kd_status kd_fused_fwd_bwd_lse(const kd_problem* p, const void* h_t, const void*
                                float* dW_s, int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
                                void* stream);
 
+/* ---- top-k teacher baseline: the prior-art transfer KDFlow replaces — "only transferring
+ * the top-k logits breaks the mathematical equivalence of the loss function" (Table 1).  A
+ * negative control: it measures what is lost (and what the student step costs without the teacher head).
+ * Definition (SPEC, oracle/kd_topk.py): K_n = the k largest teacher logits of row n (ties: lower index
+ * first, reading R17); p̂ = softmax of those k logits / T, 0 off the support; q = softmax(z_s / T) over the full
+ * vocabulary; ℓ_n = FKL_topk = Σ_{v∈K_n} p̂_v ln(p̂_v / q_v); G = loss_scale·mask_n·(q − p̂)/T.
+ *
+ * kd_teacher_topk (teacher side; full vocabulary; d_s / kind only size the workspace):
+ *   h_t [N, d_t] bf16, W_t [V, d_t] bf16, mask [N] u8 or NULL (rows with mask = 0 are not written)
+ *   k in [1, min(V, 32)] (k > 32: KD_ERR_UNSUPPORTED; k < 1 or k > V: KD_ERR_INVALID_ARG)
+ *   topk_idx [N, k] i32 out: vocabulary indices, by (logit desc, index asc)
+ *   topk_val [N, k] f32 out: the raw teacher logits z_t = h_t·W_t[v] (fp32 tensor-core accumulation; not / T)
+ * kd_topk_fwd_bwd (student side; forward KL only — RKL against a truncated teacher is +inf, KD_ERR_UNSUPPORTED):
+ *   the student's own head only: h_s [N, d_s], W_s [V, d_s] (p->d_t is ignored but must be a valid width);
+ *   topk_idx / topk_val as written by kd_teacher_topk (or any teacher: k distinct indices in [0, V) per row);
+ *   loss, dh_s, dW_s, n_nonfinite, workspace as kd_fused_fwd_bwd.  A row holding an index outside [0, V) or a
+ *   non-finite logit gets loss NaN (counted in n_nonfinite) and no teacher term in G. */
+kd_status kd_teacher_topk(const kd_problem* p, const void* h_t, const void* W_t, const uint8_t* mask, int32_t k,
+                          int32_t* topk_idx, float* topk_val, void* workspace, size_t workspace_bytes, void* stream);
+kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s, const uint8_t* mask, int32_t k,
+                          const int32_t* topk_idx, const float* topk_val, float* loss, float* dh_s, float* dW_s,
+                          int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- vocabulary-sharded execution (north_star: "vocabulary sharding of W_t/W_s, with a tiny
  * all-reduce of per-token stats").  Rank r owns rows [v_begin, v_end) of both heads.
  * FKL/RKL: kd_vocab_stats -> exchange -> kd_vocab_backward.  JSD/TVD: see kd_vocab_partials below.

@@ -6,8 +6,8 @@ dL/dW_s — hand-written tcgen05/TMA kernels behind the C ABI in ``include/kdfus
 """
 from .kdfused import (KDError, KDProblem, KDResult, VocabFixState, fused_fwd_bwd, fused_fwd_bwd_lse, gemm_bf16_f32,
                       last_launch_count, lib, make_problem, profile_enable, profile_read, vocab_backward,
-                      teacher_lse, vocab_finish, vocab_partials, vocab_stats, workspace_size)
+                      teacher_lse, teacher_topk, topk_fwd_bwd, vocab_finish, vocab_partials, vocab_stats, workspace_size)
 
 __all__ = ["KDError", "KDProblem", "KDResult", "VocabFixState", "fused_fwd_bwd", "fused_fwd_bwd_lse", "gemm_bf16_f32",
            "last_launch_count", "lib", "make_problem", "profile_enable", "profile_read", "vocab_backward",
-           "teacher_lse", "vocab_finish", "vocab_partials", "vocab_stats", "workspace_size"]
+           "teacher_lse", "teacher_topk", "topk_fwd_bwd", "vocab_finish", "vocab_partials", "vocab_stats", "workspace_size"]

@@ -43,8 +43,17 @@ cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0
                            float* kj, long long N, cudaStream_t s);
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
                              const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
-                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s);
+                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v = nullptr,
+                             const float* corr2_r = nullptr, int n_slots2 = 0);
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
+cudaError_t launch_topk_merge(const float* tk_val, const int* tk_idx, int n_slots, int n_rows, int row0,
+                              const int* n_eff, const int* idx, int k, int v_base, int* out_idx, float* out_val,
+                              cudaStream_t s);
+cudaError_t launch_topk_fix(const __nv_bfloat16* hs, const __nv_bfloat16* Ws, int d_s, int V, int n_rows, int row0,
+                            const int* n_eff, const int* idx, int k, const int* tk_i, const float* tk_v, float alpha,
+                            const float* fstats, float gscale, __nv_bfloat16* ghi, __nv_bfloat16* glo, int* corr_v,
+                            float* corr_r, int n_corr, int* tkr_v, float* tkr_r, float* loss, long long* nonfinite,
+                            cudaStream_t s);
 }  // namespace kd
 
 using namespace kd;
@@ -73,9 +82,9 @@ static kd_status fail(kd_status st, const char* fmt, ...) {
 // When enabled, every launch is bracketed by two CUDA events on the launch stream; kd_profile_read()
 // resolves them into per-kernel totals (bench.py uses this for the live roofline figure).
 enum KernelId : int { K_COMPACT, K_GATHER, K_ZERO, K_PASS1, K_MERGE, K_PASS2, K_KFIX, K_GEMM_DH, K_REDUCE_DH,
-                      K_GEMM_DW, K_GEMM, K_NUM };
+                      K_GEMM_DW, K_GEMM, K_TOPK, K_NUM };
 static const char* kKernelNames[K_NUM] = {"compact", "gather", "zero_masked", "pass1", "merge", "pass2",
-                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm"};
+                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm", "topk"};
 struct ProfRec { int id; cudaEvent_t a, b; };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -194,7 +203,8 @@ struct Plan {
   bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
   int g_planes;  // bf16 planes of G fed to the backward GEMMs: 2 (split hi + lo) or 1 (KD_GRAD_BF16)
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
-      off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, off_zscr, total;
+      off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, off_zscr, off_tkv, off_tki, off_tkr_v, off_tkr_r,
+      total;
 };
 
 // Static round-robin of units over a persistent grid: makespan in tiles (+ per-unit refill cost).
@@ -319,7 +329,15 @@ static Plan make_plan(const kd_problem* p) {
   P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
   P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
   P.off_zscr = take((size_t)P.num_sms * P.bn * kBM * 4);  // decoupled pass 2 staging (19 MB: L2-resident)
+  P.off_tkr_v = take((size_t)P.Nc * kTopK * 4);  // top-k baseline: residual slots of the k support entries
+  P.off_tkr_r = take((size_t)P.Nc * kTopK * 4);
   P.total = o;
+  // kd_teacher_topk's candidate lists [n_split*parts][Nc][kTopK] (values, indices) reuse the G / dh scratch, which
+  // that call does not touch (extended only if a tiny vocabulary makes the scratch smaller than the lists)
+  const size_t tk_bytes = align256((size_t)P.n_split * epi_parts(1, KIND_TOPK) * P.Nc * kTopK * 4);
+  P.off_tkv = P.off_ghi;
+  P.off_tki = P.off_ghi + tk_bytes;
+  if (P.off_tki + tk_bytes > P.total) P.total = P.off_tki + tk_bytes;
   return P;
 }
 
@@ -346,8 +364,10 @@ struct Ctx {
 }  // namespace
 
 // teacher_only (kd_teacher_lse): h_s / W_s are absent; the student maps alias the teacher's and are never read.
+// student_only (kd_topk_fwd_bwd): h_t / W_t are absent; the teacher maps alias the student's and are never read.
 static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
-                          const uint8_t* mask, int64_t* n_nonfinite, bool teacher_only = false) {
+                          const uint8_t* mask, int64_t* n_nonfinite, bool teacher_only = false,
+                          bool student_only = false) {
   const Plan& P = c.P;
   c.n_eff = ws_at<int>(c.ws, P.off_neff);
   c.nonfinite = n_nonfinite ? reinterpret_cast<long long*>(n_nonfinite) : ws_at<long long>(c.ws, P.off_nonfinite);
@@ -359,7 +379,8 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
     KD_LAUNCH(K_COMPACT, launch_compact(mask, P.N, idx, c.n_eff, c.s));
     auto* pt = ws_at<__nv_bfloat16>(c.ws, P.off_ht);
     auto* ps = ws_at<__nv_bfloat16>(c.ws, P.off_hs);
-    KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_t), P.d_t, pt, P.d_t, P.N, idx, c.n_eff, c.s));
+    if (!student_only)
+      KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_t), P.d_t, pt, P.d_t, P.N, idx, c.n_eff, c.s));
     if (!teacher_only)
       KD_LAUNCH(K_GATHER, launch_gather(static_cast<const __nv_bfloat16*>(h_s), P.d_s, ps, P.d_s, P.N, idx, c.n_eff, c.s));
     c.ht = pt;
@@ -372,6 +393,13 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
     c.idx = nullptr;
   }
   kd_status st;
+  if (student_only) {
+    if ((st = make_map(&c.maps[2], c.hs, P.d_s, P.N, (uint64_t)P.d_s * 2, kBK, kBM)) != KD_OK) return st;
+    if ((st = make_map(&c.maps[3], c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, kBK, P.bn / P.cg)) != KD_OK) return st;
+    c.maps[0] = c.maps[2];
+    c.maps[1] = c.maps[3];
+    return KD_OK;
+  }
   if ((st = make_map(&c.maps[0], c.ht, P.d_t, P.N, (uint64_t)P.d_t * 2, kBK, kBM)) != KD_OK) return st;
   if ((st = make_map(&c.maps[1], c.Wt, P.d_t, P.V_r, (uint64_t)P.d_t * 2, kBK, P.bn / P.cg)) != KD_OK) return st;
   if (teacher_only) {
@@ -417,6 +445,8 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.l2_hints = l2_hints;
   pp.side_lo = 0;
   pp.side_hi = 2;
+  pp.tk_val = ws_at<float>(c.ws, P.off_tkv);
+  pp.tk_idx = ws_at<int>(c.ws, P.off_tki);
   return pp;
 }
 
@@ -428,18 +458,19 @@ static int pass_grid(const Plan& P) {  // CTAs (a multiple of the CTA group)
 
 // pass 2 for one chunk whose final per-token statistics are already in fstats: G (FKL/RKL) or the two JSD/TVD
 // planes + partial K, J.
-static kd_status grad_chunk(Ctx& c, int row0) {
+static kd_status grad_chunk(Ctx& c, int row0, int side_lo = 0) {
   const Plan& P = c.P;
   PassParams pp = pass_params(c, row0);
+  pp.side_lo = side_lo;  // 1: student-only pass 2 (top-k baseline: G = gscale·q, the teacher put back afterwards)
   static const bool p2_coupled = env_int("KD_P2_COUPLED", 0) != 0;
-  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, p2_coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, p2_coupled && side_lo == 0, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
   return KD_OK;
 }
 
 // After pass 2: [JSD/TVD fix-up with the local K partials, or with the P ranks' per-token totals kj_ranks]
 // + dh GEMM (+ split-K reduce) + dW GEMM for one chunk.
 static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW, const float* kj_ranks,
-                              int n_ranks) {
+                              int n_ranks, int topk = 0) {
   const Plan& P = c.P;
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
@@ -475,7 +506,9 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
                                    P.g_planes == 2 ? &mg_lo : nullptr, &mw, gp, P.num_sms, c.s));
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                                           P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
-                                          P.n_split * epi_parts(2, P.kind) * kCorrSlots, c.Ws, c.s));
+                                          P.n_split * epi_parts(2, P.kind) * kCorrSlots, c.Ws, c.s,
+                                          topk ? ws_at<int>(c.ws, P.off_tkr_v) : nullptr,
+                                          topk ? ws_at<float>(c.ws, P.off_tkr_r) : nullptr, topk));
   if (dW) {
     CUtensorMap ma_hi, ma_lo, mh;
     // dW_s += Gᵀ · H_s: A = Gᵀ [g_ld][Nc] is K-major (K = tokens), B = H_s chunk MN-major
@@ -626,6 +659,85 @@ kd_status kd_teacher_lse(const kd_problem* p, const void* h_t, const void* W_t, 
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, KD_FKL), P.Nc, row0,
                                     c.n_eff, KD_FKL, 2, nullptr, nullptr, lse_t, (long long)P.N, c.idx, 0,
                                     c.nonfinite, 0, c.s));
+  }
+  return KD_OK;
+}
+
+kd_status kd_teacher_topk(const kd_problem* p, const void* h_t, const void* W_t, const uint8_t* mask, int32_t k,
+                          int32_t* topk_idx, float* topk_val, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = validate(p, true);
+  if (st != KD_OK) return st;
+  if (k < 1 || k > p->vocab) return fail(KD_ERR_INVALID_ARG, "k must lie in [1, vocab] (got %d)", k);
+  if (k > kTopK) return fail(KD_ERR_UNSUPPORTED, "k = %d > %d (the register lists of the top-k pass)", k, kTopK);
+  Ctx c{};
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  const Plan& P = c.P;
+  if (P.N > 0 && (!h_t || !topk_idx || !topk_val)) return fail(KD_ERR_INVALID_ARG, "NULL h_t / topk_idx / topk_val");
+  if (!W_t) return fail(KD_ERR_INVALID_ARG, "NULL W_t");
+  if ((h_t && !aligned16(h_t)) || !aligned16(W_t)) return fail(KD_ERR_ALIGNMENT, "h_t / W_t must be 16-byte aligned");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255) || workspace_bytes < P.total)
+    return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace must be 256-byte aligned and >= %zu bytes", P.total);
+  if (P.N == 0) return KD_OK;
+  if ((st = prologue(c, h_t, W_t, nullptr, nullptr, mask, nullptr, true)) != KD_OK) return st;
+  for (int ch = 0; ch < P.n_chunks; ++ch) {
+    const int row0 = ch * P.Nc;
+    PassParams pp = pass_params(c, row0);
+    pp.side_hi = 1;  // teacher half-tiles only
+    KD_LAUNCH(K_PASS1, launch_pass(1, KIND_TOPK, false, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_TOPK, launch_topk_merge(pp.tk_val, pp.tk_idx, P.n_split * epi_parts(1, KIND_TOPK), P.Nc, row0,
+                                        c.n_eff, c.idx, k, (int)p->v_begin, topk_idx, topk_val, c.s));
+  }
+  return KD_OK;
+}
+
+kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s, const uint8_t* mask, int32_t k,
+                          const int32_t* topk_idx, const float* topk_val, float* loss, float* dh_s, float* dW_s,
+                          int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = validate(p, true);
+  if (st != KD_OK) return st;
+  if (p->kind != KD_FKL)
+    return fail(KD_ERR_UNSUPPORTED, "kd_topk_fwd_bwd is forward KL only: RKL against a truncated teacher is +inf "
+                                    "off the support (DESIGN.md R17)");
+  if (k < 1 || k > p->vocab) return fail(KD_ERR_INVALID_ARG, "k must lie in [1, vocab] (got %d)", k);
+  if (k > kTopK) return fail(KD_ERR_UNSUPPORTED, "k = %d > %d", k, kTopK);
+  Ctx c{};
+  c.p = p;
+  c.P = make_plan(p);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.ws = workspace;
+  float* dW = p->want_dW ? dW_s : nullptr;
+  // h_t / W_t are not inputs of the top-k student: the student's own tensors stand in for the pointer checks
+  if ((st = check_common(p, h_s, W_s, h_s, W_s, loss, dh_s, dW, workspace, workspace_bytes, c.P)) != KD_OK) return st;
+  const Plan& P = c.P;
+  if (P.N > 0 && (!topk_idx || !topk_val)) return fail(KD_ERR_INVALID_ARG, "NULL topk_idx / topk_val");
+  if (dW && !p->accumulate_dW) KD_CUDA(cudaMemsetAsync(dW, 0, (size_t)P.V_r * P.d_s * 4, c.s));
+  if (P.N == 0) {
+    if (n_nonfinite) KD_CUDA(cudaMemsetAsync(n_nonfinite, 0, 8, c.s));
+    return KD_OK;
+  }
+  if ((st = prologue(c, nullptr, nullptr, h_s, W_s, mask, n_nonfinite, false, true)) != KD_OK) return st;
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s, P.d_s, c.s));
+  for (int ch = 0; ch < P.n_chunks; ++ch) {
+    const int row0 = ch * P.Nc;
+    PassParams pp = pass_params(c, row0);
+    pp.side_lo = 1;  // student half-tiles only: LSE_s (the teacher's part of the record mirrors it, unused)
+    KD_LAUNCH(K_PASS1, launch_pass(1, KD_FKL, false, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0,
+                                    c.n_eff, P.kind, 0, ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0,
+                                    c.nonfinite, 0, c.s));
+    if ((st = grad_chunk(c, row0, 1)) != KD_OK) return st;
+    KD_LAUNCH(K_TOPK, launch_topk_fix(c.hs, c.Ws, P.d_s, P.V_r, P.Nc, row0, c.n_eff, c.idx, k, topk_idx, topk_val,
+                                      pp.alpha, pp.fstats, pp.gscale, pp.g_hi, pp.g_lo, pp.corr_v, pp.corr_r,
+                                      P.n_split * epi_parts(2, P.kind) * kCorrSlots, ws_at<int>(c.ws, P.off_tkr_v),
+                                      ws_at<float>(c.ws, P.off_tkr_r), loss, c.nonfinite, c.s));
+    if ((st = finish_chunk(c, row0, loss, dh_s, dW, nullptr, 0, k)) != KD_OK) return st;
   }
   return KD_OK;
 }

@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ par
                                                    int d_s, int n_rows, int row0, const int* __restrict__ n_eff,
                                                    const int* __restrict__ idx, float* __restrict__ dh,
                                                    const int* __restrict__ corr_v, const float* __restrict__ corr_r,
-                                                   int n_slots, const __nv_bfloat16* __restrict__ Ws) {
+                                                   int n_slots, const __nv_bfloat16* __restrict__ Ws,
+                                                   const int* __restrict__ corr2_v, const float* __restrict__ corr2_r,
+                                                   int n_slots2) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int valid = min(n_rows, *n_eff - row0);
@@ -335,6 +337,35 @@ __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ par
         }
       }
     }
+    if (corr2_r) {  // top-k baseline: exact residuals of the k support entries (k_topk_fix)
+      const float* rr = corr2_r + (size_t)r * n_slots2;
+      const int* vv = corr2_v + (size_t)r * n_slots2;
+      for (int base = 0; base < n_slots2; base += 32) {
+        const float myr = base + lane < n_slots2 ? rr[base + lane] : 0.f;
+        unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
+        while (live) {
+          const int src = __ffs(live) - 1;
+          live &= live - 1;
+          const float coef = __shfl_sync(0xffffffffu, myr, src);
+          const __nv_bfloat16* w = Ws + (size_t)vv[base + src] * d_s;
+#pragma unroll
+          for (int g = 0; g < kRedVec; ++g) {
+            const int col = cb + (g * 32 + lane) * 8;
+            if (col < d_s) {
+              const uint4 q = *reinterpret_cast<const uint4*>(w + col);
+              acc[g][0] = fmaf(coef, bf16lo_to_f32(q.x), acc[g][0]);
+              acc[g][1] = fmaf(coef, bf16hi_to_f32(q.x), acc[g][1]);
+              acc[g][2] = fmaf(coef, bf16lo_to_f32(q.y), acc[g][2]);
+              acc[g][3] = fmaf(coef, bf16hi_to_f32(q.y), acc[g][3]);
+              acc[g][4] = fmaf(coef, bf16lo_to_f32(q.z), acc[g][4]);
+              acc[g][5] = fmaf(coef, bf16hi_to_f32(q.z), acc[g][5]);
+              acc[g][6] = fmaf(coef, bf16lo_to_f32(q.w), acc[g][6]);
+              acc[g][7] = fmaf(coef, bf16hi_to_f32(q.w), acc[g][7]);
+            }
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int g = 0; g < kRedVec; ++g) {
       const int col = cb + (g * 32 + lane) * 8;
@@ -350,6 +381,193 @@ __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ par
 cudaError_t launch_compact(const uint8_t* mask, int N, int* idx, int* n_eff, cudaStream_t s) {
   if (mask) k_compact<<<1, 1024, 0, s>>>(mask, N, idx, n_eff);
   else k_set_count<<<1, 1, 0, s>>>(n_eff, N);
+  return cudaGetLastError();
+}
+// ------------------------------------------------------------------ top-k teacher baseline
+// (value desc, index asc) order of the candidate lists
+__device__ __forceinline__ bool tk_better(float x, int xi, float y, int yi) { return x > y || (x == y && xi < yi); }
+
+// Per row: the k best of the n_slots sorted candidate lists the top-k pass wrote (tk_val/tk_idx
+// [n_slots][n_rows][kTopK]).  One warp per row: lane l folds lists l, l+32, ... into its own register top-kTopK
+// (a list stops at its first non-improving entry), then k rounds of a warp arg-best pop the global order.
+// Output per ORIGINAL row: out_idx [N][k] (global vocab index), out_val [N][k] (raw teacher logit).
+__global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ tk_val, const int* __restrict__ tk_idx,
+                                                    int n_slots, int n_rows, int row0, const int* __restrict__ n_eff,
+                                                    const int* __restrict__ idx, int k, int v_base,
+                                                    int* __restrict__ out_idx, float* __restrict__ out_val) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int valid = min(n_rows, *n_eff - row0);
+  if (r >= valid) return;
+  float tv[kTopK];
+  int ti[kTopK];
+#pragma unroll
+  for (int j = 0; j < kTopK; ++j) { tv[j] = -INFINITY; ti[j] = 0x7fffffff; }
+  for (int sl = lane; sl < n_slots; sl += 32) {
+    const size_t base = ((size_t)sl * n_rows + r) * kTopK;
+#pragma unroll 1
+    for (int j = 0; j < kTopK; ++j) {
+      float x = tk_val[base + j];
+      int xi = tk_idx[base + j];
+      if (!tk_better(x, xi, tv[kTopK - 1], ti[kTopK - 1])) break;  // the list is sorted: nothing further improves
+#pragma unroll
+      for (int t = 0; t < kTopK; ++t) {
+        const bool gt = tk_better(x, xi, tv[t], ti[t]);
+        const float a = tv[t];
+        const int b = ti[t];
+        tv[t] = gt ? x : a;
+        ti[t] = gt ? xi : b;
+        x = gt ? a : x;
+        xi = gt ? b : xi;
+      }
+    }
+  }
+  const int orow = idx ? idx[row0 + r] : row0 + r;
+  for (int j = 0; j < k; ++j) {
+    float bv = tv[0];
+    int bi = ti[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (tk_better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) {
+      out_idx[(size_t)orow * k + j] = bi == 0x7fffffff ? -1 : bi + v_base;
+      out_val[(size_t)orow * k + j] = bv;
+    }
+    if (ti[0] == bi && tv[0] == bv) {  // the owner pops its head (indices are unique across lists)
+#pragma unroll
+      for (int t = 0; t < kTopK - 1; ++t) { tv[t] = tv[t + 1]; ti[t] = ti[t + 1]; }
+      tv[kTopK - 1] = -INFINITY;
+      ti[kTopK - 1] = 0x7fffffff;
+    }
+  }
+}
+
+// Student side of the top-k baseline, after its student-only pass 2 wrote G = gscale·q for every column: per row,
+// put the truncated teacher back in at its k support columns,
+//   p̂_j = 2^{a_j − m} / Σ_i 2^{a_i − m},  a_j = α·val_j  (renormalised over the support)
+//   g_j = gscale·(q_j − p̂_j)   (split bf16 hi + lo, overwriting the pass-2 entry; stale residual slots dropped)
+//   ℓ   = ln2 · Σ_j p̂_j (log2 p̂_j − log2 q_j)     (FKL_topk; q from the same base-2 LSE record as pass 2)
+// with z_s at the support recomputed as an fp32 dot product h_s[n]·W_s[v] (warp per row; k·d_s MACs).
+// An index outside [0, V) makes the row's loss NaN (counted in n_nonfinite) and leaves G untouched there.
+__global__ void __launch_bounds__(256) k_topk_fix(const __nv_bfloat16* __restrict__ hs, const __nv_bfloat16* __restrict__ Ws,
+                                                  int d_s, int V, int n_rows, int row0, const int* __restrict__ n_eff,
+                                                  const int* __restrict__ idx, int k, const int* __restrict__ tk_i,
+                                                  const float* __restrict__ tk_v, float alpha,
+                                                  const float* __restrict__ fstats, float gscale,
+                                                  __nv_bfloat16* __restrict__ ghi, __nv_bfloat16* __restrict__ glo,
+                                                  int* __restrict__ corr_v, float* __restrict__ corr_r, int n_corr,
+                                                  int* __restrict__ tkr_v, float* __restrict__ tkr_r,
+                                                  float* __restrict__ loss, long long* __restrict__ nonfinite) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int valid = min(n_rows, *n_eff - row0);
+  if (r >= valid) return;
+  const int orow = idx ? idx[row0 + r] : row0 + r;
+  const bool mine = lane < k;
+  const int v_me = mine ? tk_i[(size_t)orow * k + lane] : -1;
+  const float a_me = mine ? tk_v[(size_t)orow * k + lane] * alpha : -INFINITY;
+  const bool bad = __any_sync(0xffffffffu, mine && (v_me < 0 || v_me >= V || !isfinite(a_me)));
+  // z_s at the support columns
+  const __nv_bfloat16* h = hs + (size_t)(row0 + r) * d_s;
+  float zs_me = 0.f;
+  for (int j = 0; j < k; ++j) {
+    const int v = __shfl_sync(0xffffffffu, v_me, j);
+    float acc = 0.f;
+    if (!bad) {
+      const __nv_bfloat16* w = Ws + (size_t)v * d_s;
+      for (int e = lane * 8; e < d_s; e += 256) {
+        const uint4 hv = *reinterpret_cast<const uint4*>(h + e);
+        const uint4 wv = *reinterpret_cast<const uint4*>(w + e);
+        const uint32_t hh[4] = {hv.x, hv.y, hv.z, hv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc = fmaf(bf16lo_to_f32(hh[q]), bf16lo_to_f32(ww[q]), acc);
+          acc = fmaf(bf16hi_to_f32(hh[q]), bf16hi_to_f32(ww[q]), acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == j) zs_me = acc;
+  }
+  float m = a_me;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float e_me = mine ? exp2f(a_me - m) : 0.f;
+  float S = e_me;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+  const float Ms2 = fstats[2 * n_rows + r], lSs = fstats[3 * n_rows + r];
+  const float ph = e_me / S;
+  const float u = fmaf(zs_me, alpha, -Ms2);        // log2 q + log2 S_s
+  float ell = mine ? ph * ((a_me - m - log2f(S)) - (u - lSs)) : 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ell += __shfl_xor_sync(0xffffffffu, ell, o);
+  ell *= kLn2;
+  if (bad) ell = __int_as_float(0x7fc00000);
+  // G at the support: start from the value pass 2 formed for q there (hi + lo + its exact residual, if it recorded
+  // one: then bit-for-bit the fp32 gscale·q of the GEMM logits, consistent with the LSE record; the dot-product
+  // logit above differs from the GEMM's by its rounding, and e^{δz} would move q_top ≈ 1 by δz itself)
+  __shared__ float s_res[8][32];
+  float* my_res = s_res[threadIdx.x >> 5];
+  my_res[lane] = 0.f;
+  __syncwarp();
+  if (!bad && corr_v) {
+    const size_t cb = (size_t)r * n_corr;
+    for (int base = 0; base < n_corr; base += 32) {  // warp-uniform trip count (shuffles inside)
+      const int i = base + lane;
+      const int cv = i < n_corr ? corr_v[cb + i] : -1;
+      int hit = -1;
+      for (int j = 0; j < k; ++j)
+        if (cv == __shfl_sync(0xffffffffu, v_me, j)) hit = j;
+      if (hit >= 0 && cv >= 0) {  // each support column sits in one unit's slots at most once
+        my_res[hit] = corr_r[cb + i];
+        corr_r[cb + i] = 0.f;  // folded into the new support value below
+      }
+    }
+  }
+  __syncwarp();
+  if (mine) {
+    float res = 0.f;
+    if (!bad) {
+      const size_t e = (size_t)v_me * n_rows + r;
+      const float g_old = (__bfloat162float(ghi[e]) + (glo ? __bfloat162float(glo[e]) : 0.f)) + my_res[lane];
+      const float g = g_old - gscale * ph;
+      const uint32_t hb = pack_bf16x2(g, 0.f);
+      const float lo = g - bf16lo_to_f32(hb);
+      const __nv_bfloat16 lb = __float2bfloat16_rn(lo);
+      ghi[e] = __ushort_as_bfloat16((unsigned short)(hb & 0xFFFFu));
+      if (glo) glo[e] = lb;
+      // exact residual of the stored split (k_reduce_dh adds res·W_s[v]): |g| reaches 1 at the support
+      res = g - (bf16lo_to_f32(hb) + (glo ? __bfloat162float(lb) : 0.f));
+    }
+    tkr_v[(size_t)r * k + lane] = bad ? 0 : v_me;
+    tkr_r[(size_t)r * k + lane] = res;
+  }
+  if (lane == 0) {
+    loss[orow] = ell;
+    if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
+  }
+}
+
+cudaError_t launch_topk_merge(const float* tk_val, const int* tk_idx, int n_slots, int n_rows, int row0,
+                              const int* n_eff, const int* idx, int k, int v_base, int* out_idx, float* out_val,
+                              cudaStream_t s) {
+  k_topk_merge<<<(n_rows + 7) / 8, 256, 0, s>>>(tk_val, tk_idx, n_slots, n_rows, row0, n_eff, idx, k, v_base,
+                                                 out_idx, out_val);
+  return cudaGetLastError();
+}
+cudaError_t launch_topk_fix(const __nv_bfloat16* hs, const __nv_bfloat16* Ws, int d_s, int V, int n_rows, int row0,
+                            const int* n_eff, const int* idx, int k, const int* tk_i, const float* tk_v, float alpha,
+                            const float* fstats, float gscale, __nv_bfloat16* ghi, __nv_bfloat16* glo, int* corr_v,
+                            float* corr_r, int n_corr, int* tkr_v, float* tkr_r, float* loss, long long* nonfinite,
+                            cudaStream_t s) {
+  if (d_s % 8) return cudaErrorInvalidValue;
+  k_topk_fix<<<(n_rows + 7) / 8, 256, 0, s>>>(hs, Ws, d_s, V, n_rows, row0, n_eff, idx, k, tk_i, tk_v, alpha, fstats,
+                                               gscale, ghi, glo, corr_v, corr_r, n_corr, tkr_v, tkr_r, loss, nonfinite);
   return cudaGetLastError();
 }
 cudaError_t launch_gather(const __nv_bfloat16* src, long long src_ld, __nv_bfloat16* dst, int d, int N,
@@ -411,10 +629,11 @@ cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0
 }
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
                              const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
-                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s) {
+                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v,
+                             const float* corr2_r, int n_slots2) {
   if (d_s % 8 != 0) return cudaErrorInvalidValue;
   k_reduce_dh<<<(n_rows + 7) / 8, 256, 0, s>>>(part, split_stride, k_split, d_s, n_rows, row0, n_eff, idx, dh, corr_v,
-                                                corr_r, n_slots, Ws);
+                                                corr_r, n_slots, Ws, corr2_v, corr2_r, n_slots2);
   return cudaGetLastError();
 }
 

@@ -5,7 +5,9 @@
 
 namespace kd {
 
-enum Kind : int { KIND_FKL = 0, KIND_RKL = 1, KIND_JSD = 2, KIND_TVD = 3 };
+enum Kind : int { KIND_FKL = 0, KIND_RKL = 1, KIND_JSD = 2, KIND_TVD = 3,
+                  KIND_TOPK = 4 /* kernel-internal: teacher-only pass 1 selecting the per-row top-kTopK logits */ };
+constexpr int kTopK = 32;  // largest k of the top-k teacher baseline (kd_teacher_topk): per-thread register lists
 
 constexpr int kBM = 128;        // token rows per tile (UMMA M, one TMEM lane per token)
 constexpr int kBN = 128;        // vocab columns per tile in the fused passes
@@ -57,6 +59,10 @@ struct PassParams {
   // (0, 2) = both (default); (1, 2) = student only (teacher LSE supplied by the caller);
   // (0, 1) = teacher only (kd_teacher_lse).
   int side_lo, side_hi;
+  // KIND_TOPK pass 1: per (record slot, row) the kTopK largest teacher logits, sorted by (value desc, index asc):
+  // tk_val / tk_idx [n_split*parts][n_rows][kTopK]
+  float* tk_val;
+  int* tk_idx;
 };
 
 // Generic bf16 GEMM with fp32 TMEM accumulation: D[M, N] = sum_{a < NUM_A} A_a[M, K] * B[N, K]^T.

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
   using C = PassCfg<CG, BN>;
   constexpr int kStages = C::kStages;
   constexpr int kNB = DEC ? 2 : C::kNumBuf;  // accumulator buffers (DEC: one half-tile side per buffer)
-  static_assert(!DEC || PASS == 2 || KIND == KIND_FKL, "decoupled pass 1 uses the FKL role order");
+  static_assert(!DEC || PASS == 2 || KIND == KIND_FKL || KIND == KIND_TOPK, "decoupled pass 1 uses the FKL role order");
+  static_assert(KIND != KIND_TOPK || (PASS == 1 && DEC), "top-k selection is a one-sided decoupled pass 1");
   constexpr int kBMt = kBM * CG;  // token rows per work tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
         const int vrow = vt * BN + rank * (BN / CG);           // this CTA's share of the vocab tile
         // decoupled pass 1 may sweep one side only: teacher K blocks are [0, kb_t), student [kb_t, kb_t + kb_s)
-        const int kb_lo = (DEC && PASS == 1 && p.side_lo == 1) ? p.kb_t : 0;
+        const int kb_lo = (DEC && p.side_lo == 1) ? p.kb_t : 0;  // pass 2 too: student-only (top-k baseline)
         const int kb_hi = (DEC && PASS == 1 && p.side_hi == 1) ? p.kb_t : p.kb_t + p.kb_s;
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++kit) {
           const uint32_t st = kit % kStages, ph = (kit / kStages) & 1;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       for (int u = worker; u < n_units; u += n_workers) {
         const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
-          const int s_lo = PASS == 1 ? p.side_lo : 0, s_hi = PASS == 1 ? p.side_hi : 2;
+          const int s_lo = p.side_lo, s_hi = PASS == 1 ? p.side_hi : 2;
           for (int side = s_lo; side < s_hi; ++side, ++it) {
             const uint32_t buf = it & 1, tph = (it >> 1) & 1;
 #ifdef KD_EPI_TIMING
@@ -334,7 +335,63 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         else mbar_arrive_relaxed(&tempty[buf]);
       }
     };
-    if constexpr (DEC && PASS == 1) {
+    if constexpr (KIND == KIND_TOPK) {
+      // teacher-only sweep keeping, per row, the kTopK largest logits of this thread's columns (sorted by value desc,
+      // index asc; the baseline KDFlow replaces: P:37).  Columns arrive in increasing vocab order, so a value
+      // equal to the current minimum is never better; acceptances become rare after the first tiles of a unit.
+      constexpr int kChunks = BN / 32;
+      const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
+      for (int u = worker; u < n_units; u += n_workers) {
+        const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
+        const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;
+        const bool row_ok = r_local < valid_rows;
+        const int rslot = (u / m_tiles) * EP + part;
+        float tv[kTopK];
+        int ti[kTopK];
+#pragma unroll
+        for (int j = 0; j < kTopK; ++j) { tv[j] = -INFINITY; ti[j] = 0x7fffffff; }
+        for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
+          const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+          mbar_wait(&tfull[buf], tph);
+          tc_fence_after();
+          const uint32_t t_addr = tmem_base + lane_addr + buf * BN;
+#pragma unroll 1
+          for (int c = c_beg; c < c_end; ++c) {
+            float z[32];
+            tmem_ld32_sync(t_addr + c * 32, z);
+            if (c == c_end - 1) release(buf);
+            const int v0 = vt * BN + c * 32;
+            const int nvalid = min(32, p.V_r - v0);
+            if (nvalid <= 0) continue;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float x = i < nvalid ? z[i] : -INFINITY;
+              if (x > tv[kTopK - 1]) {
+                int xi = v0 + i;
+#pragma unroll
+                for (int j = 0; j < kTopK; ++j) {  // insertion by (value desc, index asc); static indices only
+                  const bool gt = x > tv[j] || (x == tv[j] && xi < ti[j]);
+                  const float t = tv[j];
+                  const int w = ti[j];
+                  tv[j] = gt ? x : t;
+                  ti[j] = gt ? xi : w;
+                  x = gt ? t : x;
+                  xi = gt ? w : xi;
+                }
+              }
+            }
+          }
+        }
+        if (row_ok) {
+          const size_t base = ((size_t)rslot * p.n_rows + r_local) * kTopK;
+#pragma unroll
+          for (int j = 0; j < kTopK; j += 4) {
+            *reinterpret_cast<float4*>(p.tk_val + base + j) = make_float4(tv[j], tv[j + 1], tv[j + 2], tv[j + 3]);
+            *reinterpret_cast<int4*>(p.tk_idx + base + j) = make_int4(ti[j], ti[j + 1], ti[j + 2], ti[j + 3]);
+          }
+        }
+      }
+    } else if constexpr (DEC && PASS == 1) {
       constexpr int kChunks = BN / 32;
       const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
       for (int u = worker; u < n_units; u += n_workers) {
@@ -606,7 +663,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 #ifdef KD_EPI_TIMING
           long long tw = 0, tt = 0, ts = 0, t0 = clock64();
 #endif
-          {  // teacher half
+          if (p.side_lo == 0) {  // teacher half (skipped by the student-only pass 2 of the top-k baseline)
             const uint32_t buf = it & 1, tph = (it >> 1) & 1;
             ++it;
             mbar_wait(&tfull[buf], tph);
@@ -654,13 +711,18 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               float zt[32], zs[32];
               const float4* zc = zrow + (size_t)c * 8 * kBM;
 #ifndef KD_X_NOSTAGE
+              if (p.side_lo == 0) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 v = zc[j * kBM];
-                zt[4 * j] = v.x;
-                zt[4 * j + 1] = v.y;
-                zt[4 * j + 2] = v.z;
-                zt[4 * j + 3] = v.w;
+                for (int j = 0; j < 8; ++j) {
+                  const float4 v = zc[j * kBM];
+                  zt[4 * j] = v.x;
+                  zt[4 * j + 1] = v.y;
+                  zt[4 * j + 2] = v.z;
+                  zt[4 * j + 3] = v.w;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) zt[j] = -1e30f;  // no teacher: p ≡ 0, g = gscale·q (fixed up later)
               }
               tmem_ld32_sync(t_addr + c * 32, zs);
 #else
@@ -856,6 +918,7 @@ static cudaError_t launch_pass_cg(int pass, int kind, bool coupled, const CUtens
                                   int grid, cudaStream_t stream) {
   if (pass == 1) {
     // pass 1 only distinguishes which side is "primary" (RKL swaps the roles) and coupled vs decoupled sides
+    if (kind == KIND_TOPK) return launch_pass_t<1, KIND_TOPK, CG, BN, true>(maps, p, grid, stream);
     if (kind == KIND_RKL) return launch_pass_t<1, KIND_RKL, CG, BN>(maps, p, grid, stream);
     return coupled ? launch_pass_t<1, KIND_FKL, CG, BN>(maps, p, grid, stream)
                    : launch_pass_t<1, KIND_FKL, CG, BN, true>(maps, p, grid, stream);

@@ -20,6 +20,7 @@ KINDS = {"fkl": 0, "rkl": 1, "jsd": 2, "tvd": 3}
 STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALIGNMENT", 4: "KD_ERR_UNSUPPORTED",
           5: "KD_ERR_WORKSPACE_TOO_SMALL", 6: "KD_ERR_CUDA"}
 EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_teacher_lse", "kd_fused_fwd_bwd_lse",
+            "kd_teacher_topk", "kd_topk_fwd_bwd",
             "kd_vocab_stats", "kd_vocab_backward",
             "kd_vocab_partials", "kd_vocab_finish", "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
@@ -65,6 +66,10 @@ def lib() -> ctypes.CDLL:
     L.kd_teacher_lse.restype = ctypes.c_int
     L.kd_fused_fwd_bwd_lse.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64p, vp, sz, vp]
     L.kd_fused_fwd_bwd_lse.restype = ctypes.c_int
+    L.kd_teacher_topk.argtypes = [P, vp, vp, vp, i32, vp, vp, vp, sz, vp]
+    L.kd_teacher_topk.restype = ctypes.c_int
+    L.kd_topk_fwd_bwd.argtypes = [P, vp, vp, vp, i32, vp, vp, vp, vp, vp, i64p, vp, sz, vp]
+    L.kd_topk_fwd_bwd.restype = ctypes.c_int
     L.kd_vocab_stats.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.kd_vocab_stats.restype = ctypes.c_int
     L.kd_vocab_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
@@ -251,6 +256,54 @@ def fused_fwd_bwd_lse(h_t, W_t, h_s, W_s, lse_t, mask=None, *, T=1.0, kind="fkl"
     _check(lib().kd_fused_fwd_bwd_lse(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(h_s), _ptr(W_s), _ptr(mask),
                                       _ptr(lse_t), _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf),
                                       _ptr(ws), ws.numel(), _stream_handle(stream)))
+    return KDResult(loss, dh, dW_s if want_dW else None, nnf)
+
+
+def teacher_topk(h_t, W_t, mask=None, *, k, d_s, T=1.0, chunk_tokens=0, stream=None):
+    """kd_teacher_topk: the top-k teacher baseline's transfer (idx [N, k] int32, val [N, k] float32 raw logits)."""
+    h_t, W_t = _as_bf16(h_t, "h_t"), _as_bf16(W_t, "W_t")
+    N, d_t = h_t.shape
+    V = W_t.shape[0]
+    p = make_problem(N, d_t, d_s, V, T=T, chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
+    idx = torch.full((N, k), -1, dtype=torch.int32, device=h_t.device)
+    val = torch.zeros(N, k, dtype=torch.float32, device=h_t.device)
+    ws = _workspace(workspace_size(p), h_t.device)
+    _check(lib().kd_teacher_topk(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(mask), int(k), _ptr(idx), _ptr(val),
+                                 _ptr(ws), ws.numel(), _stream_handle(stream)))
+    return idx, val
+
+
+def topk_fwd_bwd(h_s, W_s, topk_idx, topk_val, mask=None, *, d_t=64, T=1.0, loss_scale=1.0, want_dW=False,
+                 accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split", out=None,
+                 stream=None) -> KDResult:
+    """kd_topk_fwd_bwd: FKL against the renormalised top-k teacher (student head only)."""
+    h_s, W_s = _as_bf16(h_s, "h_s"), _as_bf16(W_s, "W_s")
+    N, d_s = h_s.shape
+    V = W_s.shape[0]
+    dev = h_s.device
+    k = int(topk_idx.shape[1])
+    if topk_idx.dtype != torch.int32 or topk_val.dtype != torch.float32 or tuple(topk_val.shape) != (N, k) \
+            or tuple(topk_idx.shape) != (N, k) or not topk_idx.is_cuda or not topk_val.is_cuda:
+        raise ValueError("topk_idx / topk_val must be CUDA int32 / float32 tensors of shape [N, k]")
+    topk_idx, topk_val = topk_idx.contiguous(), topk_val.contiguous()
+    p = make_problem(N, d_t, d_s, V, T=T, kind="fkl", loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, chunk_tokens=chunk_tokens, grad_precision=grad_precision)
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    if out is None:
+        loss = torch.empty(N, dtype=torch.float32, device=dev)
+        dh = torch.empty(N, d_s, dtype=torch.float32, device=dev)
+        nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        loss, dh, nnf = out.loss, out.dh_s, out.n_nonfinite
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if accumulate_dW else torch.empty)(V, d_s, dtype=torch.float32, device=dev)
+    ws = _workspace(workspace_size(p), dev)
+    _check(lib().kd_topk_fwd_bwd(ctypes.byref(p), _ptr(h_s), _ptr(W_s), _ptr(mask), k, _ptr(topk_idx),
+                                 _ptr(topk_val), _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf),
+                                 _ptr(ws), ws.numel(), _stream_handle(stream)))
     return KDResult(loss, dh, dW_s if want_dW else None, nnf)
 
 

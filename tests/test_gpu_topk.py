@@ -1,0 +1,149 @@
+"""the top-k teacher baseline (kd_teacher_topk + kd_topk_fwd_bwd) against its fp64 oracle
+(oracle/kd_topk.py), and the negative control itself: top-k transfer does NOT reproduce full-logit KD.
+
+Selection parity: the GPU ranks fp32 tensor-core logits, the oracle fp64 ones, so a near-tie at the k-th place may
+legitimately pick another index.  What is unique is checked exactly (the value of every selected logit, the sorted
+order); the set is checked for validity (every selected logit >= the (k+1)-th fp64 logit minus the fp32 GEMM error)
+and for agreement with the oracle's set on all rows without such a near-tie.  The student side is then compared
+with the oracle fed the GPU's own (idx, val) — the transfer the student receives.
+"""
+import numpy as np
+import pytest
+import torch
+
+import kd_inputs as KI
+from oracle.kd_oracle import divergence, lm_head_logits
+from oracle.kd_topk import fkl_topk_support, kd_topk_fwd_bwd, teacher_topk
+from tests.kdtest_util import (FLOOR_DRAWS, LOGIT_SIGMA, LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close,
+                               dev_bf16, f64)
+
+pytestmark = pytest.mark.gpu
+GEMM_ABS = 2e-4  # fp32-accumulated bf16 logits vs fp64 at these widths (|z| <~ 30): SURVEY Appendix A.1 ~1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def kd():
+    import paper_2603_01875_b200 as m
+    return m
+
+
+def topk_grad_floor(hs, Ws, idx, val, mask, T, seed=1234):
+    """Reading R14's conditioning floor for the top-k student: the oracle's 1-sigma dh_s / dW_s spread when the
+    student logits carry independent N(0, LOGIT_SIGMA^2) errors (the teacher's shipped values are exact inputs)."""
+    live = np.flatnonzero(mask)
+    dh_var = np.zeros((hs.shape[0], Ws.shape[1]))
+    dW_var = np.zeros_like(Ws)
+    rng = np.random.default_rng(seed)
+    for i in range(0, live.size, 64):
+        r = live[i:i + 64]
+        z = lm_head_logits(hs[r], Ws)
+        _, G = fkl_topk_support(idx[r], val[r], z, T)
+        for _ in range(FLOOR_DRAWS):
+            _, Gk = fkl_topk_support(idx[r], val[r], z + LOGIT_SIGMA * rng.standard_normal(z.shape), T)
+            D = Gk - G
+            dh_var[r] += (D @ Ws) ** 2 / FLOOR_DRAWS
+            dW_var += (D.T @ hs[r]) ** 2 / FLOOR_DRAWS
+    return np.sqrt(dh_var), np.sqrt(dW_var)
+
+
+def _check_selection(z64, idx, val, k):
+    N, V = z64.shape
+    ref_idx, ref_val = teacher_topk(z64, min(k + 1, V))
+    exact_rows = 0
+    for n in range(N):
+        assert len(set(idx[n].tolist())) == k and idx[n].min() >= 0 and idx[n].max() < V
+        np.testing.assert_allclose(val[n], z64[n, idx[n]], rtol=1e-5, atol=GEMM_ABS)   # values are the logits
+        assert np.all(np.diff(val[n]) <= 0)                                           # sorted, largest first
+        kth_next = ref_val[n, k] if k < V else -np.inf
+        assert np.all(z64[n, idx[n]] >= kth_next - 2 * GEMM_ABS)                      # a valid top-k
+        gap = ref_val[n, k - 1] - kth_next
+        if gap > 4 * GEMM_ABS:
+            assert set(idx[n].tolist()) == set(ref_idx[n, :k].tolist())
+            exact_rows += 1
+    return exact_rows
+
+
+@pytest.mark.parametrize("k", [1, 8, 32])
+def test_teacher_topk_vs_oracle(k):
+    N, d_t, V = 600, 256, 7001
+    inp = KI.make_inputs(N, d_t, 128, V, seed=40 + k)
+    mask = np.ones(N, np.uint8)
+    mask[5::9] = 0
+    idx, val = kd().teacher_topk(dev_bf16(inp.H_t), dev_bf16(inp.W_t), torch.from_numpy(mask).cuda(), k=k, d_s=128,
+                                 chunk_tokens=256)
+    torch.cuda.synchronize()
+    idx, val = idx.cpu().numpy(), val.cpu().numpy()
+    live = np.flatnonzero(mask)
+    assert np.all(idx[mask == 0] == -1)  # masked rows are not written
+    z = lm_head_logits(f64(inp.H_t[live]), f64(inp.W_t))
+    exact = _check_selection(z, idx[live], val[live], k)
+    assert exact >= 0.9 * live.size
+
+
+def test_teacher_topk_full_vocab_config2_shapes():
+    cfg = KI.CONFIGS["c2"]
+    inp = KI.make_config_inputs(cfg, n_tokens=256)
+    idx, val = kd().teacher_topk(dev_bf16(inp.H_t), dev_bf16(inp.W_t), k=16, d_s=cfg.d_s)
+    torch.cuda.synchronize()
+    rows = np.arange(0, 256, 4)
+    z = lm_head_logits(f64(inp.H_t[rows]), f64(inp.W_t))
+    _check_selection(z, idx.cpu().numpy()[rows], val.cpu().numpy()[rows], 16)
+
+
+@pytest.mark.parametrize("k,T", [(1, 1.0), (8, 2.0), (32, 1.0)])
+def test_topk_student_side_vs_oracle(k, T):
+    N, d_t, d_s, V = 500, 256, 128, 5003
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=60 + k)
+    mask = (np.random.default_rng(k).random(N) > 0.25).astype(np.uint8)
+    m = torch.from_numpy(mask).cuda()
+    ht, Wt, hs, Ws = (dev_bf16(x) for x in (inp.H_t, inp.W_t, inp.H_s, inp.W_s))
+    idx, val = kd().teacher_topk(ht, Wt, m, k=k, d_s=d_s, T=T, chunk_tokens=256)
+    r = kd().topk_fwd_bwd(hs, Ws, idx, val, m, d_t=d_t, T=T, want_dW=True, chunk_tokens=256)
+    torch.cuda.synchronize()
+    idx_np, val_np = idx.cpu().numpy().astype(np.int64), val.cpu().numpy().astype(np.float64)
+    idx_np[mask == 0] = 0  # never read (masked); any in-range placeholder for the oracle's array shape
+    loss, dh, dW = kd_topk_fwd_bwd(f64(inp.H_s), f64(inp.W_s), idx_np, val_np, mask, T=T, want_dW=True)
+    fl_dh, fl_dW = topk_grad_floor(f64(inp.H_s), f64(inp.W_s), idx_np, val_np, mask, T)
+    assert int(r.n_nonfinite.item()) == 0
+    assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh, fl_dh)
+    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW, fl_dW)
+
+
+def test_topk_is_a_negative_control():
+    """P:37 / P:130: the top-k loss differs from full-logit KD (which KDFlow's recompute reproduces), and the gap
+    shrinks as k grows — at config-2 head shapes, on the same rows, GPU against GPU and against the oracle."""
+    cfg = KI.CONFIGS["c2"]
+    inp = KI.make_config_inputs(cfg, n_tokens=256)
+    ht, Wt, hs, Ws = (dev_bf16(x) for x in (inp.H_t, inp.W_t, inp.H_s, inp.W_s))
+    full = kd().fused_fwd_bwd(ht, Wt, hs, Ws, T=1.0, kind="fkl").loss.cpu().numpy().astype(np.float64)
+    gaps = {}
+    for k in (1, 8, 32):
+        idx, val = kd().teacher_topk(ht, Wt, k=k, d_s=cfg.d_s)
+        top = kd().topk_fwd_bwd(hs, Ws, idx, val, d_t=cfg.d_t, T=1.0).loss.cpu().numpy().astype(np.float64)
+        gaps[k] = np.abs(top - full)
+    rows = np.arange(0, 256, 16)
+    ref_full = divergence("fkl", lm_head_logits(f64(inp.H_t[rows]), f64(inp.W_t)),
+                          lm_head_logits(f64(inp.H_s[rows]), f64(inp.W_s)), 1.0)
+    np.testing.assert_allclose(full[rows], ref_full, rtol=LOSS_RTOL, atol=LOSS_ATOL)
+    assert np.median(gaps[1]) > 1e-3                      # equivalence broken ...
+    assert gaps[1].mean() >= gaps[8].mean() >= gaps[32].mean()   # ... less so as k grows
+    assert gaps[32].mean() > 1e-5
+
+
+def test_topk_rejects():
+    inp = KI.make_inputs(64, 64, 64, 256, seed=3)
+    ht, Wt, hs, Ws = (dev_bf16(x) for x in (inp.H_t, inp.W_t, inp.H_s, inp.W_s))
+    with pytest.raises(kd().KDError, match="UNSUPPORTED"):
+        kd().teacher_topk(ht, Wt, k=33, d_s=64)
+    idx, val = kd().teacher_topk(ht, Wt, k=4, d_s=64)
+    bad = idx.clone()
+    bad[3, 1] = 10_000  # out of range: that row's loss is NaN and counted
+    r = kd().topk_fwd_bwd(hs, Ws, bad, val)
+    torch.cuda.synchronize()
+    assert int(r.n_nonfinite.item()) == 1 and np.isnan(r.loss[3].item())
