@@ -64,6 +64,9 @@ def parse():
                     help="SURVEY §8(f) NEXT-3 negative control: the prior-art top-k teacher transfer (k <= 32).  The "
                          "teacher's (idx, logit) top-k is produced once by kd_teacher_topk outside the timed region; "
                          "the timed step is kd_topk_fwd_bwd (student head only, FKL against the truncated teacher)")
+    ap.add_argument("--stage", action="store_true",
+                    help="staged variant (kd_problem.stage_logits, SURVEY §8(f) NEXT-2(ii)): pass 1 writes the token "
+                         "chunk's fp32 logits, an HBM-bound kernel forms G from them (no second tensor sweep)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=128)
@@ -82,7 +85,7 @@ def peaks():
 
 
 def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_precision: str = "split",
-                  teacher_lse: bool = False, topk: int = 0):
+                  teacher_lse: bool = False, topk: int = 0, stage: bool = False):
     mask_desc = {"none": "all ones", "prompt_pad": "prompt L_p~U[64,512] + padding beyond L~U[2048,4096] masked",
                  "ragged": "ragged L~U[256,8192], prompt L_p~U[32,min(512,L/2)] masked"}[cfg.mask]
     heads_b = cfg.vocab * (cfg.d_t + cfg.d_s) * 2
@@ -91,11 +94,13 @@ def workload_desc(cfg: KI.KDConfig, n_tok: int, want_dW: bool, world: int, grad_
                     f"{cfg.kind.upper()} T={cfg.temperature:g}" + (" +dW_s" if want_dW else "")
                     + (" [G: one bf16 plane]" if grad_precision == "bf16" else "")
                     + (" [teacher-shipped LSE record: pass 1 sweeps W_s only]" if teacher_lse else "")
-                    + (f" [NEGATIVE CONTROL: top-{topk} teacher transfer, student head only]" if topk else ""),
+                    + (f" [NEGATIVE CONTROL: top-{topk} teacher transfer, student head only]" if topk else "")
+                    + (" [staged: pass 1 writes the token chunk's fp32 logits, G from them, no pass-2 sweep]"
+                       if stage else ""),
         "baseline_config": cfg.notes,
         "tokens_per_gpu": n_tok, "d_t": cfg.d_t, "d_s": cfg.d_s, "vocab": cfg.vocab, "kind": cfg.kind,
         "temperature": cfg.temperature, "jsd_beta": cfg.jsd_beta if cfg.kind == "jsd" else None,
-        "want_dW": want_dW, "mask": mask_desc, "grad_precision": grad_precision,
+        "want_dW": want_dW, "mask": mask_desc, "grad_precision": grad_precision, "stage_logits": stage,
         "parallelism": f"token-sharded x{world} (no data-path collective)" if world > 1 else "1 GPU",
         "l2": f"no flush: resident inputs {heads_b / 1e9:.2f} GB heads + {n_tok * (cfg.d_t + cfg.d_s) * 2 / 1e9:.2f} GB "
               f"hidden > {L2_BYTES / 2 ** 20:.0f} MiB L2",
@@ -324,6 +329,10 @@ def main():
     del W_t, W_s
     kw = dict(T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0, want_dW=want_dW,
               accumulate_dW=False, grad_precision=args.grad_precision)
+    if args.stage:
+        if args.topk or args.teacher_lse:
+            raise SystemExit("--stage combines with neither --topk nor --teacher-lse (kdfused.h stage_logits)")
+        kw["stage_logits"] = True
     out = kd.KDResult(torch.empty(n_tok, dtype=torch.float32, device=dev),
                       torch.empty(n_tok, cfg.d_s, dtype=torch.float32, device=dev), None,
                       torch.zeros(1, dtype=torch.int64, device=dev))
@@ -402,6 +411,12 @@ def main():
         if name in algo:
             e["algorithmic_tflops"] = algo[name] * args.steps / (t / 1e3) / 1e12
             e["tensor_pipe_tflops_executed"] = e["algorithmic_tflops"] * exec_mult[name]
+        if name == "stage_grad":
+            # HBM-bound: per (token, v) 8 B of staged logits read + G written (split: 4 B, bf16: 2 B, JSD/TVD: 8 B)
+            wb = 8 if cfg.kind in ("jsd", "tvd") else (4 if args.grad_precision == "split" else 2)
+            e["algorithmic_bytes_per_launch"] = n_eff * cfg.vocab * (8 + wb) * args.steps / n
+            e["achieved_GBps"] = e["algorithmic_bytes_per_launch"] / (t / n / 1e3) / 1e9
+            e["hbm_frac"] = e["achieved_GBps"] / pk["hbm_gbs"]
         kernels[name] = e
     dom = max((k for k in kernels if k in algo), key=lambda k: kernels[k]["ms_per_step"])
     peak_sust = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
@@ -528,7 +543,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (kd_inputs recipe, seeded)",
-                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision, args.teacher_lse, args.topk),
+                "config": workload_desc(cfg, n_tok, want_dW, world, args.grad_precision, args.teacher_lse, args.topk,
+                                        args.stage),
                 "clocks": clocks, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "roofline": roofline, "cpu_baseline": cpu,
                 "useful_flop_frac": useful_frac, "kernels": kernels, "nonfinite_tokens": nonfinite,

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KDFUSED_ABI_VERSION 1
+#define KDFUSED_ABI_VERSION 2
 
 typedef enum {
   KD_FKL = 0, /* forward KL  Σ p ln(p/q) */
@@ -80,7 +80,13 @@ typedef struct {
   int32_t chunk_tokens;  /* token chunk Nc bounding the G scratch (0 = default: ~24 MiB of H_t|H_s rows, clamped to
                             [1024, 8192], so the chunk stays L2-resident; rounded up to the 256-row pair tile) */
   int32_t grad_precision;/* kd_grad_precision: how G reaches the backward GEMMs */
-  int32_t reserved[4];   /* must be zero */
+  int32_t stage_logits;  /* 0 (default): pass 2 recomputes both LM heads to form G — no logit ever reaches HBM.
+                            1: the STAGED variant, kd_fused_fwd_bwd only: pass 1 also writes
+                            its raw fp32 logit tiles of the current token chunk (2·Nc·V·4 B of workspace, one chunk at a
+                            time, never the [N × V] logits of the call) and an HBM-bound kernel forms G from them —
+                            no second tensor-core sweep.  Same outputs within the same tolerances (same arithmetic).
+                            Other entry points return KD_ERR_UNSUPPORTED when it is set. */
+  int32_t reserved[3];   /* must be zero */
 } kd_problem;
 
 /* Host-only validation of `p` (no CUDA call): the status kd_fused_fwd_bwd / kd_vocab_* would return for

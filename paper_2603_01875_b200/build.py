@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libkdfused.so")
-SOURCES = ["kd_pass.cu", "kd_gemm.cu", "kd_aux.cu", "kd_api.cu"]
+SOURCES = ["kd_pass.cu", "kd_gemm.cu", "kd_aux.cu", "kd_stage.cu", "kd_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -41,6 +41,7 @@ cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, c
                         int num_sms, const float* kj_ranks, int n_ranks, long long N, cudaStream_t s);
 cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, const int* idx,
                            float* kj, long long N, cudaStream_t s);
+cudaError_t launch_stage_grad(int kind, const StageParams& sp, int n_slots, cudaStream_t s);
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
                              const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
                              int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v = nullptr,
@@ -82,9 +83,10 @@ static kd_status fail(kd_status st, const char* fmt, ...) {
 // When enabled, every launch is bracketed by two CUDA events on the launch stream; kd_profile_read()
 // resolves them into per-kernel totals (bench.py uses this for the live roofline figure).
 enum KernelId : int { K_COMPACT, K_GATHER, K_ZERO, K_PASS1, K_MERGE, K_PASS2, K_KFIX, K_GEMM_DH, K_REDUCE_DH,
-                      K_GEMM_DW, K_GEMM, K_TOPK, K_NUM };
+                      K_GEMM_DW, K_GEMM, K_TOPK, K_STAGE_GRAD, K_NUM };
 static const char* kKernelNames[K_NUM] = {"compact", "gather", "zero_masked", "pass1", "merge", "pass2",
-                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm", "topk"};
+                                          "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm", "topk",
+                                          "stage_grad"};
 struct ProfRec { int id; cudaEvent_t a, b; };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -202,9 +204,12 @@ struct Plan {
   int bn;  // vocab tile of the fused passes (UMMA N): 256 or 128
   bool fix;  // JSD / TVD (two fp32 planes + K fix-up)
   int g_planes;  // bf16 planes of G fed to the backward GEMMs: 2 (split hi + lo) or 1 (KD_GRAD_BF16)
+  bool stage;    // staged variant (kd_problem.stage_logits): pass 1 writes the chunk's logits, k_stage_grad makes G
+  int n_gslots;  // per-row slots of the G step's partials (loss / (K, J) / residual fix): pass 2's n_split * parts,
+                 // or the staged kernel's vocab slots
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
       off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, off_zscr, off_tkv, off_tki, off_tkr_v, off_tkr_r,
-      total;
+      off_zst, total;
 };
 
 // Static round-robin of units over a persistent grid: makespan in tiles (+ per-unit refill cost).
@@ -253,8 +258,10 @@ static int choose_k_split(int m_tiles, int n_tiles, int kbs, int workers, long l
 
 static kd_status validate(const kd_problem* p, bool require_full_vocab) {
   if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 3; ++i)
     if (p->reserved[i] != 0) return fail(KD_ERR_INVALID_ARG, "reserved fields must be zero");
+  if (p->stage_logits != 0 && p->stage_logits != 1)
+    return fail(KD_ERR_INVALID_ARG, "stage_logits must be 0 or 1 (got %d)", p->stage_logits);
   if (p->grad_precision != KD_GRAD_SPLIT_BF16 && p->grad_precision != KD_GRAD_BF16)
     return fail(KD_ERR_INVALID_ARG, "unknown grad_precision %d", p->grad_precision);
   if (!(p->temperature > 0.f) || !std::isfinite(p->temperature))
@@ -273,6 +280,14 @@ static kd_status validate(const kd_problem* p, bool require_full_vocab) {
   if (require_full_vocab && (p->v_begin != 0 || p->v_end != p->vocab))
     return fail(KD_ERR_SHAPE, "kd_fused_fwd_bwd needs the full vocabulary; use kd_vocab_* for shards");
   if (p->chunk_tokens < 0) return fail(KD_ERR_SHAPE, "chunk_tokens must be >= 0");
+  return KD_OK;
+}
+
+// Entry points other than kd_fused_fwd_bwd: the staged variant is not implemented there (kdfused.h stage_logits).
+static kd_status validate_unstaged(const kd_problem* p, bool require_full_vocab) {
+  const kd_status st = validate(p, require_full_vocab);
+  if (st != KD_OK) return st;
+  if (p->stage_logits) return fail(KD_ERR_UNSUPPORTED, "stage_logits is implemented by kd_fused_fwd_bwd only");
   return KD_OK;
 }
 
@@ -307,6 +322,14 @@ static Plan make_plan(const kd_problem* p) {
   P.v_tiles = (P.V_r + P.bn - 1) / P.bn;
   P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, P.num_sms / P.cg);
   P.g_ld = ((P.V_r + 63) / 64) * 64;
+  P.stage = p->stage_logits != 0;
+  {
+    // staged G kernel: one 128-thread block per (128 rows, vocab slot); ~4 blocks per SM in one wave
+    const int row_blocks = P.Nc / 128, nch = P.g_ld / 32;
+    int s = (4 * P.num_sms + row_blocks - 1) / row_blocks;
+    P.n_gslots = P.stage ? (s < 1 ? 1 : (s > nch ? nch : s)) : P.n_split * epi_parts(2, P.kind);
+  }
+  const int slots_max = std::max(P.n_gslots, P.n_split * epi_parts(2, P.kind));
   P.k_split = choose_k_split((P.Nc + kBM * gemm_cg() - 1) / (kBM * gemm_cg()), (P.d_s + kGemmBN - 1) / kGemmBN,
                              (P.V_r + kBK - 1) / kBK, P.num_sms / gemm_cg(), P.Nc, P.d_s);
   size_t o = 0;
@@ -319,18 +342,19 @@ static Plan make_plan(const kd_problem* p) {
   P.off_part = take((size_t)5 * P.n_split * epi_parts(1, P.kind) * P.Nc * 4);
   P.off_fstats = take((size_t)5 * P.Nc * 4);
   // JSD/TVD: K and J partials; FKL: the loss partials of pass 2 (plane 0)
-  P.off_kpart = take((P.fix || P.kind == KD_FKL) ? (size_t)2 * P.n_split * epi_parts(2, P.kind) * P.Nc * 4 : 0);
+  P.off_kpart = take((P.fix || P.kind == KD_FKL) ? (size_t)2 * slots_max * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
   P.off_ghi = take((size_t)P.Nc * P.g_ld * 2);
   P.off_glo = take(P.g_planes == 2 ? (size_t)P.Nc * P.g_ld * 2 : 0);
   P.off_ga = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_gb = take(P.fix ? (size_t)P.Nc * P.g_ld * 4 : 0);
   P.off_dhp = take((size_t)P.k_split * P.Nc * P.d_s * 4);
-  P.off_corr_v = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
-  P.off_corr_r = take(P.fix ? 0 : (size_t)P.n_split * epi_parts(2, P.kind) * kCorrSlots * P.Nc * 4);
+  P.off_corr_v = take(P.fix ? 0 : (size_t)slots_max * kCorrSlots * P.Nc * 4);
+  P.off_corr_r = take(P.fix ? 0 : (size_t)slots_max * kCorrSlots * P.Nc * 4);
   P.off_zscr = take((size_t)P.num_sms * P.bn * kBM * 4);  // decoupled pass 2 staging (19 MB: L2-resident)
   P.off_tkr_v = take((size_t)P.Nc * kTopK * 4);  // top-k baseline: residual slots of the k support entries
   P.off_tkr_r = take((size_t)P.Nc * kTopK * 4);
+  P.off_zst = take(P.stage ? (size_t)2 * P.g_ld * P.Nc * 4 : 0);  // staged logits of one chunk (2.5 GB at c2)
   P.total = o;
   // kd_teacher_topk's candidate lists [n_split*parts][Nc][kTopK] (values, indices) reuse the G / dh scratch, which
   // that call does not touch (extended only if a tiny vocabulary makes the scratch smaller than the lists)
@@ -478,7 +502,7 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
     const double cscale = (double)p->loss_scale / (double)p->temperature;
     const float scale = (float)(P.kind == KD_JSD ? cscale * (1.0 - (double)p->jsd_beta) * 0.6931471805599453
                                                  : 0.5 * cscale);
-    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
+    KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_gslots, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
                           pp.g_hi, pp.g_lo, P.num_sms, kj_ranks, n_ranks, (long long)P.N, c.s));
   }
@@ -506,7 +530,7 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
                                    P.g_planes == 2 ? &mg_lo : nullptr, &mw, gp, P.num_sms, c.s));
   KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
                                           P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
-                                          P.n_split * epi_parts(2, P.kind) * kCorrSlots, c.Ws, c.s,
+                                          P.n_gslots * kCorrSlots, c.Ws, c.s,
                                           topk ? ws_at<int>(c.ws, P.off_tkr_v) : nullptr,
                                           topk ? ws_at<float>(c.ws, P.off_tkr_r) : nullptr, topk));
   if (dW) {
@@ -580,6 +604,8 @@ static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_
     return fail(KD_ERR_UNSUPPORTED, "kd_fused_fwd_bwd_lse: RKL's gradient needs its loss (a cross term of both heads) "
                                     "before pass 2, so pass 1 cannot skip the teacher head");
   if (lse_t && !aligned16(lse_t)) return fail(KD_ERR_ALIGNMENT, "lse_t must be 16-byte aligned");
+  if (lse_t && p->stage_logits)
+    return fail(KD_ERR_UNSUPPORTED, "stage_logits needs the teacher logits from pass 1; kd_fused_fwd_bwd_lse skips them");
   Ctx c{};
   c.p = p;
   c.P = make_plan(p);
@@ -602,13 +628,38 @@ static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_
     // decoupled pass 1 (independent teacher / student LSEs) for FKL/JSD/TVD; RKL needs its loss in pass 2
     const bool coupled = P.kind == KD_RKL;
     if (lse_t) pp.side_lo = 1;  // student half-tiles only
+    if (P.stage) pp.zst = ws_at<float>(c.ws, P.off_zst);
     KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, (long long)P.N, c.idx, 0, c.nonfinite,
                            coupled ? 1 : 0, c.s, lse_t));
-    if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) return st;
+    if (P.stage) {
+      // staged variant: G from the chunk's staged logits (HBM-bound) instead of pass 2's second tensor sweep
+      StageParams sp{};
+      sp.n_eff = c.n_eff;
+      sp.row0 = row0;
+      sp.n_rows = P.Nc;
+      sp.V_r = P.V_r;
+      sp.g_ld = P.g_ld;
+      sp.alpha = pp.alpha;
+      sp.gscale = pp.gscale;
+      sp.beta = pp.beta;
+      sp.zst = pp.zst;
+      sp.fstats = pp.fstats;
+      sp.g_hi = pp.g_hi;
+      sp.g_lo = pp.g_lo;
+      sp.g_a = pp.g_a;
+      sp.g_b = pp.g_b;
+      sp.kpart = pp.kpart;
+      sp.corr_v = pp.corr_v;
+      sp.corr_r = pp.corr_r;
+      KD_LAUNCH(K_STAGE_GRAD, launch_stage_grad(P.kind, sp, P.n_gslots, c.s));
+      if ((st = finish_chunk(c, row0, loss, dh_s, dW, nullptr, 0)) != KD_OK) return st;
+    } else if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) {
+      return st;
+    }
     if (P.kind == KD_FKL)
-      KD_LAUNCH(K_MERGE, launch_loss_rows(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, row0, c.n_eff, loss, c.idx,
+      KD_LAUNCH(K_MERGE, launch_loss_rows(pp.kpart, P.n_gslots, P.Nc, row0, c.n_eff, loss, c.idx,
                                           c.nonfinite, c.s));
   }
   return KD_OK;
@@ -634,7 +685,7 @@ kd_status kd_teacher_lse(const kd_problem* p, const void* h_t, const void* W_t, 
                          void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
-  kd_status st = validate(p, true);
+  kd_status st = validate_unstaged(p, true);
   if (st != KD_OK) return st;
   Ctx c{};
   c.p = p;
@@ -667,7 +718,7 @@ kd_status kd_teacher_topk(const kd_problem* p, const void* h_t, const void* W_t,
                           int32_t* topk_idx, float* topk_val, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
-  kd_status st = validate(p, true);
+  kd_status st = validate_unstaged(p, true);
   if (st != KD_OK) return st;
   if (k < 1 || k > p->vocab) return fail(KD_ERR_INVALID_ARG, "k must lie in [1, vocab] (got %d)", k);
   if (k > kTopK) return fail(KD_ERR_UNSUPPORTED, "k = %d > %d (the register lists of the top-k pass)", k, kTopK);
@@ -700,7 +751,7 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
                           int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
-  kd_status st = validate(p, true);
+  kd_status st = validate_unstaged(p, true);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL)
     return fail(KD_ERR_UNSUPPORTED, "kd_topk_fwd_bwd is forward KL only: RKL against a truncated teacher is +inf "
@@ -746,7 +797,7 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
                          const uint8_t* mask, float* rec, void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
-  kd_status st = validate(p, false);
+  kd_status st = validate_unstaged(p, false);
   if (st != KD_OK) return st;
   Ctx c{};
   c.p = p;
@@ -778,7 +829,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
                             size_t workspace_bytes, void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
-  kd_status st = validate(p, false);
+  kd_status st = validate_unstaged(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL && p->kind != KD_RKL)
     return fail(KD_ERR_UNSUPPORTED, "JSD/TVD vocab shards need the K exchange: use kd_vocab_partials + kd_vocab_finish");
@@ -816,7 +867,7 @@ static kd_status vocab_fix_setup(Ctx& c, const kd_problem* p, void* workspace, s
                                  int32_t n_ranks) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
-  kd_status st = validate(p, false);
+  kd_status st = validate_unstaged(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_JSD && p->kind != KD_TVD)
     return fail(KD_ERR_UNSUPPORTED, "kd_vocab_partials/finish are the JSD/TVD shard path; FKL/RKL use kd_vocab_backward");

@@ -63,6 +63,25 @@ struct PassParams {
   // tk_val / tk_idx [n_split*parts][n_rows][kTopK]
   float* tk_val;
   int* tk_idx;
+  // staged variant, pass 1 only: NULL = off; else the raw fp32 logits of the chunk,
+  // teacher plane Z_tᵀ [g_ld][n_rows] at zst, student plane Z_sᵀ at zst + g_ld·n_rows (columns < g_ld written)
+  float* zst;
+};
+
+// Logit-gradient kernel of the staged variant (kd_stage.cu): pass 2's outputs from the staged logits.
+struct StageParams {
+  const int* n_eff;
+  int row0, n_rows, V_r, g_ld;
+  float alpha, gscale, beta;
+  const float* zst;     // [2][g_ld][n_rows] (teacher plane, then student plane)
+  const float* fstats;  // [5][n_rows] as PassParams::fstats
+  __nv_bfloat16* g_hi;
+  __nv_bfloat16* g_lo;
+  float* g_a;
+  float* g_b;
+  float* kpart;         // FKL: loss partials [n_slots][n_rows]; JSD/TVD: (K, J) [2][n_slots][n_rows]
+  int* corr_v;          // FKL/RKL residual-fix slots [n_rows][n_slots][kCorrSlots]
+  float* corr_r;
 };
 
 // Generic bf16 GEMM with fp32 TMEM accumulation: D[M, N] = sum_{a < NUM_A} A_a[M, K] * B[N, K]^T.

@@ -43,6 +43,15 @@ __device__ __forceinline__ void kd_unroll32(F&& f) {
   kd_unroll_impl(f, std::make_integer_sequence<int, 32>{});
 }
 
+// Staged variant: one thread's 32 raw logits of a row into the transposed fp32 plane
+// [g_ld][n_rows] — for each column the warp's 32 rows are one contiguous 128 B run.  Streaming stores (evict-first):
+// the plane is read back only after the whole pass, and must not push the chunk's hidden rows out of L2.
+__device__ __forceinline__ void stage_store(float* plane, const float (&z)[32], int v0, int n_rows, int r) {
+  float* d = plane + (size_t)v0 * n_rows + r;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) __stcs(d + (size_t)i * n_rows, z[i]);
+}
+
 constexpr int kTileBytes = kBM * kBK * 2;  // 16 KB: one 128x64 bf16 tile (A or B)
 
 // CG = CTA group: 1 = one SM computes a 128-token x 128-vocab tile (UMMA M=128);
@@ -422,6 +431,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
                 }
               }
               const int v0 = vt * BN + c * 32;
+              if (p.zst && v0 < p.g_ld) stage_store(p.zst + (size_t)side * p.g_ld * p.n_rows, z, v0, p.n_rows, r_local);
               const int nvalid = min(32, p.V_r - v0);
               if (nvalid <= 0) continue;
               if (nvalid < 32) {
@@ -788,6 +798,10 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           const int v0 = vbase + c * 32;
           const int nvalid = min(32, p.V_r - v0);  // columns of this chunk inside [0, V_r)
           if (PASS == 1) {
+            if (p.zst && v0 < p.g_ld) {  // staged variant: raw logits of both heads (before the role swap / masking)
+              stage_store(p.zst, zt, v0, p.n_rows, r_local);
+              stage_store(p.zst + (size_t)p.g_ld * p.n_rows, zs, v0, p.n_rows, r_local);
+            }
             if (nvalid <= 0) continue;
             float* zp = (KIND == KIND_RKL) ? zs : zt;
             float* zq = (KIND == KIND_RKL) ? zt : zs;

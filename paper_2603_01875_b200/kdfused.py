@@ -39,7 +39,7 @@ class KDProblem(ctypes.Structure):
                 ("temperature", ctypes.c_float), ("kind", ctypes.c_int32), ("jsd_beta", ctypes.c_float),
                 ("loss_scale", ctypes.c_float), ("want_dW", ctypes.c_int32), ("accumulate_dW", ctypes.c_int32),
                 ("chunk_tokens", ctypes.c_int32), ("grad_precision", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("stage_logits", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 _lib = None
@@ -111,7 +111,8 @@ GRAD_PRECISION = {"split": 0, "bf16": 1}
 
 
 def make_problem(n_tokens, d_t, d_s, vocab, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False,
-                 accumulate_dW=False, v_begin=0, v_end=None, chunk_tokens=0, grad_precision="split") -> KDProblem:
+                 accumulate_dW=False, v_begin=0, v_end=None, chunk_tokens=0, grad_precision="split",
+                 stage_logits=False) -> KDProblem:
     p = KDProblem()
     p.n_tokens, p.d_t, p.d_s, p.vocab = int(n_tokens), int(d_t), int(d_s), int(vocab)
     p.v_begin = int(v_begin)
@@ -124,6 +125,7 @@ def make_problem(n_tokens, d_t, d_s, vocab, *, T=1.0, kind="fkl", beta=0.5, loss
     p.accumulate_dW = int(bool(accumulate_dW))
     p.chunk_tokens = int(chunk_tokens)
     p.grad_precision = GRAD_PRECISION[grad_precision] if isinstance(grad_precision, str) else int(grad_precision)
+    p.stage_logits = int(bool(stage_logits))
     return p
 
 
@@ -184,15 +186,18 @@ class KDResult:
 
 
 def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False,
-                  accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split", out=None,
-                  stream=None) -> KDResult:
-    """kd_fused_fwd_bwd: per-token loss, dL/dh_s and (optionally) dL/dW_s for device tensors."""
+                  accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split", stage_logits=False,
+                  out=None, stream=None) -> KDResult:
+    """kd_fused_fwd_bwd: per-token loss, dL/dh_s and (optionally) dL/dW_s for device tensors.
+
+    ``stage_logits=True`` selects the staged variant (pass 1 writes the chunk's fp32 logits, G from them)."""
     h_t, W_t, h_s, W_s = (_as_bf16(x, n) for x, n in ((h_t, "h_t"), (W_t, "W_t"), (h_s, "h_s"), (W_s, "W_s")))
     N, d_t = h_t.shape
     V, d_s = W_s.shape
     dev = h_t.device
     p = make_problem(N, d_t, d_s, V, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
-                     accumulate_dW=accumulate_dW, chunk_tokens=chunk_tokens, grad_precision=grad_precision)
+                     accumulate_dW=accumulate_dW, chunk_tokens=chunk_tokens, grad_precision=grad_precision,
+                     stage_logits=stage_logits)
     if mask is not None:
         mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
     if out is None:

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(kdfused.EXPORTED)
-    assert L.kd_abi_version() == 1
+    assert L.kd_abi_version() == 2
 
 
 def test_struct_layout_matches_header():
@@ -37,9 +37,10 @@ def test_struct_layout_matches_header():
 #include <stddef.h>
 #include "kdfused.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(kd_problem), offsetof(kd_problem, vocab),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(kd_problem), offsetof(kd_problem, vocab),
          offsetof(kd_problem, temperature), offsetof(kd_problem, loss_scale), offsetof(kd_problem, want_dW),
-         offsetof(kd_problem, chunk_tokens), offsetof(kd_problem, grad_precision), offsetof(kd_problem, reserved));
+         offsetof(kd_problem, chunk_tokens), offsetof(kd_problem, grad_precision), offsetof(kd_problem, stage_logits),
+         offsetof(kd_problem, reserved));
   return 0;
 }
 '''
@@ -51,7 +52,7 @@ int main(void) {
         got = [int(x) for x in subprocess.check_output([exe]).split()]
     P = kdfused.KDProblem
     want = [ctypes.sizeof(P), P.vocab.offset, P.temperature.offset, P.loss_scale.offset, P.want_dW.offset,
-            P.chunk_tokens.offset, P.grad_precision.offset, P.reserved.offset]
+            P.chunk_tokens.offset, P.grad_precision.offset, P.stage_logits.offset, P.reserved.offset]
     assert got == want
 
 
@@ -62,6 +63,21 @@ def test_workspace_size_host_only():
     assert 2.4e9 < n < 6e9
     pj = kd.make_problem(32768, 4096, 2048, 151936, kind="jsd", chunk_tokens=4096)
     assert kd.workspace_size(pj) > n + 0.99 * 4096 * 151936 * 8  # + two fp32 G planes
+
+
+def test_staged_workspace_adds_one_chunk_of_logits():
+    # stage_logits: + the chunk's two fp32 logit planes [2][g_ld][Nc] (kdfused.h stage_logits)
+    p = kd.make_problem(32768, 4096, 2048, 151936, chunk_tokens=2048)
+    ps = kd.make_problem(32768, 4096, 2048, 151936, chunk_tokens=2048, stage_logits=True)
+    extra = kd.workspace_size(ps) - kd.workspace_size(p)
+    assert 2 * 151936 * 2048 * 4 <= extra < 2 * 151936 * 2048 * 4 + (64 << 20)
+
+
+def test_stage_logits_rejected_outside_the_fused_call():
+    p = kd.make_problem(64, 256, 256, 1024, stage_logits=True)
+    assert kd.lib().kd_check_problem(ctypes.byref(p)) == 0
+    p.stage_logits = 2
+    assert kd.lib().kd_check_problem(ctypes.byref(p)) == 1  # KD_ERR_INVALID_ARG
 
 
 def test_default_chunk_keeps_hidden_rows_l2_resident():
