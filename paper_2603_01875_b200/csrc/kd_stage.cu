@@ -9,168 +9,221 @@
 // residual-fix slots and loss / (K, J) partials — so every downstream kernel (merge, loss rows, JSD/TVD fix-up,
 // dh / dW GEMMs, reduce) is shared unchanged.
 //
-// Mapping: one thread per token row, a warp = 32 consecutive rows, so every load of a staged column and every
-// store of a Gᵀ column is one contiguous run (128 B / 64 B per warp instruction).  blockIdx.y = vocab slot s:
-// the row's 32-column chunks [s·nch/S, (s+1)·nch/S) — slot s plays the role of pass 2's record slot.
+// Mapping: R consecutive token rows per thread, a warp = 32·R consecutive rows, so every load of a staged column
+// and every store of a Gᵀ column is one contiguous run.  blockIdx.y = vocab slot s: the row's column steps
+// [s·nst/S, (s+1)·nst/S) — slot s plays the role of pass 2's record slot.
 #include "kd_params.cuh"
 #include "sm100.cuh"
 
 namespace kd {
 
-template <int KIND>
+// R consecutive token rows per thread (R = 1, 2, 4), C = 32 / R vocab columns per step: every load of a staged
+// column is an R-wide vector (a warp: one 128·R-byte run) and every Gᵀ store packs the R rows' bf16 (R = 4: 8 B).
+// The arithmetic per element is independent of R.
+template <int R>
+__device__ __forceinline__ void ld_rows(const float* p, float (&v)[R]) {
+  if constexpr (R == 1) {
+    v[0] = __ldcs(p);
+  } else if constexpr (R == 2) {
+    const float2 x = __ldcs(reinterpret_cast<const float2*>(p));
+    v[0] = x.x; v[1] = x.y;
+  } else {
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+}
+template <int R>
+__device__ __forceinline__ void st_rows_f32(float* p, const float (&v)[R]) {
+  if constexpr (R == 1) *p = v[0];
+  else if constexpr (R == 2) *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  else *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+// R bf16 (packed pairs, row j in the low half of pair j/2) to consecutive addresses
+template <int R>
+__device__ __forceinline__ void st_rows_bf16(__nv_bfloat16* p, const uint32_t (&w)[(R + 1) / 2]) {
+  if constexpr (R == 1) st_global_b16(p, (uint16_t)(w[0] & 0xFFFFu));
+  else if constexpr (R == 2) *reinterpret_cast<uint32_t*>(p) = w[0];
+  else *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+}
+
+template <int KIND, int R>
 __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
-  const int r = blockIdx.x * 128 + threadIdx.x;  // chunk-local row
+  constexpr int C = 32 / R;  // vocab columns per step
+  const int r0 = (blockIdx.x * 128 + threadIdx.x) * R;  // chunk-local rows r0 .. r0 + R - 1
   const int valid = min(sp.n_rows, *sp.n_eff - sp.row0);
   const int rows_pad = valid > 0 ? min(sp.n_rows, (valid + 255) / 256 * 256) : 0;
-  if (r >= rows_pad) return;
-  const bool row_ok = r < valid;
+  if (r0 >= rows_pad) return;
   const int slot = blockIdx.y, n_slots = gridDim.y;
-  const int nch = sp.g_ld / 32;
-  const int c0 = (int)((long long)slot * nch / n_slots), c1 = (int)((long long)(slot + 1) * nch / n_slots);
+  const int nst = sp.g_ld / C;  // C-column steps of the scratch row
+  const int c0 = (int)((long long)slot * nst / n_slots), c1 = (int)((long long)(slot + 1) * nst / n_slots);
   const float alpha = sp.alpha;
-  float Mt2 = 0.f, lSt = 0.f, Ms2 = 0.f, lSs = 0.f, ell2 = 0.f, iSt = 1.f, iSs = 1.f;
-  if (row_ok) {
-    Mt2 = sp.fstats[r];
-    lSt = sp.fstats[sp.n_rows + r];
-    Ms2 = sp.fstats[2 * sp.n_rows + r];
-    lSs = sp.fstats[3 * sp.n_rows + r];
-    ell2 = sp.fstats[4 * sp.n_rows + r];
-    iSt = exp2f(-lSt);
-    iSs = exp2f(-lSs);
+  bool row_ok[R];
+  float Mt2[R], lSt[R], Ms2[R], lSs[R], iSt[R], iSs[R], dlr[R], dlt[R];
+  float2 cTS[R];
+  // row totals (Kahan-compensated over steps): FKL loss L; JSD/TVD K and J
+  float Ltot[R], cL[R], Ktot[R], cK[R], Jtot[R], cJ[R], cr0[R], cr1[R];
+  int cv0[R], cv1[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int r = r0 + j;
+    row_ok[j] = r < valid;
+    Mt2[j] = lSt[j] = Ms2[j] = lSs[j] = 0.f;
+    float ell2 = 0.f;
+    iSt[j] = iSs[j] = 1.f;
+    if (row_ok[j]) {
+      Mt2[j] = sp.fstats[r];
+      lSt[j] = sp.fstats[sp.n_rows + r];
+      Ms2[j] = sp.fstats[2 * sp.n_rows + r];
+      lSs[j] = sp.fstats[3 * sp.n_rows + r];
+      ell2 = sp.fstats[4 * sp.n_rows + r];
+      iSt[j] = exp2f(-lSt[j]);
+      iSs[j] = exp2f(-lSs[j]);
+    }
+    cTS[j] = make_float2(__fmul_rn(iSt[j], sp.gscale), __fmul_rn(iSs[j], sp.gscale));
+    dlr[j] = (lSs[j] - lSt[j]) + ell2;
+    dlt[j] = lSt[j] - lSs[j];
+    Ltot[j] = cL[j] = Ktot[j] = cK[j] = Jtot[j] = cJ[j] = cr0[j] = cr1[j] = 0.f;
+    cv0[j] = cv1[j] = 0;
   }
-  const float2 negM2 = make_float2(-Mt2, -Ms2);
-  const float2 cTS = make_float2(__fmul_rn(iSt, sp.gscale), __fmul_rn(iSs, sp.gscale));
-  const float dlr = (lSs - lSt) + ell2;
-  const float dlt = lSt - lSs;
-  float Lacc = 0.f, cL = 0.f, Kacc = 0.f, cK = 0.f, Jacc = 0.f, cJ = 0.f;
-  float cr0 = 0.f, cr1 = 0.f;
-  int cv0 = 0, cv1 = 0;
+  bool any_ok = false;
+#pragma unroll
+  for (int j = 0; j < R; ++j) any_ok |= row_ok[j];
   const size_t plane = (size_t)sp.g_ld * sp.n_rows;
   for (int c = c0; c < c1; ++c) {
-    const int v0 = c * 32;
-    const int nvalid = min(32, sp.V_r - v0);
-    const size_t col0 = (size_t)v0 * sp.n_rows + r;
-    float zt[32], zs[32];
-    if (row_ok && nvalid > 0) {
+    const int v0 = c * C;
+    const int nvalid = min(C, sp.V_r - v0);
+    const size_t col0 = (size_t)v0 * sp.n_rows + r0;
+    float zt[C][R], zs[C][R];
+    float stepL[R], stepK[R], stepJ[R];  // this step's partial sums
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        zt[i] = __ldcs(sp.zst + col0 + (size_t)i * sp.n_rows);
-        zs[i] = __ldcs(sp.zst + plane + col0 + (size_t)i * sp.n_rows);
+    for (int j = 0; j < R; ++j) stepL[j] = stepK[j] = stepJ[j] = 0.f;
+    if (any_ok && nvalid > 0) {
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        ld_rows<R>(sp.zst + col0 + (size_t)i * sp.n_rows, zt[i]);
+        ld_rows<R>(sp.zst + plane + col0 + (size_t)i * sp.n_rows, zs[i]);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) zt[i] = zs[i] = 0.f;
+      for (int i = 0; i < C; ++i)
+#pragma unroll
+        for (int j = 0; j < R; ++j) zt[i][j] = zs[i][j] = 0.f;
     }
     if (KIND == KIND_FKL || KIND == KIND_RKL) {
-      float g[32];
-      float la = 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const bool ok = row_ok && (i < nvalid);
-        const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
-        const float2 e2 = make_float2(ex2(u.x), ex2(u.y));
-        const float2 e = fmul2(e2, cTS);  // (gscale·p, gscale·q)
-        const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr);
-        g[i] = ok ? gi : 0.f;
-        if (KIND == KIND_FKL && ok) la = fmaf(e2.x, (u.x - u.y) - dlt, la);
-      }
-      if (KIND == KIND_FKL) kahan_add(Lacc, cL, la);
-      uint32_t hi[16], lo[16];
       const bool two = sp.g_lo != nullptr;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) split2(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
-      float amax = 0.f;
+      for (int i = 0; i < C; ++i) {
+        float g[R];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(g[i]));
-      if (amax > kCorrThresh) {
+        for (int j = 0; j < R; ++j) {
+          const bool ok = row_ok[j] && (i < nvalid);
+          const float2 u = ffma2(make_float2(zt[i][j], zs[i][j]), make_float2(alpha, alpha),
+                                 make_float2(-Mt2[j], -Ms2[j]));
+          const float2 e2 = make_float2(ex2(u.x), ex2(u.y));
+          const float2 e = fmul2(e2, cTS[j]);  // (gscale·p, gscale·q)
+          const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr[j]);
+          g[j] = ok ? gi : 0.f;
+          if (KIND == KIND_FKL && ok) stepL[j] = fmaf(e2.x, (u.x - u.y) - dlt[j], stepL[j]);
+        }
+        // split-bf16 planes: hi = RNE(g), lo = RNE(g − hi); rows packed pairwise
+        uint32_t hi[(R + 1) / 2], lo[(R + 1) / 2];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int j = 0; j < R; j += 2) {
+          const float b = (j + 1 < R) ? g[j + 1] : 0.f;
+          split2(g[j], b, hi[j / 2], lo[j / 2]);
+        }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float gv = g[2 * i + h];
-            if (fabsf(gv) > kCorrThresh) {
-              const float rep = h ? bf16hi_to_f32(hi[i]) + (two ? bf16hi_to_f32(lo[i]) : 0.f)
-                                  : bf16lo_to_f32(hi[i]) + (two ? bf16lo_to_f32(lo[i]) : 0.f);
-              const float rr = gv - rep;
-              if (fabsf(rr) > fabsf(cr1)) {
-                if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
-                else { cr1 = rr; cv1 = v0 + 2 * i + h; }
-              }
+        for (int j = 0; j < R; ++j) {
+          if (fabsf(g[j]) > kCorrThresh) {  // exact residuals of the largest entries (added back by k_reduce_dh)
+            const uint32_t h = hi[j / 2], l = lo[j / 2];
+            const float rep = (j & 1) ? bf16hi_to_f32(h) + (two ? bf16hi_to_f32(l) : 0.f)
+                                      : bf16lo_to_f32(h) + (two ? bf16lo_to_f32(l) : 0.f);
+            const float rr = g[j] - rep;
+            if (fabsf(rr) > fabsf(cr1[j])) {
+              if (fabsf(rr) > fabsf(cr0[j])) { cr1[j] = cr0[j]; cv1[j] = cv0[j]; cr0[j] = rr; cv0[j] = v0 + i; }
+              else { cr1[j] = rr; cv1[j] = v0 + i; }
             }
           }
         }
-      }
-      __nv_bfloat16* ph = sp.g_hi + col0;
-      __nv_bfloat16* pl = two ? sp.g_lo + col0 : nullptr;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        st_global_b16(ph, (uint16_t)(hi[i] & 0xFFFFu));
-        st_global_b16(ph + sp.n_rows, (uint16_t)(hi[i] >> 16));
-        ph += 2 * (size_t)sp.n_rows;
-        if (two) {
-          st_global_b16(pl, (uint16_t)(lo[i] & 0xFFFFu));
-          st_global_b16(pl + sp.n_rows, (uint16_t)(lo[i] >> 16));
-          pl += 2 * (size_t)sp.n_rows;
-        }
+        const size_t e = col0 + (size_t)i * sp.n_rows;
+        st_rows_bf16<R>(sp.g_hi + e, hi);
+        if (two) st_rows_bf16<R>(sp.g_lo + e, lo);
       }
     } else {  // JSD / TVD: the two fp32 planes (q·ℓ_v or q·sign, q) + partial (K, J), fixed up downstream
-      float kk = 0.f, jj = 0.f;
-      float* pa = sp.g_a + col0;
-      float* pb = sp.g_b + col0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float ut = fmaf(zt[i], alpha, -Mt2), us = fmaf(zs[i], alpha, -Ms2);
-        const float pt = __fmul_rn(ex2(ut), iSt), qs = __fmul_rn(ex2(us), iSs);
-        const float xt = ut - lSt;  // log2 p
-        const float xs = us - lSs;  // log2 q
-        const bool ok = row_ok && (i < nvalid);
-        float ga, gb;
-        if (KIND == KIND_JSD) {
-          const float m = fmaxf(fmaf(sp.beta, pt, (1.f - sp.beta) * qs), 1.17549435e-38f);
-          const float lm = lg2(m);
-          const float a = qs * (xs - lm);  // q·log2(q/m)
-          ga = ok ? a : 0.f;
-          gb = ok ? qs : 0.f;
-          kk += ga;
-          jj += ok ? pt * (xt - lm) : 0.f;
-        } else {
-          const float d = qs - pt;
-          const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-          ga = ok ? qs * sgn : 0.f;
-          gb = ok ? qs : 0.f;
-          kk += ga;
-          jj += ok ? fabsf(d) : 0.f;
+      for (int i = 0; i < C; ++i) {
+        float ga[R], gb[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const float ut = fmaf(zt[i][j], alpha, -Mt2[j]), us = fmaf(zs[i][j], alpha, -Ms2[j]);
+          const float pt = __fmul_rn(ex2(ut), iSt[j]), qs = __fmul_rn(ex2(us), iSs[j]);
+          const float xt = ut - lSt[j];  // log2 p
+          const float xs = us - lSs[j];  // log2 q
+          const bool ok = row_ok[j] && (i < nvalid);
+          if (KIND == KIND_JSD) {
+            const float m = fmaxf(fmaf(sp.beta, pt, (1.f - sp.beta) * qs), 1.17549435e-38f);
+            const float lm = lg2(m);
+            ga[j] = ok ? qs * (xs - lm) : 0.f;  // q·log2(q/m)
+            gb[j] = ok ? qs : 0.f;
+            stepK[j] += ga[j];
+            stepJ[j] += ok ? pt * (xt - lm) : 0.f;
+          } else {
+            const float d = qs - pt;
+            const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+            ga[j] = ok ? qs * sgn : 0.f;
+            gb[j] = ok ? qs : 0.f;
+            stepK[j] += ga[j];
+            stepJ[j] += ok ? fabsf(d) : 0.f;
+          }
         }
-        pa[(size_t)i * sp.n_rows] = ga;
-        pb[(size_t)i * sp.n_rows] = gb;
+        const size_t e = col0 + (size_t)i * sp.n_rows;
+        st_rows_f32<R>(sp.g_a + e, ga);
+        st_rows_f32<R>(sp.g_b + e, gb);
       }
-      kahan_add(Kacc, cK, kk);
-      kahan_add(Jacc, cJ, jj);
+    }
+    // per-step partial sums enter the row totals Kahan-compensated (one step = C columns)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (KIND == KIND_FKL) kahan_add(Ltot[j], cL[j], stepL[j]);
+      if (KIND == KIND_JSD || KIND == KIND_TVD) {
+        kahan_add(Ktot[j], cK[j], stepK[j]);
+        kahan_add(Jtot[j], cJ[j], stepJ[j]);
+      }
     }
   }
-  if (!row_ok) return;
-  const size_t idx = (size_t)slot * sp.n_rows + r;
-  if (KIND == KIND_JSD || KIND == KIND_TVD) {
-    sp.kpart[idx] = Kacc - cK;
-    sp.kpart[(size_t)n_slots * sp.n_rows + idx] = Jacc - cJ;
-  } else {
-    if (KIND == KIND_FKL) sp.kpart[idx] = __fmul_rn(Lacc - cL, iSt);  // FKL loss partial (bits)
-    const size_t q = ((size_t)r * n_slots + slot) * kCorrSlots;
-    sp.corr_v[q] = cv0;
-    sp.corr_r[q] = cr0;
-    sp.corr_v[q + 1] = cv1;
-    sp.corr_r[q + 1] = cr1;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (!row_ok[j]) continue;
+    const int r = r0 + j;
+    const size_t idx = (size_t)slot * sp.n_rows + r;
+    if (KIND == KIND_JSD || KIND == KIND_TVD) {
+      sp.kpart[idx] = Ktot[j] - cK[j];
+      sp.kpart[(size_t)n_slots * sp.n_rows + idx] = Jtot[j] - cJ[j];
+    } else {
+      if (KIND == KIND_FKL) sp.kpart[idx] = __fmul_rn(Ltot[j] - cL[j], iSt[j]);  // FKL loss partial (bits)
+      const size_t q = ((size_t)r * n_slots + slot) * kCorrSlots;
+      sp.corr_v[q] = cv0[j];
+      sp.corr_r[q] = cr0[j];
+      sp.corr_v[q + 1] = cv1[j];
+      sp.corr_r[q + 1] = cr1[j];
+    }
   }
 }
 
-// grid: (n_rows / 128) x n_slots (n_rows is a multiple of 128).
+#ifndef KD_STAGE_ROWS
+#define KD_STAGE_ROWS 4  // rows per thread of k_stage_grad (1, 2 or 4; A/B knob)
+#endif
+int stage_rows() { return KD_STAGE_ROWS; }
+
+// grid: (n_rows / (128·R)) x n_slots.
 cudaError_t launch_stage_grad(int kind, const StageParams& sp, int n_slots, cudaStream_t s) {
-  const dim3 grid(sp.n_rows / 128, n_slots);
+  constexpr int R = KD_STAGE_ROWS;
+  const dim3 grid((sp.n_rows + 128 * R - 1) / (128 * R), n_slots);
   switch (kind) {
-    case KIND_FKL: k_stage_grad<KIND_FKL><<<grid, 128, 0, s>>>(sp); break;
-    case KIND_RKL: k_stage_grad<KIND_RKL><<<grid, 128, 0, s>>>(sp); break;
-    case KIND_JSD: k_stage_grad<KIND_JSD><<<grid, 128, 0, s>>>(sp); break;
-    default: k_stage_grad<KIND_TVD><<<grid, 128, 0, s>>>(sp); break;
+    case KIND_FKL: k_stage_grad<KIND_FKL, R><<<grid, 128, 0, s>>>(sp); break;
+    case KIND_RKL: k_stage_grad<KIND_RKL, R><<<grid, 128, 0, s>>>(sp); break;
+    case KIND_JSD: k_stage_grad<KIND_JSD, R><<<grid, 128, 0, s>>>(sp); break;
+    default: k_stage_grad<KIND_TVD, R><<<grid, 128, 0, s>>>(sp); break;
   }
   return cudaGetLastError();
 }

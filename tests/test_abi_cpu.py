@@ -76,8 +76,17 @@ def test_staged_workspace_adds_one_chunk_of_logits():
 def test_stage_logits_rejected_outside_the_fused_call():
     p = kd.make_problem(64, 256, 256, 1024, stage_logits=True)
     assert kd.lib().kd_check_problem(ctypes.byref(p)) == 0
+    # every entry point but kd_fused_fwd_bwd rejects it before touching a pointer or the device
+    L = kd.lib()
+    assert L.kd_teacher_lse(ctypes.byref(p), None, None, None, None, None, 0, None) == 4  # KD_ERR_UNSUPPORTED
+    assert L.kd_teacher_topk(ctypes.byref(p), None, None, None, 8, None, None, None, 0, None) == 4
+    assert L.kd_vocab_stats(ctypes.byref(p), None, None, None, None, None, None, None, 0, None) == 4
+    fake = ctypes.c_void_p(256)  # never dereferenced: the status is decided on the host first
+    assert L.kd_fused_fwd_bwd_lse(ctypes.byref(p), None, None, None, None, None, fake, None, None, None, None, None,
+                                  0, None) == 4
+    assert "stage_logits" in L.kd_last_error().decode()
     p.stage_logits = 2
-    assert kd.lib().kd_check_problem(ctypes.byref(p)) == 1  # KD_ERR_INVALID_ARG
+    assert L.kd_check_problem(ctypes.byref(p)) == 1  # KD_ERR_INVALID_ARG
 
 
 def test_default_chunk_keeps_hidden_rows_l2_resident():

@@ -106,9 +106,11 @@ def test_staged_close_to_default_path(kind):
     torch.cuda.synchronize()
     assert_kd_close("loss", got.loss.cpu().numpy(), ref.loss.cpu().numpy(), 2e-6, 1e-7)
     # G differs by ex2.approx vs pass 2's FMA-pipe exp2 (<= 2^-22 relative) and the split-bf16 rounding that
-    # difference can flip; summed over 9000 vocab rows (dh) or 943 tokens (dW): 4x inside the oracle tolerance
-    assert_kd_close("dh_s", got.dh_s.cpu().numpy(), ref.dh_s.cpu().numpy(), 5e-4, 1e-7)
-    assert_kd_close("dW_s", got.dW_s.cpu().numpy(), ref.dW_s.cpu().numpy(), 5e-4, 1e-7)
+    # difference can flip (TVD: the sign of q − p where q ≈ p); summed over 9000 vocab rows (dh) or 943 tokens (dW),
+    # so elements far smaller than their terms get an absolute allowance of 1e-3 of the largest element
+    for name, a, b in (("dh_s", got.dh_s, ref.dh_s), ("dW_s", got.dW_s, ref.dW_s)):
+        b = b.cpu().numpy()
+        assert_kd_close(name, a.cpu().numpy(), b, 5e-4, 1e-3 * float(np.abs(b).max()))
 
 
 @pytest.mark.parametrize("name", ["c2", "c3_rkl", "c3_jsd"])
@@ -137,11 +139,3 @@ def test_staged_full_size_sampled(name):
     assert_grad_close("dh_s", r.dh_s.cpu().numpy()[rows], dh, fl)
     if mask is not None:
         assert np.all(r.loss.cpu().numpy()[mask == 0] == 0)
-
-
-def test_staged_rejected_by_other_entry_points():
-    inp = KI.make_inputs(64, 64, 64, 256, seed=3)
-    ht, Wt, hs, Ws = _dev(inp)
-    rec = kd().teacher_lse(ht, Wt, d_s=64)
-    with pytest.raises(kd().KDError, match="UNSUPPORTED"):
-        kd().fused_fwd_bwd_lse(ht, Wt, hs, Ws, rec, kind="fkl", stage_logits=True)
