@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--stage", action="store_true",
                     help="staged variant (kd_problem.stage_logits, SURVEY §8(f) NEXT-2(ii)): pass 1 writes the token "
                          "chunk's fp32 logits, an HBM-bound kernel forms G from them (no second tensor sweep)")
+    ap.add_argument("--no-variants", action="store_true", help="skip the staged-variant leg of the default run")
+    ap.add_argument("--handoff", action="store_true",
+                    help="add the hidden-state hand-off leg (SURVEY NEXT-4): teacher process -> student via CUDA IPC")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=128)
@@ -282,6 +285,74 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
             "exchange_bytes_per_step_per_rank": {"records_allgather": rec_bytes, "kj_allgather": kj_bytes,
                                                  "dh_allreduce": 4 * n_all * cfg.d_s},
             "loss_finite": bool(torch.isfinite(r.loss).all().item())}
+
+
+# ------------------------------------------------------------------------------------------- hand-off leg
+def _handoff_teacher(conn, h_bits, vocab, device):
+    """Teacher PROCESS of the hand-off leg: owns H_t (the batch's bit pattern) and, for comparison, a buffer the size
+    of the full bf16 logits it would otherwise ship; exports both (kd_handoff_export) and waits."""
+    import torch
+
+    import paper_2603_01875_b200 as kd
+    torch.cuda.set_device(device)
+    ht = torch.from_numpy(h_bits.view(np.int16)).to(f"cuda:{device}").view(torch.bfloat16)
+    logits = torch.zeros(h_bits.shape[0], vocab, dtype=torch.bfloat16, device=f"cuda:{device}")
+    torch.cuda.synchronize()
+    conn.send((kd.handoff_export(ht), tuple(ht.shape), kd.handoff_export(logits), tuple(logits.shape)))
+    conn.recv()
+
+
+def handoff_leg(args, cfg, kd, H_t_bits, Ht_local, Wt, Hs, Ws, mask, kw, out, dW, n_eff, stream, local):
+    """KDFlow's hidden-state transfer between a teacher process and this (student)
+    process through kd_handoff_* (CUDA IPC).  Measures (a) the pull of H_t into the student's buffer, (b) the pull of
+    the full bf16 logits the hidden-state design avoids shipping (the ~37x volume of P:133), (c) the KD step reading
+    the teacher's H_t in place (zero copy).  Same GPU here (gpurun gives one): the pulls are device-to-device copies
+    through the exporter's mapping; on a multi-GPU node the same handle maps a peer GPU's memory over NVLink."""
+    import multiprocessing as mp
+
+    import torch
+    ctx = mp.get_context("spawn")
+    parent, child = ctx.Pipe()
+    proc = ctx.Process(target=_handoff_teacher, args=(child, H_t_bits, cfg.vocab, local))
+    proc.start()
+    try:
+        h_ht, s_ht, h_lg, s_lg = parent.recv()
+        m_ht = kd.HandoffTensor(h_ht, s_ht, torch.bfloat16)
+        m_lg = kd.HandoffTensor(h_lg, s_lg, torch.bfloat16)
+        assert torch.equal(m_ht.tensor, Ht_local)
+        dst_ht = torch.empty_like(Ht_local)
+        dst_lg = torch.empty(s_lg, dtype=torch.bfloat16, device=Ht_local.device)
+
+        def timed(fn, reps):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        t_ht = timed(lambda: dst_ht.copy_(m_ht.tensor), 20)
+        t_lg = timed(lambda: dst_lg.copy_(m_lg.tensor), 5)
+        t_step = timed(lambda: kd.fused_fwd_bwd(m_ht.tensor, Wt, Hs, Ws, mask, dW_s=dW, out=out, **kw), args.steps)
+        b_ht, b_lg = m_ht.nbytes, m_lg.nbytes
+        del dst_lg
+        m_ht.close()
+        m_lg.close()
+    finally:
+        parent.send("done")
+        proc.join(timeout=120)
+    return {"transport": "kd_handoff_export/open (CUDA IPC); teacher and student are separate processes on the same "
+                         "B200 — pulls are D2D copies through the exporter's mapping (read + write of the bytes)",
+            "h_t_bytes_per_step": b_ht, "full_logits_bytes_per_step": b_lg, "volume_ratio": b_lg / b_ht,
+            "pull_h_t_ms": t_ht, "pull_logits_ms": t_lg, "time_ratio": t_lg / t_ht,
+            "pull_h_t_GBps": b_ht / (t_ht / 1e3) / 1e9, "pull_logits_GBps": b_lg / (t_lg / 1e3) / 1e9,
+            "zero_copy_step": {"value": n_eff / (t_step / 1e3), "unit": UNIT, "ms_per_step": t_step,
+                               "what": "kd_fused_fwd_bwd reading the teacher process's H_t in place"}}
 
 
 # ------------------------------------------------------------------------------------------- GPU arm
@@ -527,8 +598,49 @@ def main():
                "sample": f"{args.cpu_sample_tokens} tokens at full {cfg.name} shapes, fp64 numpy "
                          f"({dt:.1f} s; BLAS threads = all {cores} affinity cores)"}
 
-    # ---- the other layout, measured in the same run (north star: vocab sharding, token sharding alongside)
+    # ---- the staged variant (kd_problem.stage_logits) on the same inputs, timed the same way
     alongside = {}
+    if not (args.stage or args.topk or args.teacher_lse or args.no_variants):
+        kw_st = dict(kw, stage_logits=True)
+        for _ in range(max(3, args.warmup)):
+            kd.fused_fwd_bwd(Ht, Wt, Hs, Ws, mask, dW_s=dW, out=out, **kw_st)
+        torch.cuda.synchronize()
+        barrier()
+        kd.profile_read()
+        kd.profile_enable(True)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            kd.fused_fwd_bwd(Ht, Wt, Hs, Ws, mask, dW_s=dW, out=out, **kw_st)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        kd.profile_enable(False)
+        sprof = kd.profile_read()
+        ms_st = max_over_ranks(s0.elapsed_time(s1))
+        stot = sum(t for _, t in sprof.values()) or 1.0
+        alongside["staged_variant"] = {
+            "value": world * n_eff * args.steps / (ms_st / 1e3), "unit": UNIT, "ms_per_step": ms_st / args.steps,
+            "what": "kd_problem.stage_logits=1 (SURVEY NEXT-2(ii)): pass 1 also writes the token chunk's fp32 logits "
+                    "(2 x Nc x V x 4 B, one chunk at a time), an HBM-bound kernel forms G from them; no pass-2 sweep. "
+                    "Same outputs within the same tolerances (tests/test_gpu_stage.py); same launch config otherwise",
+            "useful_flop_frac": step_useful * args.steps / (ms_st / 1e3) / 1e12 / peak_sust,
+            "kernels": {k: {"launches": n, "ms_per_step": t / args.steps, "share": t / stot}
+                        for k, (n, t) in sorted(sprof.items(), key=lambda kv: -kv[1][1])}}
+        if "stage_grad" in sprof:
+            n_l, t_l = sprof["stage_grad"]
+            wb = 8 if cfg.kind in ("jsd", "tvd") else (4 if args.grad_precision == "split" else 2)
+            b = n_eff * cfg.vocab * (8 + wb) * args.steps / n_l  # per launch (one token chunk)
+            alongside["staged_variant"]["stage_grad_roofline"] = {
+                "bound": "hbm", "achieved": b / (t_l / n_l / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": b / (t_l / n_l / 1e3) / 1e9 / pk["hbm_gbs"],
+                "algorithmic_per_launch": f"tokens*V*(8 + {wb}) B = {b:.4g}"}
+
+    if args.handoff and world == 1:
+        alongside["handoff"] = handoff_leg(args, cfg, kd, H_t, Ht, Wt, Hs, Ws, mask, kw, out, dW, n_eff, stream, local)
+
+    # ---- the other layout, measured in the same run (north star: vocab sharding, token sharding alongside)
     if world > 1 or args.shard == "vocab":
         vleg = vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, want_dW)
         tleg = {"value": value, "unit": UNIT, "ms_per_step": ms_max / args.steps, "scaling": "weak",

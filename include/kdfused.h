@@ -200,6 +200,28 @@ kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t,
                           float* loss, float* dh_s_partial, float* dW_s, int64_t* n_nonfinite,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- hidden-state hand-off, teacher process -> student process.  KDFlow's transfer
+ * mechanism: the teacher ships only its final hidden states H_t ("transmit only the hidden states", P:131-135;
+ * 2·d_t B/token instead of 2·V B/token of logits, the ~37× of P:133 at d_t = 4096, V = 151936), and the student
+ * recomputes the logits with the teacher's LM head (kd_fused_fwd_bwd).  On one B200 node the two sides are
+ * processes on the same or on NVLink-connected GPUs; these calls move a device buffer between them as a CUDA IPC
+ * handle, so the student reads H_t in place (zero copy; over NVLink when the exporter is another GPU) or pulls
+ * it into its own buffer with one device-to-device copy.
+ *   kd_handoff_export: `handle` (KD_HANDOFF_HANDLE_BYTES bytes, caller-owned, any alignment) receives the IPC handle
+ *     of the allocation holding [dev_ptr, dev_ptr + bytes) and dev_ptr's offset inside it (allocations made by
+ *     cudaMalloc / the PyTorch caching allocator; VMM / managed memory -> KD_ERR_CUDA).  The exporting process keeps
+ *     the buffer alive (and unmodified) until every importer has closed it.
+ *   kd_handoff_open: maps the exported buffer into this process (another process than the exporter's) and
+ *     returns the device pointer of the exported byte range and its length in *bytes; the mapping is
+ *     read-write, the synchronisation of producer and consumer is the caller's (e.g. an event or a pipe).
+ *   kd_handoff_close: unmaps a pointer returned by kd_handoff_open.
+ * Errors: NULL arguments -> KD_ERR_INVALID_ARG (before any CUDA call); a handle not written by
+ * kd_handoff_export -> KD_ERR_INVALID_ARG; CUDA failures -> KD_ERR_CUDA. */
+#define KD_HANDOFF_HANDLE_BYTES 96
+kd_status kd_handoff_export(const void* dev_ptr, uint64_t bytes, void* handle);
+kd_status kd_handoff_open(const void* handle, void** dev_ptr, uint64_t* bytes);
+kd_status kd_handoff_close(void* dev_ptr);
+
 /* Building block exposed for verification: D[M, N] = A · Bᵀ with bf16 operands and fp32 tcgen05
  * accumulation.  A is [M, K] (a_mn_major = 0) or stored transposed as [K, M] (a_mn_major = 1); B is
  * [N, K] (b_mn_major = 0) or [K, N] (b_mn_major = 1).  D is [M, N] fp32 row-major.  M, N, K >= 1,

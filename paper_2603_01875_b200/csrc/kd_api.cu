@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -93,6 +94,7 @@ static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_ev_pool;
+static std::unordered_map<void*, void*> g_handoff_bases;  // kd_handoff_open: returned pointer -> mapped base
 static thread_local cudaStream_t g_cur_stream = nullptr;
 
 static cudaEvent_t prof_event() {
@@ -958,6 +960,76 @@ kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, in
   gp.out_ld = N;
   KD_LAUNCH(K_GEMM, launch_gemm(a_mn_major != 0, b_mn_major != 0, 1, EPI_STORE, gemm_cg(), &ma, nullptr, &mb, gp,
                                 device_sms(), static_cast<cudaStream_t>(stream)));
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------------------------ hand-off (NEXT-4)
+namespace {
+struct HandoffWire {  // the KD_HANDOFF_HANDLE_BYTES bytes a handle occupies
+  uint32_t magic;     // 'KDH1'
+  uint32_t version;
+  uint64_t offset;    // exported range: [base + offset, base + offset + bytes)
+  uint64_t bytes;
+  uint64_t pad;
+  cudaIpcMemHandle_t ipc;  // 64 B: the allocation holding the range
+};
+static_assert(sizeof(HandoffWire) == KD_HANDOFF_HANDLE_BYTES, "wire size");
+constexpr uint32_t kHandoffMagic = 0x3148444bu;
+}  // namespace
+
+kd_status kd_handoff_export(const void* dev_ptr, uint64_t bytes, void* handle) {
+  if (!dev_ptr || !handle) return fail(KD_ERR_INVALID_ARG, "kd_handoff_export: NULL pointer");
+  // driver entry point resolved at run time (the library keeps no link-time dependency on libcuda)
+  static PFN_cuMemGetAddressRange_v3020 get_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) ? reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn) : nullptr;
+  }();
+  if (!get_range) return fail(KD_ERR_CUDA, "kd_handoff_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(KD_ERR_CUDA, "kd_handoff_export: not a device allocation");
+  const uint64_t off = reinterpret_cast<CUdeviceptr>(dev_ptr) - base;
+  if (off + bytes > size) return fail(KD_ERR_INVALID_ARG, "kd_handoff_export: range exceeds its allocation");
+  HandoffWire w{};
+  w.magic = kHandoffMagic;
+  w.version = KDFUSED_ABI_VERSION;
+  w.offset = off;
+  w.bytes = bytes;
+  KD_CUDA(cudaIpcGetMemHandle(&w.ipc, reinterpret_cast<void*>(base)));
+  std::memcpy(handle, &w, sizeof w);
+  return KD_OK;
+}
+
+kd_status kd_handoff_open(const void* handle, void** dev_ptr, uint64_t* bytes) {
+  if (!handle || !dev_ptr || !bytes) return fail(KD_ERR_INVALID_ARG, "kd_handoff_open: NULL pointer");
+  HandoffWire w;
+  std::memcpy(&w, handle, sizeof w);
+  if (w.magic != kHandoffMagic) return fail(KD_ERR_INVALID_ARG, "kd_handoff_open: not a kd_handoff_export handle");
+  void* base = nullptr;
+  KD_CUDA(cudaIpcOpenMemHandle(&base, w.ipc, cudaIpcMemLazyEnablePeerAccess));
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_handoff_bases[static_cast<char*>(base) + w.offset] = base;
+  }
+  *dev_ptr = static_cast<char*>(base) + w.offset;
+  *bytes = w.bytes;
+  return KD_OK;
+}
+
+kd_status kd_handoff_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(KD_ERR_INVALID_ARG, "kd_handoff_close: NULL pointer");
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    auto it = g_handoff_bases.find(dev_ptr);
+    if (it == g_handoff_bases.end()) return fail(KD_ERR_INVALID_ARG, "kd_handoff_close: not from kd_handoff_open");
+    base = it->second;
+    g_handoff_bases.erase(it);
+  }
+  KD_CUDA(cudaIpcCloseMemHandle(base));
   return KD_OK;
 }
 

@@ -22,7 +22,8 @@ STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALI
 EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_teacher_lse", "kd_fused_fwd_bwd_lse",
             "kd_teacher_topk", "kd_topk_fwd_bwd",
             "kd_vocab_stats", "kd_vocab_backward",
-            "kd_vocab_partials", "kd_vocab_finish", "kd_gemm_bf16_f32",
+            "kd_vocab_partials", "kd_vocab_finish", "kd_handoff_export", "kd_handoff_open", "kd_handoff_close",
+            "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
             "kd_last_error", "kd_abi_version")
 
@@ -78,6 +79,12 @@ def lib() -> ctypes.CDLL:
     L.kd_vocab_partials.restype = ctypes.c_int
     L.kd_vocab_finish.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
     L.kd_vocab_finish.restype = ctypes.c_int
+    L.kd_handoff_export.argtypes = [vp, ctypes.c_uint64, vp]
+    L.kd_handoff_export.restype = ctypes.c_int
+    L.kd_handoff_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)]
+    L.kd_handoff_open.restype = ctypes.c_int
+    L.kd_handoff_close.argtypes = [vp]
+    L.kd_handoff_close.restype = ctypes.c_int
     L.kd_gemm_bf16_f32.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     L.kd_gemm_bf16_f32.restype = ctypes.c_int
     L.kd_last_launch_count.restype = ctypes.c_int32
@@ -417,3 +424,58 @@ def gemm_bf16_f32(A, B, *, M, N, K, a_mn_major=False, b_mn_major=False, stream=N
     _check(lib().kd_gemm_bf16_f32(_ptr(A), _ptr(B), _ptr(D), M, N, K, int(a_mn_major), int(b_mn_major),
                                   _stream_handle(stream)))
     return D
+
+
+# ------------------------------------------------------------------ hidden-state hand-off
+HANDOFF_HANDLE_BYTES = 96
+
+
+def handoff_export(t: torch.Tensor) -> bytes:
+    """kd_handoff_export: an opaque handle (bytes) through which ANOTHER process maps ``t``'s storage (CUDA IPC).
+    The caller keeps ``t`` alive and unmodified until every importer has closed it."""
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("handoff_export needs a contiguous CUDA tensor")
+    buf = ctypes.create_string_buffer(HANDOFF_HANDLE_BYTES)
+    _check(lib().kd_handoff_export(_ptr(t), t.numel() * t.element_size(), buf))
+    return buf.raw
+
+
+class _DevView:
+    """A device byte range exposed through __cuda_array_interface__ (zero-copy torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {torch.bfloat16: "<V2", torch.float32: "<f4", torch.uint8: "|u1", torch.int32: "<i4"}
+
+
+class HandoffTensor:
+    """kd_handoff_open: the exporter's buffer mapped into this process; ``.tensor`` is a zero-copy view
+    (reads go to the exporter's memory — over NVLink when it lives on another GPU).  ``close()`` unmaps it."""
+
+    def __init__(self, handle: bytes, shape, dtype, device=None):
+        ptr, nbytes = ctypes.c_void_p(), ctypes.c_uint64()
+        _check(lib().kd_handoff_open(ctypes.create_string_buffer(handle, HANDOFF_HANDLE_BYTES), ctypes.byref(ptr),
+                                     ctypes.byref(nbytes)))
+        self.ptr, self.nbytes = ptr.value, int(nbytes.value)
+        numel = 1
+        for x in shape:
+            numel *= int(x)
+        esz = torch.empty((), dtype=dtype).element_size()
+        if numel * esz != self.nbytes:
+            self.close()
+            raise ValueError(f"handle covers {self.nbytes} bytes, shape {tuple(shape)} x {esz} B does not match")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if dtype == torch.bfloat16:  # __cuda_array_interface__ has no bf16: map as int16 and reinterpret
+            t = torch.as_tensor(_DevView(self.ptr, shape, "<i2"), device=dev).view(torch.bfloat16)
+        else:
+            t = torch.as_tensor(_DevView(self.ptr, shape, _TYPESTR[dtype]), device=dev)
+        self.tensor = t
+
+    def close(self):
+        if self.ptr:
+            self.tensor = None
+            _check(lib().kd_handoff_close(ctypes.c_void_p(self.ptr)))
+            self.ptr = None

@@ -89,6 +89,23 @@ def test_stage_logits_rejected_outside_the_fused_call():
     assert L.kd_check_problem(ctypes.byref(p)) == 1  # KD_ERR_INVALID_ARG
 
 
+def test_handoff_rejects_null_and_foreign_handles_on_the_host():
+    L = kd.lib()
+    buf = ctypes.create_string_buffer(kdfused.HANDOFF_HANDLE_BYTES)
+    assert L.kd_handoff_export(None, 16, buf) == 1
+    ptr, n = ctypes.c_void_p(), ctypes.c_uint64()
+    assert L.kd_handoff_open(None, ctypes.byref(ptr), ctypes.byref(n)) == 1
+    assert L.kd_handoff_open(buf, ctypes.byref(ptr), ctypes.byref(n)) == 1  # zeros: not an exported handle
+    assert "not a kd_handoff_export handle" in L.kd_last_error().decode()
+    assert L.kd_handoff_close(None) == 1
+    assert L.kd_handoff_close(ctypes.c_void_p(4096)) == 1  # never opened
+
+
+def test_handoff_handle_size_matches_header():
+    src = open(os.path.join(ROOT, "include", "kdfused.h")).read()
+    assert f"#define KD_HANDOFF_HANDLE_BYTES {kdfused.HANDOFF_HANDLE_BYTES}" in src
+
+
 def test_default_chunk_keeps_hidden_rows_l2_resident():
     # default chunk = 24 MiB of H_t|H_s rows: 2048 tokens at d_t + d_s = 6144, 4096 at 3072 (kdfused.h chunk_tokens)
     for d_t, d_s, nc in ((4096, 2048, 2048), (2048, 1024, 4096)):
