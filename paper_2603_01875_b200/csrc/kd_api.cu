@@ -44,6 +44,7 @@ cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0
                            float* kj, long long N, cudaStream_t s);
 cudaError_t launch_stage_grad(int kind, const StageParams& sp, int n_slots, cudaStream_t s);
 int stage_rows();
+int stage_cols();
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
                              const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
                              int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v = nullptr,
@@ -327,9 +328,10 @@ static Plan make_plan(const kd_problem* p) {
   P.g_ld = ((P.V_r + 63) / 64) * 64;
   P.stage = p->stage_logits != 0;
   {
-    // staged G kernel: one 128-thread block per (128·R rows, vocab slot); ~4 blocks per SM in one wave
-    const int R = stage_rows(), row_blocks = (P.Nc + 128 * R - 1) / (128 * R), nch = P.g_ld / (32 / R);
-    int s = (4 * P.num_sms + row_blocks - 1) / row_blocks;
+    // staged G kernel: one 128-thread block per (128·R rows, vocab slot); ~8 blocks per SM in one wave
+    const int R = stage_rows(), row_blocks = (P.Nc + 128 * R - 1) / (128 * R), nch = P.g_ld / stage_cols();
+    static const int bps = env_int("KD_STAGE_BPS", 8);  // target resident blocks per SM (A/B knob)
+    int s = (bps * P.num_sms + row_blocks - 1) / row_blocks;
     P.n_gslots = P.stage ? (s < 1 ? 1 : (s > nch ? nch : s)) : P.n_split * epi_parts(2, P.kind);
   }
   const int slots_max = std::max(P.n_gslots, P.n_split * epi_parts(2, P.kind));

@@ -17,7 +17,7 @@
 
 namespace kd {
 
-// R consecutive token rows per thread (R = 1, 2, 4), C = 32 / R vocab columns per step: every load of a staged
+// R consecutive token rows per thread (R = 1, 2, 4), C vocab columns per step: every load of a staged
 // column is an R-wide vector (a warp: one 128·R-byte run) and every Gᵀ store packs the R rows' bf16 (R = 4: 8 B).
 // The arithmetic per element is independent of R.
 template <int R>
@@ -46,9 +46,16 @@ __device__ __forceinline__ void st_rows_bf16(__nv_bfloat16* p, const uint32_t (&
   else *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
 }
 
+#ifndef KD_STAGE_ROWS
+#define KD_STAGE_ROWS 4  // rows per thread of k_stage_grad (1, 2 or 4; A/B knob)
+#endif
+#ifndef KD_STAGE_COLS
+#define KD_STAGE_COLS 4  // vocab columns per step (R x C elements per thread per step; A/B knob)
+#endif
+
 template <int KIND, int R>
 __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
-  constexpr int C = 32 / R;  // vocab columns per step
+  constexpr int C = KD_STAGE_COLS;  // vocab columns per step
   const int r0 = (blockIdx.x * 128 + threadIdx.x) * R;  // chunk-local rows r0 .. r0 + R - 1
   const int valid = min(sp.n_rows, *sp.n_eff - sp.row0);
   const int rows_pad = valid > 0 ? min(sp.n_rows, (valid + 255) / 256 * 256) : 0;
@@ -85,9 +92,12 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
     Ltot[j] = cL[j] = Ktot[j] = cK[j] = Jtot[j] = cJ[j] = cr0[j] = cr1[j] = 0.f;
     cv0[j] = cv1[j] = 0;
   }
-  bool any_ok = false;
+  bool any_ok = false, all_ok = true;
 #pragma unroll
-  for (int j = 0; j < R; ++j) any_ok |= row_ok[j];
+  for (int j = 0; j < R; ++j) {
+    any_ok |= row_ok[j];
+    all_ok &= row_ok[j];
+  }
   const size_t plane = (size_t)sp.g_ld * sp.n_rows;
   for (int c = c0; c < c1; ++c) {
     const int v0 = c * C;
@@ -98,10 +108,14 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
 #pragma unroll
     for (int j = 0; j < R; ++j) stepL[j] = stepK[j] = stepJ[j] = 0.f;
     if (any_ok && nvalid > 0) {
+      const float* pzt = sp.zst + col0;
+      const float* pzs = sp.zst + plane + col0;
 #pragma unroll
       for (int i = 0; i < C; ++i) {
-        ld_rows<R>(sp.zst + col0 + (size_t)i * sp.n_rows, zt[i]);
-        ld_rows<R>(sp.zst + plane + col0 + (size_t)i * sp.n_rows, zs[i]);
+        ld_rows<R>(pzt, zt[i]);
+        ld_rows<R>(pzs, zs[i]);
+        pzt += sp.n_rows;
+        pzs += sp.n_rows;
       }
     } else {
 #pragma unroll
@@ -111,43 +125,61 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
     }
     if (KIND == KIND_FKL || KIND == KIND_RKL) {
       const bool two = sp.g_lo != nullptr;
+      // the step's gradient: every element first (no per-element control flow on the fast path)
+      float g[C][R];
+      float amax = 0.f;
+      auto elem = [&](int i, int j, bool ok) {
+        const float2 u = ffma2(make_float2(zt[i][j], zs[i][j]), make_float2(alpha, alpha),
+                               make_float2(-Mt2[j], -Ms2[j]));
+        const float2 e2 = make_float2(ex2(u.x), ex2(u.y));
+        const float2 e = fmul2(e2, cTS[j]);  // (gscale·p, gscale·q)
+        const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr[j]);
+        g[i][j] = ok ? gi : 0.f;
+        if (KIND == KIND_FKL) stepL[j] = fmaf(ok ? e2.x : 0.f, (u.x - u.y) - dlt[j], stepL[j]);
+        amax = fmaxf(amax, fabsf(g[i][j]));
+      };
+      if (all_ok && nvalid == C) {  // every chunk but the vocab tail and the chunk's last rows
 #pragma unroll
-      for (int i = 0; i < C; ++i) {
-        float g[R];
+        for (int i = 0; i < C; ++i)
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const bool ok = row_ok[j] && (i < nvalid);
-          const float2 u = ffma2(make_float2(zt[i][j], zs[i][j]), make_float2(alpha, alpha),
-                                 make_float2(-Mt2[j], -Ms2[j]));
-          const float2 e2 = make_float2(ex2(u.x), ex2(u.y));
-          const float2 e = fmul2(e2, cTS[j]);  // (gscale·p, gscale·q)
-          const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr[j]);
-          g[j] = ok ? gi : 0.f;
-          if (KIND == KIND_FKL && ok) stepL[j] = fmaf(e2.x, (u.x - u.y) - dlt[j], stepL[j]);
-        }
-        // split-bf16 planes: hi = RNE(g), lo = RNE(g − hi); rows packed pairwise
-        uint32_t hi[(R + 1) / 2], lo[(R + 1) / 2];
+          for (int j = 0; j < R; ++j) elem(i, j, true);
+      } else {
 #pragma unroll
-        for (int j = 0; j < R; j += 2) {
-          const float b = (j + 1 < R) ? g[j + 1] : 0.f;
-          split2(g[j], b, hi[j / 2], lo[j / 2]);
-        }
+        for (int i = 0; i < C; ++i)
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          if (fabsf(g[j]) > kCorrThresh) {  // exact residuals of the largest entries (added back by k_reduce_dh)
-            const uint32_t h = hi[j / 2], l = lo[j / 2];
-            const float rep = (j & 1) ? bf16hi_to_f32(h) + (two ? bf16hi_to_f32(l) : 0.f)
-                                      : bf16lo_to_f32(h) + (two ? bf16lo_to_f32(l) : 0.f);
-            const float rr = g[j] - rep;
-            if (fabsf(rr) > fabsf(cr1[j])) {
-              if (fabsf(rr) > fabsf(cr0[j])) { cr1[j] = cr0[j]; cv1[j] = cv0[j]; cr0[j] = rr; cv0[j] = v0 + i; }
-              else { cr1[j] = rr; cv1[j] = v0 + i; }
+          for (int j = 0; j < R; ++j) elem(i, j, row_ok[j] && (i < nvalid));
+      }
+      // split-bf16 planes: hi = RNE(g), lo = RNE(g − hi); rows packed pairwise
+      uint32_t hi[C][(R + 1) / 2], lo[C][(R + 1) / 2];
+#pragma unroll
+      for (int i = 0; i < C; ++i)
+#pragma unroll
+        for (int j = 0; j < R; j += 2) split2(g[i][j], (j + 1 < R) ? g[i][j + 1] : 0.f, hi[i][j / 2], lo[i][j / 2]);
+      if (amax > kCorrThresh) {  // exact residuals of the largest entries (added back by k_reduce_dh); rare
+#pragma unroll
+        for (int i = 0; i < C; ++i)
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            if (fabsf(g[i][j]) > kCorrThresh) {
+              const uint32_t h = hi[i][j / 2], l = lo[i][j / 2];
+              const float rep = (j & 1) ? bf16hi_to_f32(h) + (two ? bf16hi_to_f32(l) : 0.f)
+                                        : bf16lo_to_f32(h) + (two ? bf16lo_to_f32(l) : 0.f);
+              const float rr = g[i][j] - rep;
+              if (fabsf(rr) > fabsf(cr1[j])) {
+                if (fabsf(rr) > fabsf(cr0[j])) { cr1[j] = cr0[j]; cv1[j] = cv0[j]; cr0[j] = rr; cv0[j] = v0 + i; }
+                else { cr1[j] = rr; cv1[j] = v0 + i; }
+              }
             }
           }
-        }
-        const size_t e = col0 + (size_t)i * sp.n_rows;
-        st_rows_bf16<R>(sp.g_hi + e, hi);
-        if (two) st_rows_bf16<R>(sp.g_lo + e, lo);
+      }
+      __nv_bfloat16* ph = sp.g_hi + col0;
+      __nv_bfloat16* pl = two ? sp.g_lo + col0 : nullptr;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        st_rows_bf16<R>(ph, hi[i]);
+        if (two) st_rows_bf16<R>(pl, lo[i]);
+        ph += sp.n_rows;
+        pl += sp.n_rows;
       }
     } else {  // JSD / TVD: the two fp32 planes (q·ℓ_v or q·sign, q) + partial (K, J), fixed up downstream
 #pragma unroll
@@ -210,9 +242,7 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
   }
 }
 
-#ifndef KD_STAGE_ROWS
-#define KD_STAGE_ROWS 4  // rows per thread of k_stage_grad (1, 2 or 4; A/B knob)
-#endif
+int stage_cols() { return KD_STAGE_COLS; }
 int stage_rows() { return KD_STAGE_ROWS; }
 
 // grid: (n_rows / (128·R)) x n_slots.
