@@ -61,15 +61,19 @@ constexpr int kTileBytes = kBM * kBK * 2;  // 16 KB: one 128x64 bf16 tile (A or 
 // BN = vocab columns per tile = UMMA N.  BN = 128 double-buffers the TMEM accumulators (2 x (t + s) = 512 cols) so
 //      the epilogue overlaps the next tile's MMAs; BN = 256 fills TMEM with one (t + s) pair (no overlap) but its
 //      UMMA N=256 instructions sustain a much higher tensor-pipe rate (measured).
-template <int CG, int BN>
+#ifndef KD_P2_SMEM_STAGE
+#define KD_P2_SMEM_STAGE 0  // 1: decoupled pass 2 parks the teacher half-tile in shared memory (shallower ring; A/B)
+#endif
+template <int CG, int BN, bool SST = false>
 struct PassCfg {
   static constexpr int kABytes = kTileBytes;                 // 128 rows of H per CTA
   static constexpr int kBBytes = (BN / CG) * kBK * 2;        // BN/CG rows of W per CTA
+  static constexpr int kStageBytes = SST ? BN * kBM * 4 : 0; // SST: the teacher half-tile's fp32 logits in smem
   // operand pipeline: as deep as shared memory allows — the epilogue's global traffic (G stores, z_t staging)
   // raises the TMA latency the pipeline must cover (7 x 32 KB stages for the SM-pair 256-col tile)
-  static constexpr int kStages = (KD_PASS_SMEM_KB * 1024) / (kABytes + kBBytes);
+  static constexpr int kStages = (KD_PASS_SMEM_KB * 1024 - kStageBytes) / (kABytes + kBBytes);
   static constexpr int kNumBuf = 512 / (2 * BN);             // TMEM accumulator buffers
-  static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * (kABytes + kBBytes) + kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct UnitRange {
@@ -96,7 +100,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
                    const PassParams p) {
-  using C = PassCfg<CG, BN>;
+  constexpr bool SST = KD_P2_SMEM_STAGE && DEC && PASS == 2;
+  using C = PassCfg<CG, BN, SST>;
   constexpr int kStages = C::kStages;
   constexpr int kNB = DEC ? 2 : C::kNumBuf;  // accumulator buffers (DEC: one half-tile side per buffer)
   static_assert(!DEC || PASS == 2 || KIND == KIND_FKL || KIND == KIND_TOPK, "decoupled pass 1 uses the FKL role order");
@@ -666,7 +671,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         // while the next vocab tile's teacher MMAs proceed.
         // staging layout [column / 4][row][4]: each lane moves 16 B per access and a warp's access is one
         // contiguous 512 B run
-        float4* zrow = reinterpret_cast<float4*>(p.zscr + (size_t)blockIdx.x * (BN * kBM)) + r_in_tile;
+        float4* zrow = (SST ? reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256)  // after the barrier block
+                            : reinterpret_cast<float4*>(p.zscr + (size_t)blockIdx.x * (BN * kBM))) + r_in_tile;
         constexpr int kChunks = BN / 32;
         const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
@@ -743,7 +749,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (c == c_end - 1) release(buf);
               const int v0 = vt * BN + c * 32;
               p2chunk(zt, zs, v0, min(32, p.V_r - v0));
-              if (p.l2_hints & 2) {
+              if (!SST && (p.l2_hints & 2)) {
                 // the staged lines are dead: drop them from L2 without a write-back (the warp's 4 KB of the chunk)
                 __syncwarp();
                 l2_discard128(reinterpret_cast<const char*>(zc - lane) + (size_t)(lane >> 2) * kBM * 16 + (lane & 3) * 128);
@@ -909,7 +915,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 template <int PASS, int KIND, int CG, int BN, bool DEC = false>
 static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t stream) {
   auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC>;
-  const int smem = PassCfg<CG, BN>::kSmem;
+  const int smem = PassCfg<CG, BN, KD_P2_SMEM_STAGE && DEC && PASS == 2>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
