@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--vocab-ranks", type=int, default=0,
                     help="vocab-sharded leg on a 2-D grid: ranks per vocab group (P_voc; default all ranks). "
                          "world / P_voc token groups (BASELINE config 4: 8x1, 4x2, 2x4, 1x8)")
+    ap.add_argument("--sim-vocab-shards", type=int, default=0,
+                    help="1 GPU: time rank 0's share of a P-way vocab-sharded step (compute only, no exchange)")
     ap.add_argument("--topk", type=int, default=0,
                     help="SURVEY §8(f) NEXT-3 negative control: the prior-art top-k teacher transfer (k <= 32).  The "
                          "teacher's (idx, logit) top-k is produced once by kd_teacher_topk outside the timed region; "
@@ -215,8 +217,9 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
 
     from paper_2603_01875_b200 import sharding
 
-    pv = args.vocab_ranks if args.vocab_ranks > 0 else world
-    if world % pv:
+    sim = world == 1 and args.sim_vocab_shards > 1  # one GPU playing rank 0 of a P-way vocab group (no exchange)
+    pv = args.sim_vocab_shards if sim else (args.vocab_ranks if args.vocab_ranks > 0 else world)
+    if not sim and world % pv:
         raise SystemExit(f"--vocab-ranks {pv} must divide the world size {world}")
     group, g0 = None, (rank // pv) * pv
     if world > 1 and pv < world:
@@ -228,7 +231,10 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     bounds = sharding.vocab_shard_bounds(cfg.vocab, pv)
     v0, v1 = bounds[j]
     Wt_sh, Ws_sh = Wt[v0:v1].contiguous(), Ws[v0:v1].contiguous()
-    if pv > 1:
+    if sim:  # the group's N·P tokens: this rank's own tokens stand in for the P members' slices
+        Ht_all, Hs_all = Ht.repeat(pv, 1), Hs.repeat(pv, 1)
+        mask_all = mask.repeat(pv) if mask is not None else None
+    elif pv > 1:
         def gather(x):
             parts = [torch.empty_like(x) for _ in range(pv)]
             dist.all_gather(parts, x.contiguous(), group=group)
@@ -239,7 +245,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
         Ht_all, Hs_all, mask_all = Ht, Hs, mask
     n_all = Ht_all.shape[0]
     n_eff_own = int(mask.sum().item()) if mask is not None else Ht.shape[0]
-    n_eff_job = n_eff_own
+    n_eff_job = n_eff_own * (pv if sim else 1)
     if world > 1:
         t = torch.tensor([n_eff_own], dtype=torch.float64, device=dev)
         dist.all_reduce(t)
@@ -276,7 +282,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
         ms = float(t.item())
     rec_bytes = 20 * n_all * pv
     kj_bytes = 8 * n_all * pv if cfg.kind in ("jsd", "tvd") else 0
-    grid = f"{world // pv} token groups x {pv} vocab shards"
+    grid = f"{max(1, world // pv)} token groups x {pv} vocab shards" + (" (SIMULATED on one GPU)" if sim else "")
     return {"value": n_eff_job * args.steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / args.steps,
             "scaling": "weak", "tokens_per_step": n_all * (world // pv), "vocab_rows_per_gpu": v1 - v0,
             "grid": grid,
@@ -284,7 +290,12 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
                       f"ranks, every rank of a group sees its {n_all} tokens",
             "exchange_bytes_per_step_per_rank": {"records_allgather": rec_bytes, "kj_allgather": kj_bytes,
                                                  "dh_allreduce": 4 * n_all * cfg.d_s},
-            "loss_finite": bool(torch.isfinite(r.loss).all().item())}
+            "loss_finite": bool(torch.isfinite(r.loss).all().item()),
+            **({"simulated": f"one GPU runs rank 0's work of a {pv}-way vocab group (its {v1 - v0} head rows x the "
+                             f"group's {n_all} tokens) with identity exchanges: the compute of one rank at P={pv}, no "
+                             f"communication; outputs are that shard's partial statistics, not the full result. "
+                             f"value = the group's tokens per step / this time, i.e. the P-GPU job throughput "
+                             f"excluding the exchanges"} if sim else {})}
 
 
 # ------------------------------------------------------------------------------------------- hand-off leg
@@ -597,6 +608,15 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{args.cpu_sample_tokens} tokens at full {cfg.name} shapes, fp64 numpy "
                          f"({dt:.1f} s; BLAS threads = all {cores} affinity cores)"}
+        try:  # the oracle on a single thread as well
+            from threadpoolctl import threadpool_limits
+            n1 = max(1, args.cpu_sample_tokens // 8)
+            with threadpool_limits(limits=1):
+                v1, dt1, _ = oracle_tokens_per_s(cfg, n1, want_dW)
+            cpu["single_thread"] = {"value": v1, "unit": UNIT, "cores": 1,
+                                    "sample": f"{n1} tokens at full {cfg.name} shapes ({dt1:.1f} s)"}
+        except ImportError:
+            pass
 
     # ---- the staged variant (kd_problem.stage_logits) on the same inputs, timed the same way
     alongside = {}
@@ -641,7 +661,7 @@ def main():
         alongside["handoff"] = handoff_leg(args, cfg, kd, H_t, Ht, Wt, Hs, Ws, mask, kw, out, dW, n_eff, stream, local)
 
     # ---- the other layout, measured in the same run (north star: vocab sharding, token sharding alongside)
-    if world > 1 or args.shard == "vocab":
+    if world > 1 or args.shard == "vocab" or args.sim_vocab_shards > 1:
         vleg = vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, want_dW)
         tleg = {"value": value, "unit": UNIT, "ms_per_step": ms_max / args.steps, "scaling": "weak",
                 "tokens_per_step": n_tok * world, "layout": f"token-sharded x{world}, full heads per rank"}
