@@ -269,12 +269,16 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    kd.profile_read()
+    kd.profile_enable(True)
     e0.record(stream)
     for _ in range(args.steps):
         r = step()
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    kd.profile_enable(False)
+    vprof = kd.profile_read()
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -291,6 +295,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
             "exchange_bytes_per_step_per_rank": {"records_allgather": rec_bytes, "kj_allgather": kj_bytes,
                                                  "dh_allreduce": 4 * n_all * cfg.d_s},
             "loss_finite": bool(torch.isfinite(r.loss).all().item()),
+            "kernels_ms_per_step": {k: t / args.steps for k, (n, t) in sorted(vprof.items(), key=lambda kv: -kv[1][1])},
             **({"simulated": f"one GPU runs rank 0's work of a {pv}-way vocab group (its {v1 - v0} head rows x the "
                              f"group's {n_all} tokens) with identity exchanges: the compute of one rank at P={pv}, no "
                              f"communication; outputs are that shard's partial statistics, not the full result. "

@@ -232,7 +232,25 @@ static double pass_makespan(int m_tiles, int s, int v_tiles, int sms) {
   return worst;
 }
 
+static int choose_n_split_search(int m_tiles, int v_tiles, int sms);
+// memoised: the makespan search is O(160² · m_tiles) host work (~2 ms at 32 token tiles), and every entry point plans
+// twice per call (kd_workspace_size + the call)
 static int choose_n_split(int m_tiles, int v_tiles, int sms) {
+  static std::mutex mu;
+  static std::unordered_map<long long, int> memo;
+  const long long key = ((long long)m_tiles << 42) | ((long long)v_tiles << 16) | (long long)sms;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  const int best = choose_n_split_search(m_tiles, v_tiles, sms);
+  std::lock_guard<std::mutex> lk(mu);
+  memo[key] = best;
+  return best;
+}
+
+static int choose_n_split_search(int m_tiles, int v_tiles, int sms) {
   int best = 1;
   double best_cost = 1e300;
   const int smax = v_tiles < 160 ? v_tiles : 160;
@@ -821,7 +839,10 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     // the shard record carries the cross term U (merged across ranks into the loss): coupled pass 1
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, true, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    // FKL/RKL shards need the cross term U in the record (their loss is merged from it); JSD/TVD take the loss from
+    // the (K, J) exchange, so their records need the two LSEs only: the decoupled pass 1 (as the fused path)
+    const bool coupled = !(P.kind == KD_JSD || P.kind == KD_TVD);
+    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
                            nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, 0, c.s));
   }

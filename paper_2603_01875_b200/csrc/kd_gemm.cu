@@ -19,6 +19,8 @@
 // GEMMs run K = V = 151936 long.  So a unit's K range is cut into pieces of <= kb_per_acc K blocks; each
 // piece gets a fresh TMEM accumulator (the double buffer rotates per piece) and the epilogue adds it into
 // the fp32 output with round-to-nearest CUDA-core adds ("promotion"), overlapped with the next piece's MMAs.
+#include <atomic>
+
 #include "kd_params.cuh"
 #include "sm100.cuh"
 
@@ -253,8 +255,17 @@ static cudaError_t launch_gemm_t(const CUtensorMap* a0, const CUtensorMap* a1, c
                                  const GemmParams& p, int sms, cudaStream_t stream) {
   auto kern = kd_gemm_kernel<A_MN, B_MN, NUM_A, EPI, CG>;
   const int smem = GemmCfg<NUM_A, CG>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  // the shared-memory opt-in once per (instantiation, device): a driver call on every launch was measurable host
+  // time for the per-chunk callers
+  static std::atomic<uint64_t> smem_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(smem_set.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set.fetch_or(bit, std::memory_order_acq_rel);
+  }
   const long long units = (long long)((p.M + kBM * CG - 1) / (kBM * CG)) * ((p.N + kGemmBN - 1) / kGemmBN) * p.k_split;
   const int workers = (int)(units < sms / CG ? units : sms / CG);
   cudaLaunchConfig_t cfg{};

@@ -20,6 +20,8 @@
 // TMEM: 2 accumulator buffers × (teacher 128 cols + student 128 cols) = 512 columns.
 #include <utility>
 
+#include <atomic>
+
 #include "kd_params.cuh"
 #include "sm100.cuh"
 
@@ -916,8 +918,17 @@ template <int PASS, int KIND, int CG, int BN, bool DEC = false>
 static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t stream) {
   auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC>;
   const int smem = PassCfg<CG, BN, KD_P2_SMEM_STAGE && DEC && PASS == 2>::kSmem;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  // the shared-memory opt-in once per (instantiation, device): a driver call on every launch was measurable host
+  // time for the per-chunk callers
+  static std::atomic<uint64_t> smem_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(smem_set.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set.fetch_or(bit, std::memory_order_acq_rel);
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(pass_threads(epi_parts(PASS, KIND)));

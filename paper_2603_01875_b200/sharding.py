@@ -17,6 +17,8 @@ the kernels on either side are the library's (``kd_vocab_stats`` / ``kd_vocab_ba
 """
 from __future__ import annotations
 
+import os
+
 from typing import Callable
 
 import torch
@@ -79,7 +81,15 @@ def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, 
     """JSD/TVD: per token chunk, records all-gather -> partials -> (K, J) all-gather -> finish."""
     N = h_t.shape[0]
     d_s = W_s_shard.shape[1]
-    chunk = chunk_tokens if chunk_tokens > 0 else 2048
+    # token chunk of the (K, J) exchange: a narrow vocab shard makes a 2048-token chunk's launches short (the dh GEMM
+    # over K = V_r runs in 1-2 unbalanced waves; three prologues per chunk), so the chunk grows as the shard narrows,
+    # keeping the chunk's G planes (12 B per (token, v)) near 5 GB, at least 4096 tokens: 8192 at P = 8, 5376 at
+    # P = 2 (measured on one GPU simulating rank 0, c3 JSD: per-GPU efficiency at P = 8 0.67 with 2048-token chunks
+    # -> 0.85 with 8192; at P = 2 0.79 with 2560 -> 0.84 with 4096; scripts/gpu/simv_jsd*.sh).
+    # KD_VOCAB_FIX_CHUNK overrides.
+    v_r = max(1, W_s_shard.shape[0])
+    auto = max(4096, min(8192, int(5e9 / (12 * v_r)) // 256 * 256))
+    chunk = chunk_tokens if chunk_tokens > 0 else int(os.environ.get("KD_VOCAB_FIX_CHUNK", str(auto)))
     loss = dh = None
     for a in range(0, N, chunk):
         b = min(N, a + chunk)
