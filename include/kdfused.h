@@ -166,11 +166,14 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
  * all-reduce of per-token stats").  Rank r owns rows [v_begin, v_end) of both heads.
  * FKL/RKL: kd_vocab_stats -> exchange -> kd_vocab_backward.  JSD/TVD: see kd_vocab_partials below.
  *   1) kd_vocab_stats      -> rec [5][N] f32: this shard's per-token record (base-2 running maxima,
- *                              sums and cross term; R10), 0-filled for masked rows.
+ *                              sums, and for RKL the cross term; R10), 0-filled for masked rows.
  *   2) caller all-gathers the P records into recs [P][5][N] (any transport; 20 B/token/rank).
- *   3) kd_vocab_backward   merges the P records in rank order (deterministic), writes the loss, this
- *                              shard's PARTIAL dh_s (caller all-reduces SUM over ranks) and the local
- *                              dW_s rows.  */
+ *   3) kd_vocab_backward   merges the P records in rank order (deterministic), writes this shard's
+ *                              PARTIAL dh_s (caller all-reduces SUM over ranks), the local dW_s rows and the
+ *                              loss: RKL the full ℓ_n (merged from the records' cross terms); FKL this shard's
+ *                              PARTIAL Σ_{v in shard} p_v ln(p_v/q_v) with the global LSEs (caller all-reduces
+ *                              SUM, with dh_s) — so FKL records need no cross term and pass 1 sweeps the two
+ *                              heads decoupled.  */
 kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
                          const void* W_s, const uint8_t* mask, float* rec, void* workspace,
                          size_t workspace_bytes, void* stream);

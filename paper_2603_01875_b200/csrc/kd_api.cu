@@ -839,9 +839,10 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     // the shard record carries the cross term U (merged across ranks into the loss): coupled pass 1
-    // FKL/RKL shards need the cross term U in the record (their loss is merged from it); JSD/TVD take the loss from
-    // the (K, J) exchange, so their records need the two LSEs only: the decoupled pass 1 (as the fused path)
-    const bool coupled = !(P.kind == KD_JSD || P.kind == KD_TVD);
+    // RKL shards need the cross term U in the record: the RKL value enters the gradient, so it must be merged
+    // before pass 2.  FKL (loss partials from pass 2, summed by the caller), JSD/TVD (loss from the (K, J) exchange)
+    // need the two LSEs only: the decoupled pass 1, as the fused path
+    const bool coupled = P.kind == KD_RKL;
     KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
                            nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, 0, c.s));
@@ -881,8 +882,12 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
     const int row0 = ch * P.Nc;
     // rank records [n_ranks][5][N] indexed by ORIGINAL row, merged in rank order
     KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
-                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite, 1, c.s));
+                           ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite,
+                           P.kind == KD_RKL ? 1 : 0, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_s_partial, dW)) != KD_OK) return st;
+    if (P.kind == KD_FKL)  // this shard's partial FKL: Σ over its vocab rows of p (ln p − ln q), global LSEs
+      KD_LAUNCH(K_MERGE, launch_loss_rows(pass_params(c, row0).kpart, P.n_gslots, P.Nc, row0, c.n_eff, loss, c.idx,
+                                          c.nonfinite, c.s));
   }
   return KD_OK;
 }

@@ -7,7 +7,8 @@ alongside"):
   all (the path is data-parallel); only dW_s (if requested) is a sum over ranks.
 * vocabulary sharding — rank r owns LM-head rows [v0, v1) (128-row granules; V = 151936 = 128·1187) and
   every token.  Exchanges: (1) all-gather of the per-token pass-1 records (20 B/token/rank), merged in rank
-  order by the kernels (deterministic); (2) all-reduce SUM of the partial dL/dh_s.  dW_s rows stay local.
+  order by the kernels (deterministic); (2) all-reduce SUM of the partial dL/dh_s (FKL: and of the partial
+  per-token loss, 4 B/token).  dW_s rows stay local.
   JSD/TVD add (1b): all-gather of the per-token (K, J) partials (8 B/token/rank) between the shards'
   pass 2 and the gradient fix-up, token chunk by token chunk.
 
@@ -149,6 +150,8 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
                     loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
                     chunk_tokens=chunk_tokens)
     _all_reduce_sum(r.dh_s, group)
+    if kind == "fkl":  # FKL: each shard returns its partial loss (kdfused.h kd_vocab_backward)
+        _all_reduce_sum(r.loss, group)
     return r
 
 

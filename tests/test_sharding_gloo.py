@@ -34,6 +34,8 @@ def _stats_standin(h_t, Wt, h_s, Ws, mask, *, vocab, v_begin, T, kind, chunk_tok
     b = hs @ Ws.double().numpy().T / T
     rec = block_record(b, a) if kind == "rkl" else block_record(a, b)
     out = torch.tensor(np.stack(rec))
+    if kind == "fkl":  # FKL records carry no cross term (the kernels' decoupled pass 1)
+        out[4] = 0.0
     if mask is not None:
         out[:, mask == 0] = 0.0
     return out
@@ -64,6 +66,8 @@ def _backward_standin(h_t, Wt, h_s, Ws, recs, mask, *, vocab, v_begin, T, kind, 
     p, q = np.exp(lp), np.exp(lq)
     G = loss_scale / T * ((q - p) if kind == "fkl" else q * (lq - lp - ell[:, None]))
     G = np.where(live[:, None], G, 0.0)
+    if kind == "fkl":  # this shard's partial loss, global LSEs; the caller sums over shards
+        ell = (p * (lp - lq)).sum(1)
     ell = np.where(live, ell, 0.0)
     dh = torch.tensor(G @ Ws.double().numpy())
     dW = torch.tensor(G.T @ h_s.double().numpy()) if want_dW else None
