@@ -139,3 +139,43 @@ def test_staged_full_size_sampled(name):
     assert_grad_close("dh_s", r.dh_s.cpu().numpy()[rows], dh, fl)
     if mask is not None:
         assert np.all(r.loss.cpu().numpy()[mask == 0] == 0)
+
+
+@pytest.mark.parametrize("N,V,d_t,d_s", [(1, 1, 64, 64), (129, 64, 64, 128), (257, 129, 192, 64),
+                                         (1000, 4097, 128, 320)])
+@pytest.mark.parametrize("kind", ["fkl", "jsd"])
+def test_staged_edge_shapes(N, V, d_t, d_s, kind):
+    """Single token, single vocab row, tails on every tile / column-step edge, d_s not a multiple of 256."""
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=N + V)
+    r = kd().fused_fwd_bwd(*_dev(inp), T=1.3, kind=kind, want_dW=True, chunk_tokens=256, stage_logits=True)
+    torch.cuda.synchronize()
+    loss, dh, dW = oracle_run(inp, T=1.3, kind=kind, want_dW=True)
+    assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh)
+    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW)
+
+
+@pytest.mark.parametrize("kind", ["fkl", "rkl", "tvd"])
+def test_staged_self_distillation_bitwise_zero(kind):
+    """Student := teacher: the staged planes hold identical bits for both heads, so loss and G are exactly 0."""
+    twin = KI.self_distillation_twin(KI.make_config_inputs(KI.CONFIGS["tiny"]))
+    r = kd().fused_fwd_bwd(*_dev(twin), T=1.0, kind=kind, want_dW=True, stage_logits=True)
+    torch.cuda.synchronize()
+    assert np.all(r.loss.cpu().numpy() == 0)
+    assert np.all(r.dh_s.cpu().numpy() == 0)
+    assert np.all(r.dW_s.cpu().numpy() == 0)
+
+
+def test_staged_all_masked_and_empty():
+    """Every row masked: outputs exactly 0 and no row is read (NaN garbage in H); N = 0: a no-op."""
+    inp = KI.make_inputs(300, 128, 64, 1000, seed=5)
+    ht, Wt, hs, Ws = _dev(inp)
+    ht[:] = float("nan")
+    m = torch.zeros(300, dtype=torch.uint8, device="cuda")
+    r = kd().fused_fwd_bwd(ht, Wt, hs, Ws, m, kind="rkl", want_dW=True, stage_logits=True)
+    torch.cuda.synchronize()
+    assert torch.all(r.loss == 0) and torch.all(r.dh_s == 0) and torch.all(r.dW_s == 0)
+    assert int(r.n_nonfinite.item()) == 0
+    e = kd().fused_fwd_bwd(ht[:0], Wt, hs[:0], Ws, kind="fkl", stage_logits=True)
+    torch.cuda.synchronize()
+    assert e.loss.numel() == 0 and e.dh_s.shape == (0, 64)
