@@ -613,6 +613,16 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{args.cpu_sample_tokens} tokens at full {cfg.name} shapes, fp64 numpy "
                          f"({dt:.1f} s; BLAS threads = all {cores} affinity cores)"}
+        # configs[0] (the tiny check) timed whole, all cores
+        tiny = KI.CONFIGS["tiny"]
+        from oracle.kd_oracle import kd_fused_fwd_bwd as _oracle
+        ti = KI.make_config_inputs(tiny)
+        t0 = time.perf_counter()
+        _oracle(KI.bf16_to_f64(ti.H_t), KI.bf16_to_f64(ti.W_t), KI.bf16_to_f64(ti.H_s), KI.bf16_to_f64(ti.W_s),
+                T=tiny.temperature, kind=tiny.kind, want_dW=True)
+        dt_t = time.perf_counter() - t0
+        cpu["tiny_config_whole"] = {"value": tiny.n_tokens / dt_t, "unit": UNIT, "seconds": dt_t,
+                                    "sample": f"configs[0] whole: {tiny.n_tokens} tokens, d={tiny.d_t}, V={tiny.vocab}, +dW"}
         try:  # the oracle on a single thread as well
             from threadpoolctl import threadpool_limits
             n1 = max(1, args.cpu_sample_tokens // 8)
