@@ -11,7 +11,7 @@ Qwen3-8B d_t=4096 -> Qwen3-1.7B d_s=2048, 8 x 4096 tokens, FKL, T = 1).
 Multi-GPU (torchrun): the headline value is token sharding with no data-path collective — every rank owns its
 own 32768 tokens and a full copy of both heads (weak scaling); the only collectives are the timing barrier / max.
 The north star's vocabulary sharding (LM-head rows split over the ranks, every rank sees all N·P tokens, NCCL
-all-gather of the per-token records + all-reduce of dh) is measured in the same run and reported alongside under
+all-gather of the per-token records + reduce-scatter of dh) is measured in the same run and reported alongside under
 "vocab_sharded" (``--shard vocab`` swaps the two).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -210,7 +210,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     LM-head rows [v0, v1) of both heads (128-row granules) and sees every token of the group (the members' token
     slices are all-gathered once, outside the timed region), so per-GPU work stays that of one GPU (weak scaling).
     One step = ``sharding.vocab_sharded_fwd_bwd`` on the group: kd_vocab_stats -> NCCL all-gather of the 20 B/token
-    records -> kd_vocab_backward (rank-order merge, pass 2, partial dh, local dW rows) -> NCCL all-reduce of dh
+    records -> kd_vocab_backward (rank-order merge, pass 2, partial dh, local dW rows) -> NCCL reduce-scatter of dh
     (JSD/TVD add the (K, J) all-gather per token chunk)."""
     import torch
     import torch.distributed as dist
@@ -251,8 +251,10 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
         dist.all_reduce(t)
         n_eff_job = int(t.item())
     dW = torch.empty(v1 - v0, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
+    # each rank keeps dh_s / loss of its own tokens only (the student's backward continues on them): the dh
+    # exchange is a reduce-scatter, half the bytes of an all-reduce
     kw = dict(vocab=cfg.vocab, v_begin=v0, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0,
-              want_dW=want_dW, accumulate_dW=False, group=group)
+              want_dW=want_dW, accumulate_dW=False, group=group, dh_reduce="scatter")
 
     def step():
         return sharding.vocab_sharded_fwd_bwd(Ht_all, Wt_sh, Hs_all, Ws_sh, mask_all, dW_s=dW, **kw)
@@ -293,7 +295,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
             "layout": f"vocab-sharded ({grid}): LM-head rows split in 128-row granules over each group of {pv} "
                       f"ranks, every rank of a group sees its {n_all} tokens",
             "exchange_bytes_per_step_per_rank": {"records_allgather": rec_bytes, "kj_allgather": kj_bytes,
-                                                 "dh_allreduce": 4 * n_all * cfg.d_s},
+                                                 "dh_reduce_scatter": 4 * n_all * cfg.d_s * (pv - 1) // pv},
             "loss_finite": bool(torch.isfinite(r.loss).all().item()),
             "kernels_ms_per_step": {k: t / args.steps for k, (n, t) in sorted(vprof.items(), key=lambda kv: -kv[1][1])},
             **({"simulated": f"one GPU runs rank 0's work of a {pv}-way vocab group (its {v1 - v0} head rows x the "

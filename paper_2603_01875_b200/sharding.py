@@ -72,13 +72,38 @@ def _all_reduce_sum(t: torch.Tensor, group=None):
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
 
+def _reduce_scatter_rows(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum over the group of [N, ...] and keep this rank's row slice (rows j·N/P .. (j+1)·N/P, rank order): the
+    gradient / loss of the rank's own tokens when the group's tokens are its members' slices concatenated."""
+    if not _distributed():
+        return t
+    world = dist.get_world_size(group)
+    if t.shape[0] % world:
+        raise ValueError(f"dh_reduce='scatter' needs the group's {t.shape[0]} tokens divisible by {world} ranks")
+    if t.is_cuda and dist.get_backend(group) == "gloo":  # gloo has no CUDA reduce-scatter (one-GPU rank tests)
+        t = t.contiguous()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return _own_rows(t, group)
+    out = torch.empty((t.shape[0] // world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.reduce_scatter_tensor(out, t.contiguous(), op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def _own_rows(t: torch.Tensor, group=None) -> torch.Tensor:
+    if not _distributed():
+        return t
+    world, j = dist.get_world_size(group), dist.get_rank(group)
+    n = t.shape[0] // world
+    return t[j * n:(j + 1) * n]
+
+
 class _Result:
     def __init__(self, loss, dh_s, dW_s):
         self.loss, self.dh_s, self.dW_s = loss, dh_s, dW_s
 
 
 def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, group, T, kind, beta, loss_scale,
-                       want_dW, accumulate_dW, dW_s, chunk_tokens, stats_fn, partials_fn, finish_fn):
+                       want_dW, accumulate_dW, dW_s, chunk_tokens, stats_fn, partials_fn, finish_fn, dh_reduce):
     """JSD/TVD: per token chunk, records all-gather -> partials -> (K, J) all-gather -> finish."""
     N = h_t.shape[0]
     d_s = W_s_shard.shape[1]
@@ -115,6 +140,8 @@ def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, 
     if dh is None:  # no tokens
         loss = torch.zeros(0, dtype=torch.float32, device=h_t.device)
         dh = torch.zeros(0, d_s, dtype=torch.float32, device=h_t.device)
+    if dh_reduce == "scatter":
+        return _Result(_own_rows(loss, group), _reduce_scatter_rows(dh, group), dW_s if want_dW else None)
     _all_reduce_sum(dh, group)
     return _Result(loss, dh, dW_s if want_dW else None)
 
@@ -123,8 +150,12 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
                           T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False,
                           dW_s=None, chunk_tokens=0, stats_fn: Callable | None = None,
                           backward_fn: Callable | None = None, partials_fn: Callable | None = None,
-                          finish_fn: Callable | None = None):
+                          finish_fn: Callable | None = None, dh_reduce: str = "all"):
     """One vocab-sharded step on this rank; returns a KDResult whose dh_s is the full (all-reduced) gradient.
+
+    dh_reduce="scatter": when the group's tokens are its members' equal slices concatenated in rank order (each rank
+    contributes its own batch), every rank only needs dh_s / loss for its own slice: the dh exchange becomes a
+    reduce-scatter (half the bytes of the all-reduce) and the result rows are this rank's slice.
 
     The kernel-side callables default to the CUDA entry points; tests substitute CPU stand-ins to
     exercise this exchange logic under gloo.
@@ -138,7 +169,8 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
         return _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, vocab=vocab, v_begin=v_begin, group=group,
                                   T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
                                   accumulate_dW=accumulate_dW, dW_s=dW_s, chunk_tokens=chunk_tokens,
-                                  stats_fn=stats_fn, partials_fn=partials_fn, finish_fn=finish_fn)
+                                  stats_fn=stats_fn, partials_fn=partials_fn, finish_fn=finish_fn,
+                                  dh_reduce=dh_reduce)
     if stats_fn is None or backward_fn is None:
         from . import kdfused
         stats_fn = stats_fn or kdfused.vocab_stats
@@ -149,6 +181,12 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
     r = backward_fn(h_t, W_t_shard, h_s, W_s_shard, recs, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
                     loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
                     chunk_tokens=chunk_tokens)
+    if dh_reduce not in ("all", "scatter"):
+        raise ValueError(f"dh_reduce must be 'all' or 'scatter' (got {dh_reduce!r})")
+    if dh_reduce == "scatter":
+        # FKL: each shard returns its partial loss (kdfused.h kd_vocab_backward), reduced like dh; RKL: already full
+        loss = _reduce_scatter_rows(r.loss, group) if kind == "fkl" else _own_rows(r.loss, group)
+        return _Result(loss, _reduce_scatter_rows(r.dh_s, group), r.dW_s)
     _all_reduce_sum(r.dh_s, group)
     if kind == "fkl":  # FKL: each shard returns its partial loss (kdfused.h kd_vocab_backward)
         _all_reduce_sum(r.loss, group)

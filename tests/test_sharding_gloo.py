@@ -161,7 +161,13 @@ def _worker(rank, world, port, kind, q):
         _, _, dW_part = kd_fused_fwd_bwd(ht.numpy()[sl], Wt.numpy(), hs.numpy()[sl], Ws.numpy(), mask[sl],
                                          T=1.3, kind=kind, beta=0.3, want_dW=True)
         dW_tok = token_sharded_dW_reduce(torch.tensor(dW_part))
-        q.put((rank, r.loss.numpy(), r.dh_s.numpy(), (a, b, r.dW_s.numpy()), dW_tok.numpy()))
+        # dh_reduce="scatter": the reduce-scatter of the same exchange, this rank's token slice only
+        rs = vocab_sharded_fwd_bwd(ht, Wt[a:b], hs, Ws[a:b], torch.tensor(mask), vocab=V, v_begin=a, T=1.3,
+                                   kind=kind, beta=0.3, chunk_tokens=16, stats_fn=_stats_standin,
+                                   backward_fn=_backward_standin, partials_fn=_partials_standin,
+                                   finish_fn=_finish_standin, dh_reduce="scatter")
+        q.put((rank, r.loss.numpy(), r.dh_s.numpy(), (a, b, r.dW_s.numpy()), dW_tok.numpy(),
+               (rs.loss.numpy(), rs.dh_s.numpy())))
     finally:
         dist.destroy_process_group()
 
@@ -188,7 +194,10 @@ def test_vocab_and_token_sharding_world2(kind):
     loss, dh, dW = kd_fused_fwd_bwd(f(inp.H_t), f(inp.W_t), f(inp.H_s), f(inp.W_s), mask, T=1.3, kind=kind,
                                     beta=0.3, want_dW=True)
     dW_cat = np.zeros_like(dW)
-    for rank, l, d, (a, b, dws), dW_tok in res:
+    for rank, l, d, (a, b, dws), dW_tok, (ls, ds) in res:
+        own = slice(rank * N // world, (rank + 1) * N // world)
+        np.testing.assert_allclose(ls, loss[own], rtol=1e-12, atol=1e-13)  # reduce-scatter: own tokens only
+        np.testing.assert_allclose(ds, dh[own], rtol=1e-11, atol=1e-13)
         np.testing.assert_allclose(l, loss, rtol=1e-12, atol=1e-13)
         np.testing.assert_allclose(d, dh, rtol=1e-11, atol=1e-13)   # all-reduced dh on every rank
         np.testing.assert_allclose(dW_tok, dW, rtol=1e-11, atol=1e-13)
