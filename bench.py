@@ -70,6 +70,7 @@ def parse():
                     help="staged variant (kd_problem.stage_logits, SURVEY §8(f) NEXT-2(ii)): pass 1 writes the token "
                          "chunk's fp32 logits, an HBM-bound kernel forms G from them (no second tensor sweep)")
     ap.add_argument("--no-variants", action="store_true", help="skip the staged-variant leg of the default run")
+    ap.add_argument("--graph", action="store_true", help="also time the step captured into a CUDA graph")
     ap.add_argument("--handoff", action="store_true",
                     help="add the hidden-state hand-off leg (SURVEY NEXT-4): teacher process -> student via CUDA IPC")
     ap.add_argument("--no-e2e", action="store_true")
@@ -635,8 +636,36 @@ def main():
         except ImportError:
             pass
 
-    # ---- the staged variant (kd_problem.stage_logits, SURVEY §8(f) NEXT-2(ii)) on the same inputs, timed the same way
     alongside = {}
+    if args.graph:
+        # the same step captured once into a CUDA graph and replayed (no per-launch host work; the library's calls
+        # are capturable: no host syncs, no allocation, every launch on the caller's stream)
+        cs_ = torch.cuda.Stream(device=dev)
+        cs_.wait_stream(stream)
+        with torch.cuda.stream(cs_):
+            step()
+        stream.wait_stream(cs_)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(max(3, args.warmup)):
+            graph.replay()
+        torch.cuda.synchronize()
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        ms_g = max_over_ranks(g0.elapsed_time(g1))
+        alongside["cuda_graph"] = {"value": world * n_eff * args.steps / (ms_g / 1e3), "unit": UNIT,
+                                   "ms_per_step": ms_g / args.steps,
+                                   "what": "one step captured into a CUDA graph, replayed K times (same inputs)"}
+
+    # ---- the staged variant (kd_problem.stage_logits, SURVEY §8(f) NEXT-2(ii)) on the same inputs, timed the same way
     if not (args.stage or args.topk or args.teacher_lse or args.no_variants):
         kw_st = dict(kw, stage_logits=True)
         for _ in range(max(3, args.warmup)):
