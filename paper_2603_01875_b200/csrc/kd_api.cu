@@ -95,6 +95,7 @@ static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_ev_pool;
+static std::mutex g_handoff_mu;
 static std::unordered_map<void*, void*> g_handoff_bases;  // kd_handoff_open: returned pointer -> mapped base
 static thread_local cudaStream_t g_cur_stream = nullptr;
 
@@ -1039,7 +1040,7 @@ kd_status kd_handoff_open(const void* handle, void** dev_ptr, uint64_t* bytes) {
   void* base = nullptr;
   KD_CUDA(cudaIpcOpenMemHandle(&base, w.ipc, cudaIpcMemLazyEnablePeerAccess));
   {
-    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::lock_guard<std::mutex> lk(g_handoff_mu);
     g_handoff_bases[static_cast<char*>(base) + w.offset] = base;
   }
   *dev_ptr = static_cast<char*>(base) + w.offset;
@@ -1051,7 +1052,7 @@ kd_status kd_handoff_close(void* dev_ptr) {
   if (!dev_ptr) return fail(KD_ERR_INVALID_ARG, "kd_handoff_close: NULL pointer");
   void* base = nullptr;
   {
-    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::lock_guard<std::mutex> lk(g_handoff_mu);
     auto it = g_handoff_bases.find(dev_ptr);
     if (it == g_handoff_bases.end()) return fail(KD_ERR_INVALID_ARG, "kd_handoff_close: not from kd_handoff_open");
     base = it->second;
