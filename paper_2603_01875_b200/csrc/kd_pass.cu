@@ -64,13 +64,17 @@ constexpr int kTileBytes = kBM * kBK * 2;  // 16 KB: one 128x64 bf16 tile (A or 
 //      the epilogue overlaps the next tile's MMAs; BN = 256 fills TMEM with one (t + s) pair (no overlap) but its
 //      UMMA N=256 instructions sustain a much higher tensor-pipe rate (measured).
 #ifndef KD_P2_SMEM_STAGE
-#define KD_P2_SMEM_STAGE 0  // 1: decoupled pass 2 parks the teacher half-tile in shared memory (shallower ring; A/B)
+// Decoupled pass 2 parks the first k 32-column chunks of the teacher half-tile in shared memory (16 KB each, taken
+// from the operand ring) and the rest in L2.  k = 4 (64 KB, 5-stage ring): the L2 staging traffic halves and the
+// power-capped run holds a higher clock, +1.0-1.3% per c2 step over k = 0 (7 stages) in three alternating
+// repetitions; k = 6 (4 stages) starves pass 2, k = 8 (3 stages) much more (profiles/r01_tuning.md).
+#define KD_P2_SMEM_STAGE 4
 #endif
-template <int CG, int BN, bool SST = false>
+template <int CG, int BN, int SCH = 0>
 struct PassCfg {
   static constexpr int kABytes = kTileBytes;                 // 128 rows of H per CTA
   static constexpr int kBBytes = (BN / CG) * kBK * 2;        // BN/CG rows of W per CTA
-  static constexpr int kStageBytes = SST ? BN * kBM * 4 : 0; // SST: the teacher half-tile's fp32 logits in smem
+  static constexpr int kStageBytes = SCH * 32 * kBM * 4;     // SCH chunks of the teacher half-tile in smem
   // operand pipeline: as deep as shared memory allows — the epilogue's global traffic (G stores, z_t staging)
   // raises the TMA latency the pipeline must cover (7 x 32 KB stages for the SM-pair 256-col tile)
   static constexpr int kStages = (KD_PASS_SMEM_KB * 1024 - kStageBytes) / (kABytes + kBBytes);
@@ -102,8 +106,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
                    const PassParams p) {
-  constexpr bool SST = KD_P2_SMEM_STAGE && DEC && PASS == 2;
-  using C = PassCfg<CG, BN, SST>;
+  constexpr int SCH = (DEC && PASS == 2) ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
+  using C = PassCfg<CG, BN, SCH>;
   constexpr int kStages = C::kStages;
   constexpr int kNB = DEC ? 2 : C::kNumBuf;  // accumulator buffers (DEC: one half-tile side per buffer)
   static_assert(!DEC || PASS == 2 || KIND == KIND_FKL || KIND == KIND_TOPK, "decoupled pass 1 uses the FKL role order");
@@ -673,8 +677,9 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         // while the next vocab tile's teacher MMAs proceed.
         // staging layout [column / 4][row][4]: each lane moves 16 B per access and a warp's access is one
         // contiguous 512 B run
-        float4* zrow = (SST ? reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256)  // after the barrier block
-                            : reinterpret_cast<float4*>(p.zscr + (size_t)blockIdx.x * (BN * kBM))) + r_in_tile;
+        float4* zrow = reinterpret_cast<float4*>(p.zscr + (size_t)blockIdx.x * (BN * kBM)) + r_in_tile;
+        // chunks c < SCH live in shared memory, after the barrier block (same [column / 4][row][4] layout)
+        float4* zsm = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256) + r_in_tile;
         constexpr int kChunks = BN / 32;
         const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
@@ -697,7 +702,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               float z[32];
               tmem_ld32_sync(t_addr + c * 32, z);
               if (c == c_end - 1) release(buf);
-              float4* zc = zrow + (size_t)c * 8 * kBM;
+              float4* zc = (c < SCH ? zsm : zrow) + (size_t)c * 8 * kBM;
 #ifndef KD_X_NOSTAGE  // experiment builds only: no staging traffic (the student half reuses its own logits)
 #pragma unroll
               for (int j = 0; j < 8; ++j) zc[j * kBM] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
@@ -727,7 +732,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 #pragma unroll 1
             for (int c = c_beg; c < c_end; ++c) {
               float zt[32], zs[32];
-              const float4* zc = zrow + (size_t)c * 8 * kBM;
+              const float4* zc = (c < SCH ? zsm : zrow) + (size_t)c * 8 * kBM;
 #ifndef KD_X_NOSTAGE
               if (p.side_lo == 0) {
 #pragma unroll
@@ -751,7 +756,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (c == c_end - 1) release(buf);
               const int v0 = vt * BN + c * 32;
               p2chunk(zt, zs, v0, min(32, p.V_r - v0));
-              if (!SST && (p.l2_hints & 2)) {
+              if (c >= SCH && (p.l2_hints & 2)) {
                 // the staged lines are dead: drop them from L2 without a write-back (the warp's 4 KB of the chunk)
                 __syncwarp();
                 l2_discard128(reinterpret_cast<const char*>(zc - lane) + (size_t)(lane >> 2) * kBM * 16 + (lane & 3) * 128);
@@ -917,7 +922,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 template <int PASS, int KIND, int CG, int BN, bool DEC = false>
 static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t stream) {
   auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC>;
-  const int smem = PassCfg<CG, BN, KD_P2_SMEM_STAGE && DEC && PASS == 2>::kSmem;
+  constexpr int SCH = (DEC && PASS == 2) ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
+  const int smem = PassCfg<CG, BN, SCH>::kSmem;
   // the shared-memory opt-in once per (instantiation, device): a driver call on every launch was measurable host
   // time for the per-chunk callers
   static std::atomic<uint64_t> smem_set{0};

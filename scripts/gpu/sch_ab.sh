@@ -1,0 +1,10 @@
+# A/B: decoupled pass 2 with the first k 32-column chunks of the teacher half-tile staged in smem (k=2: 6-stage ring,
+# k=4: 5 stages) vs all in L2 (7 stages).
+L=$PWD/paper_2603_01875_b200
+KD_LIB_PATH=$L/libkdfused_sch2.so timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x > gpurun_out/sch_tests.log 2>&1; tail -1 gpurun_out/sch_tests.log
+KD_LIB_PATH=$L/libkdfused_sch4.so timeout 900 python -m pytest tests/test_gpu_parity.py -q --tb=short -x > gpurun_out/sch_tests4.log 2>&1; tail -1 gpurun_out/sch_tests4.log
+for rep in 1 2; do for v in base sch2 sch4; do
+  lib=$L/libkdfused.so; [ $v != base ] && lib=$L/libkdfused_$v.so
+  KD_LIB_PATH=$lib timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-variants > gpurun_out/sch_$v.json 2>&1
+  python -c "import json; d=json.loads(open('gpurun_out/sch_$v.json').read().strip().splitlines()[-1]); k=d['kernels']; print('$v', round(d['value']), d['clocks']['sm_mhz'], {n: round(k[n]['ms_per_step'],2) for n in ('pass1','pass2','gemm_dh')})"
+done; done
