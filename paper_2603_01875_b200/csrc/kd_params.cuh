@@ -16,7 +16,12 @@ constexpr int kPassStages = 6;  // smem ring depth of the fused passes (6 x 32 K
 // Fused-pass epilogue: kEpiParts warps per TMEM lane quarter, each owning a contiguous part of the tile's columns.
 // FKL/RKL (and every pass 1) use 3 parts (12 warps, <= 128 registers); JSD/TVD pass 2 needs more registers and uses 2.
 constexpr int kEpiPartsMax = 3;
-__host__ __device__ constexpr int epi_parts(int pass, int kind) { return (pass == 2 && kind >= 2) ? 2 : 3; }
+#ifndef KD_P1_PARTS
+#define KD_P1_PARTS 3  // epilogue warps per TMEM lane quarter in pass 1 (A/B knob)
+#endif
+__host__ __device__ constexpr int epi_parts(int pass, int kind) {
+  return (pass == 2 && kind >= 2) ? 2 : (pass == 1 ? KD_P1_PARTS : 3);
+}
 __host__ __device__ constexpr int pass_threads(int parts) { return 128 + 32 * 4 * parts; }  // warps 0-3: TMA/MMA/alloc/idle
 // Per token row, each (vocab split, column part) writes its own partial record / K-J partial / residual slots:
 // "record slots" = n_split * parts, merged downstream in a fixed order.
