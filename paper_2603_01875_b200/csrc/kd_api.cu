@@ -356,6 +356,8 @@ static Plan make_plan(const kd_problem* p) {
   const int slots_max = std::max(P.n_gslots, P.n_split * epi_parts(2, P.kind));
   P.k_split = choose_k_split((P.Nc + kBM * gemm_cg() - 1) / (kBM * gemm_cg()), (P.d_s + kGemmBN - 1) / kGemmBN,
                              (P.V_r + kBK - 1) / kBK, P.num_sms / gemm_cg(), P.Nc, P.d_s);
+  static const int ks_env = env_int("KD_DH_KSPLIT", 0);  // A/B override of the dh GEMM's split-K factor
+  if (ks_env > 0) P.k_split = ks_env;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
   P.off_neff = take(8);
