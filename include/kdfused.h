@@ -12,9 +12,10 @@
  *     G   = loss_scale · mask_n · ∂ℓ_n/∂Z_s                          (teacher constant)
  *     dL/dh_s = G · W_s ,   dL/dW_s (+)= Gᵀ · H_s                    ("backward passes")
  *
- * The vocabulary is swept in 128-column tiles with an online log-sum-exp, so no [tokens × V] logit
- * tensor exists in HBM (BASELINE.json north_star).  Definitions and the readings of points the paper
- * leaves open (no T² factor, β convention, reduction, masking) are in DESIGN.md "Readings" R1-R12.
+ * The vocabulary is swept in 256-column tiles (SM-pair UMMA, 256 tokens x 256 vocab rows) with an online
+ * log-sum-exp, so no [tokens × V] logit tensor exists in HBM (BASELINE.json north_star).  Definitions and the
+ * readings of points the paper leaves open (no T² factor, β convention, reduction, masking) are in DESIGN.md
+ * "Readings" R1-R20.
  *
  * Conventions for every entry point
  *  - All tensor pointers are DEVICE pointers (cudaMalloc / PyTorch CUDA memory), row-major, owned by

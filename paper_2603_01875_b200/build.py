@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{log}")
         if verbose and log:
             print(log)
-    tmp = out + ".tmp"
+    tmp = os.path.join(bdir, os.path.basename(out) + ".link")  # link output under _build/, then moved into place
     link = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcuda"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:

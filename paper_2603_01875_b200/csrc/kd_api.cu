@@ -100,23 +100,34 @@ static std::unordered_map<void*, void*> g_handoff_bases;  // kd_handoff_open: re
 static thread_local cudaStream_t g_cur_stream = nullptr;
 
 static cudaEvent_t prof_event() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);  // kd_profile_read returns events to the pool from another thread
   if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
   cudaEvent_t e;
   cudaEventCreate(&e);
   return e;
 }
 
+// Per-launch event brackets are recorded only outside stream capture: an event recorded into a graph
+// is not something kd_profile_read could synchronise on later.
+static bool prof_active() {
+  if (!g_prof_on) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(g_cur_stream, &cs) != cudaSuccess) return false;
+  return cs == cudaStreamCaptureStatusNone;
+}
+
 #define KD_LAUNCH(id, expr)                                                  \
   do {                                                                       \
     cudaEvent_t ea_ = nullptr, eb_ = nullptr;                                \
-    if (g_prof_on) { ea_ = prof_event(); cudaEventRecord(ea_, g_cur_stream); } \
+    const bool prof_ = prof_active();                                        \
+    if (prof_) { ea_ = prof_event(); cudaEventRecord(ea_, g_cur_stream); }   \
     KD_CUDA(expr);                                                           \
     ++g_launches;                                                            \
-    if (g_prof_on) {                                                         \
+    if (prof_) {                                                             \
       eb_ = prof_event();                                                    \
       cudaEventRecord(eb_, g_cur_stream);                                    \
       std::lock_guard<std::mutex> lk_(g_prof_mu);                            \
-      g_prof.push_back({(id), ea_, eb_});                       \
+      g_prof.push_back({(id), ea_, eb_});                                    \
     }                                                                        \
   } while (0)
 
@@ -190,7 +201,11 @@ static int device_sms() {
 }
 
 // Backward GEMMs flush their TMEM accumulator into the fp32 output every kKbPerAcc K blocks (see kd_gemm.cu).
-constexpr int kKbPerAccDefault = 64;
+// 16 (1024 K values, 64 MMA steps per accumulator): the dh GEMM sums K = V = 151936 products into results ~100x smaller
+// than its terms (the bias column), and the truncating tcgen05 accumulation grows with the steps per accumulator —
+// at 64 the config-4 dh_s bias column reached 4.1x the north-star bound, at 16 0.80x (scripts/probe_parity_src.py,
+// profiles/r02_parity.md).  The promotion adds are overlapped with the next piece's MMAs (double-buffered TMEM).
+constexpr int kKbPerAccDefault = 16;
 static int kb_per_acc() {  // KD_KB_PER_ACC overrides the promotion period (precision experiments)
   static int v = [] {
     const char* e = getenv("KD_KB_PER_ACC");
@@ -366,7 +381,7 @@ static Plan make_plan(const kd_problem* p) {
   P.off_ht = take((size_t)P.N * P.d_t * 2);
   P.off_hs = take((size_t)P.N * P.d_s * 2);
   P.off_part = take((size_t)5 * P.n_split * epi_parts(1, P.kind) * P.Nc * 4);
-  P.off_fstats = take((size_t)5 * P.Nc * 4);
+  P.off_fstats = take((size_t)kFstatPlanes * P.Nc * 4);
   // JSD/TVD: K and J partials; FKL: the loss partials of pass 2 (plane 0)
   P.off_kpart = take((P.fix || P.kind == KD_FKL) ? (size_t)2 * slots_max * P.Nc * 4 : 0);
   P.off_kfin = take(P.fix ? (size_t)P.Nc * 4 : 0);
@@ -913,7 +928,10 @@ static kd_status vocab_fix_setup(Ctx& c, const kd_problem* p, void* workspace, s
   if (c.P.n_chunks > 1)
     return fail(KD_ERR_SHAPE, "JSD/TVD vocab shards run one token chunk per call: n_tokens (%d) must be <= the chunk (%d)",
                 c.P.N, c.P.Nc);
-  if (!workspace || workspace_bytes < c.P.total) return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255))
+    return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace must be non-NULL and 256-byte aligned");
+  if (workspace_bytes < c.P.total)
+    return fail(KD_ERR_WORKSPACE_TOO_SMALL, "workspace %zu bytes < required %zu", workspace_bytes, c.P.total);
   return KD_OK;
 }
 
@@ -926,7 +944,12 @@ kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_
   const Plan& P = c.P;
   if (P.N == 0) return KD_OK;
   if (!recs || !kj) return fail(KD_ERR_INVALID_ARG, "recs / kj is NULL");
-  if (!aligned16(kj)) return fail(KD_ERR_ALIGNMENT, "kj must be 16-byte aligned");
+  if (!aligned16(kj) || !aligned16(recs)) return fail(KD_ERR_ALIGNMENT, "recs / kj must be 16-byte aligned");
+  // the same input checks as every other entry point (pointers, alignment, workspace), before any launch; dW_s is
+  // kd_vocab_finish's output, not this call's
+  kd_problem q = *p;
+  q.want_dW = 0;
+  if ((st = check_common(&q, h_t, W_t, h_s, W_s, kj, kj, nullptr, workspace, workspace_bytes, P)) != KD_OK) return st;
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
   KD_CUDA(cudaMemsetAsync(kj, 0, (size_t)2 * P.N * sizeof(float), c.s));
   KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, 0, c.n_eff, P.kind, 0,

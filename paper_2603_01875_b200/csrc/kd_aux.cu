@@ -129,7 +129,7 @@ __device__ __forceinline__ Rec merge_records(const float* __restrict__ part, lon
   return Rec{Mp, Mq, warp_sum_d(Sp), warp_sum_d(Sq), warp_sum_d(U)};
 }
 
-// mode 0: final statistics of the chunk's rows (fstats + FKL/RKL loss); mode 1: the merged record itself
+// mode 0: final statistics of the chunk's rows (fstats [kFstatPlanes][n_rows] + FKL/RKL loss); mode 1: the merged record itself
 // (vocab-shard partial, written per ORIGINAL row).  Records of row r for split s live at
 // part[f*plane + s*split_stride + row], row = r (chunk-local) or the original row (orig_rows = 1).
 __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ part, long long plane,
@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
     return;
   }
   const float lp = (float)log2(A.Sp), lq = (float)log2(A.Sq);
-  const float ell2 = (float)__dadd_rn(__dsub_rn(__ddiv_rn(A.U, A.Sp), log2(A.Sp)), log2(A.Sq));  // FKL / RKL, bits
+  const double ell2d = __dadd_rn(__dsub_rn(__ddiv_rn(A.U, A.Sp), log2(A.Sp)), log2(A.Sq));  // FKL / RKL, bits
+  const float ell2 = (float)ell2d;
   const bool rkl = kind == KIND_RKL;
   // LSE_2 = M + log2 S kept as two numbers (see kd_pass.cu, pass 2)
   fstats[r] = (float)(rkl ? A.Mq : A.Mp);        // M_t  (inputs were fp32 maxima: exact)
@@ -173,6 +174,16 @@ __global__ void __launch_bounds__(256) k_merge_stats(const float* __restrict__ p
   fstats[2 * n_rows + r] = (float)(rkl ? A.Mp : A.Mq);  // M_s
   fstats[3 * n_rows + r] = rkl ? lp : lq;        // log2 S_s
   fstats[4 * n_rows + r] = ell2;
+  if (rkl) {
+    // RKL's per-row gradient offset dlr = (log2 S_s − log2 S_t) + RKL (bits), with the two log2 S as the fp32 values
+    // pass 2 normalises with, as an unevaluated hi + lo pair: one fp32 number would put its rounding (~1e-7 relative
+    // of an RKL of several bits) on every g_v = c·q_v·(u_s − u_t − dlr) alike — a common-mode error that Σ_v g_v b_v
+    // multiplies by E_q[b] (the Zipf-bias column of dh_s).  Found by tests/test_gpu_general.py at T = 0.5.
+    const double dlr = __dadd_rn(__dsub_rn((double)lp, (double)lq), ell2d);  // RKL: S_p is the student's sum
+    const float hi = (float)dlr;
+    fstats[5 * n_rows + r] = hi;
+    fstats[6 * n_rows + r] = (float)__dsub_rn(dlr, (double)hi);
+  }
   if (tstats_in) {  // teacher LSE supplied by the caller (kd_fused_fwd_bwd_lse): pass 1 swept the student only
     fstats[r] = tstats_in[orow];
     fstats[n_rows + r] = tstats_in[rec_plane + orow];

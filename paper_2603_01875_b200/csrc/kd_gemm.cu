@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4 * CG);  // every epilogue warp of the group releases
+      mbar_init(&tempty[b], kGemmEpiWarps * CG);  // every epilogue warp of the group releases
     }
     fence_barrier_init();
   }
@@ -188,7 +188,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ================================================================ epilogue
-    const uint32_t q4 = warp - 4;
+    // kGemmEpiWarps warps: (warp - 4) % 4 = TMEM lane quarter (one output row per thread), (warp - 4) / 4 = which
+    // contiguous part of the tile's 32-column chunks.  A promotion piece's read-modify-write loads all eight float4 of
+    // a chunk before the first add, so a warp keeps 8 L2 round trips in flight instead of one (with 16-block pieces
+    // the RMW would otherwise outlast the piece's MMAs).
+    constexpr int kParts = kGemmEpiWarps / 4, kChunks = kGemmBN / 32;
+    const uint32_t q4 = (warp - 4) & 3;
+    const int part = (int)(warp - 4) >> 2;
+    const int c_beg = part * kChunks / kParts, c_end = (part + 1) * kChunks / kParts;
     const uint32_t lane_addr = (q4 * 32) << 16;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     uint32_t it = 0;
@@ -201,42 +208,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool empty_k = kb1 <= kb0;
       float* orow = p.out + (size_t)ks * p.out_split_stride + (size_t)row * p.out_ld + n0;
       for (int pc = 0; pc < npieces; ++pc, ++it) {
-      const uint32_t buf = it & 1, tph = (it >> 1) & 1;
-      mbar_wait(&tfull[buf], tph);
-      tc_fence_after();
-      // first piece of an EPI_STORE unit stores; every other piece accumulates into what is there
-      const bool accumulate = (EPI == EPI_ACCUM) || pc > 0;
+        const uint32_t buf = it & 1, tph = (it >> 1) & 1;
+        mbar_wait(&tfull[buf], tph);
+        tc_fence_after();
+        // first piece of an EPI_STORE unit stores; every other piece accumulates into what is there
+        const bool accumulate = (EPI == EPI_ACCUM) || pc > 0;
 #pragma unroll 1
-      for (int c = 0; c < kGemmBN / 32; ++c) {
-        float v[32];
-        tmem_ld32_sync(tmem_base + lane_addr + buf * kGemmBN + c * 32, v);
-        if (c == kGemmBN / 32 - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + buf * 8);
-            else mbar_arrive_relaxed(&tempty[buf]);
+        for (int c = c_beg; c < c_end; ++c) {
+          float v[32];
+          tmem_ld32_sync(tmem_base + lane_addr + buf * kGemmBN + c * 32, v);
+          if (c == c_end - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + buf * 8);
+              else mbar_arrive_relaxed(&tempty[buf]);
+            }
+          }
+          if (!row_ok || n0 + c * 32 >= p.N) continue;
+          float* o = orow + c * 32;
+          if (accumulate) {
+            if (empty_k) continue;
+            float4 prev[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) prev[i] = __ldcg(reinterpret_cast<const float4*>(o + 4 * i));
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              st_global_v4(o + 4 * i, __float_as_uint(prev[i].x + v[4 * i]), __float_as_uint(prev[i].y + v[4 * i + 1]),
+                           __float_as_uint(prev[i].z + v[4 * i + 2]), __float_as_uint(prev[i].w + v[4 * i + 3]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float a = empty_k ? 0.f : v[4 * i], b = empty_k ? 0.f : v[4 * i + 1];
+              const float c2 = empty_k ? 0.f : v[4 * i + 2], d2 = empty_k ? 0.f : v[4 * i + 3];
+              st_global_v4(o + 4 * i, __float_as_uint(a), __float_as_uint(b), __float_as_uint(c2), __float_as_uint(d2));
+            }
           }
         }
-        if (!row_ok || n0 + c * 32 >= p.N) continue;
-        float* o = orow + c * 32;
-        if (accumulate) {
-          if (empty_k) continue;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 prev = *reinterpret_cast<const float4*>(o + 4 * i);
-            st_global_v4(o + 4 * i, __float_as_uint(prev.x + v[4 * i]), __float_as_uint(prev.y + v[4 * i + 1]),
-                         __float_as_uint(prev.z + v[4 * i + 2]), __float_as_uint(prev.w + v[4 * i + 3]));
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float a = empty_k ? 0.f : v[4 * i], b = empty_k ? 0.f : v[4 * i + 1];
-            const float c2 = empty_k ? 0.f : v[4 * i + 2], d2 = empty_k ? 0.f : v[4 * i + 3];
-            st_global_v4(o + 4 * i, __float_as_uint(a), __float_as_uint(b), __float_as_uint(c2), __float_as_uint(d2));
-          }
-        }
-      }
       }
     }
   }

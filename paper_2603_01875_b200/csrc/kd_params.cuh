@@ -9,13 +9,10 @@ enum Kind : int { KIND_FKL = 0, KIND_RKL = 1, KIND_JSD = 2, KIND_TVD = 3,
                   KIND_TOPK = 4 /* kernel-internal: teacher-only pass 1 selecting the per-row top-kTopK logits */ };
 constexpr int kTopK = 32;  // largest k of the top-k teacher baseline (kd_teacher_topk): per-thread register lists
 
-constexpr int kBM = 128;        // token rows per tile (UMMA M, one TMEM lane per token)
-constexpr int kBN = 128;        // vocab columns per tile in the fused passes
+constexpr int kBM = 128;        // token rows per CTA tile (one TMEM lane per token; an SM pair covers 256)
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
-constexpr int kPassStages = 6;  // smem ring depth of the fused passes (6 x 32 KB)
-// Fused-pass epilogue: kEpiParts warps per TMEM lane quarter, each owning a contiguous part of the tile's columns.
+// Fused-pass epilogue: epi_parts() warps per TMEM lane quarter, each owning a contiguous part of the tile's columns.
 // FKL/RKL (and every pass 1) use 3 parts (12 warps, <= 128 registers); JSD/TVD pass 2 needs more registers and uses 2.
-constexpr int kEpiPartsMax = 3;
 #ifndef KD_P1_PARTS
 #define KD_P1_PARTS 3  // epilogue warps per TMEM lane quarter in pass 1 (A/B knob)
 #endif
@@ -25,6 +22,7 @@ __host__ __device__ constexpr int epi_parts(int pass, int kind) {
 __host__ __device__ constexpr int pass_threads(int parts) { return 128 + 32 * 4 * parts; }  // warps 0-3: TMA/MMA/alloc/idle
 // Per token row, each (vocab split, column part) writes its own partial record / K-J partial / residual slots:
 // "record slots" = n_split * parts, merged downstream in a fixed order.
+constexpr int kFstatPlanes = 7;           // per-row final statistics planes (PassParams::fstats)
 constexpr int kCorrSlots = 2;              // residual slots per (token row, vocab split)
 constexpr float kCorrThresh = 7.8125e-3f;  // 2^-7: below it the split residual (< 2^-25·|W|) is negligible
 
@@ -35,7 +33,7 @@ struct PassParams {
   int row0;           // first packed row of the chunk
   int n_rows;         // chunk capacity (multiple of kBM)
   int kb_t, kb_s;     // K blocks of the teacher / student GEMM (d/64)
-  int v_tiles;        // ceil(V_r / kBN)
+  int v_tiles;        // ceil(V_r / BN), BN = the vocab tile (UMMA N) of the launch
   int V_r;            // local vocabulary rows
   int n_split;
   float alpha;        // log2(e) / T
@@ -43,7 +41,8 @@ struct PassParams {
   float* part;
   long long part_plane;
   // pass 2 inputs/outputs
-  const float* fstats;  // [5][n_rows]: M_t, log2 S_t, M_s, log2 S_s (base-2 LSE parts of z/T), ell2 (bits)
+  const float* fstats;  // [kFstatPlanes][n_rows]: M_t, log2 S_t, M_s, log2 S_s (base-2 LSE parts of z/T),
+                        // ell2 (bits), RKL only: dlr_hi, dlr_lo (the gradient's per-row offset, see k_merge_stats)
   float gscale;         // c = loss_scale / T (FKL/RKL already folded with ln2 where needed)
   float beta;           // JSD beta
   __nv_bfloat16* g_hi;  // Gᵀ: [g_ld][n_rows] (vocab-major, token rows contiguous)
@@ -79,7 +78,7 @@ struct StageParams {
   int row0, n_rows, V_r, g_ld;
   float alpha, gscale, beta;
   const float* zst;     // [2][g_ld][n_rows] (teacher plane, then student plane)
-  const float* fstats;  // [5][n_rows] as PassParams::fstats
+  const float* fstats;  // [kFstatPlanes][n_rows] as PassParams::fstats
   __nv_bfloat16* g_hi;
   __nv_bfloat16* g_lo;
   float* g_a;
@@ -94,7 +93,8 @@ enum GemmEpi : int { EPI_STORE = 0, EPI_ACCUM = 1 };
 enum DynDim : int { DYN_NONE = 0, DYN_M = 1, DYN_K = 2 };
 
 constexpr int kGemmBN = 256;
-constexpr int kGemmThreads = 256;
+constexpr int kGemmEpiWarps = 8;  // backward-GEMM epilogue warps: 2 per TMEM lane quarter, each half the columns
+constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;  // warps 0-3: TMA / MMA / TMEM alloc / idle
 
 struct GemmParams {
   int M, N, K;         // static extents (the dynamic one is an upper bound)

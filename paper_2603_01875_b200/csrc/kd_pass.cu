@@ -1,7 +1,7 @@
 // kd_pass.cu — the fused vocabulary sweeps of the KD hot path (sm_100a).
 //
-// One persistent CTA per SM.  Per (128-token tile, 128-vocab tile) the CTA computes BOTH LM-head
-// logit tiles with tcgen05 tensor-core MMAs into TMEM:
+// Persistent grid of SM pairs (clusters of 2, tcgen05.mma.cta_group::2): per (256-token tile, 256-vocab tile) the
+// pair computes BOTH LM-head logit tiles with UMMA M=256, N=256 into TMEM:
 //     Z_t = H_t · W_tᵀ   (K = d_t)   and   Z_s = H_s · W_sᵀ   (K = d_s)
 // ("recomputes the full logit distributions using the teacher's language model head";
 //  the student's own LM head is fused the same way), and an epilogue consumes them straight from TMEM,
@@ -15,9 +15,12 @@
 //       FKL/RKL: written as a split-bf16 (hi + lo) pair for the backward GEMMs;
 //       JSD/TVD: written as the two fp32 planes (q·ℓ_v, q) plus per-unit partial K, fixed up later.
 //
-// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM allocator,
-// warps 4..7 = epilogue (thread i of warp 4+j owns token row 32j + i = TMEM lane 32j + i).
-// TMEM: 2 accumulator buffers × (teacher 128 cols + student 128 cols) = 512 columns.
+// Warp roles (128 + 128·EP threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA only), warp 2 = TMEM
+// allocator, warp 3 idle, warps 4.. = epilogue: EP warps per TMEM lane quarter (thread i of warp 4+w owns token row
+// 32·(w%4) + i of the CTA's 128), each warp a contiguous part of the tile's 32-column chunks.
+// TMEM (512 columns): decoupled form (DEC, the default) — two 256-column accumulators, one per half-tile (teacher
+// K blocks, then student K blocks of the same vocab tile), so each half's epilogue overlaps the other half's MMAs;
+// coupled form — one (teacher 256 + student 256) pair.  BN = 128 / single-SM tiles remain as A/B variants.
 #include <utility>
 
 #include <atomic>
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       // Probabilities are evaluated as p = ex2(fma(z, α, −M)) · 2^(−log2 S): the dominant token's exponent is
       // ~0, where ex2.approx is essentially exact, and the normalisation is a correctly rounded multiply.
       // (ex2 at x − log2 S instead puts ex2's ~2^-22 error on p_top ≈ 1, which q − p then exposes.)
-      float Mt2 = 0.f, lSt = 0.f, Ms2 = 0.f, lSs = 0.f, ell2 = 0.f, Kacc = 0.f, Jacc = 0.f;
+      float Mt2 = 0.f, lSt = 0.f, Ms2 = 0.f, lSs = 0.f, Kacc = 0.f, Jacc = 0.f, dlr = 0.f, dlr_lo = 0.f;
       float iSt = 1.f, iSs = 1.f;
       float cK = 0.f, cJ = 0.f;    // Kahan compensations of the JSD/TVD row sums
       float cr0 = 0.f, cr1 = 0.f;  // residual-fix slots (pass 2, FKL/RKL)
@@ -520,7 +523,10 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         lSt = p.fstats[p.n_rows + r_local];
         Ms2 = p.fstats[2 * p.n_rows + r_local];
         lSs = p.fstats[3 * p.n_rows + r_local];
-        ell2 = p.fstats[4 * p.n_rows + r_local];
+        if (KIND == KIND_RKL) {
+          dlr = p.fstats[5 * p.n_rows + r_local];
+          dlr_lo = p.fstats[6 * p.n_rows + r_local];
+        }
         iSt = exp2f(-lSt);
         iSs = exp2f(-lSs);
       }
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       // so g = gscale·(q − p) stays exactly 0 when teacher and student agree; RKL's log-ratio offset
       const float2 negM2 = make_float2(-Mt2, -Ms2);
       const float2 cTS = make_float2(__fmul_rn(iSt, p.gscale), __fmul_rn(iSs, p.gscale));
-      const float dlr = (lSs - lSt) + ell2;
+      // RKL: g = gscale·q·((u_s − u_t) − dlr), dlr = (log2 S_s − log2 S_t) + RKL/ln2 as an fp64-exact hi + lo pair
       const float dlt = lSt - lSs;          // FKL: log2 p − log2 q = (u_t − u_s) − (log2 S_t − log2 S_s)
       float Lacc = 0.f, cL = 0.f;           // FKL loss partial (pass 2)
       // pass 2, one 32-column chunk of the tile: the logit gradient of this row from both sides' raw logits
@@ -553,7 +559,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
                 // FKL loss in bits, unnormalised: Σ 2^{u_t} · (log2 p − log2 q); × 2^-log2 S_t at unit end
                 la[i & 1] = fmaf(r.x, (u.x - u.y) - dlt, la[i & 1]);
               } else {
-                g[i] = e.y * ((u.y - u.x) - dlr);  // gscale·q·(log2(q/p) − RKL/ln2)
+                g[i] = e.y * (((u.y - u.x) - dlr) - dlr_lo);  // gscale·q·(log2(q/p) − RKL/ln2)
               }
             });
             if (KIND == KIND_FKL) kahan_add(Lacc, cL, la[0] + la[1]);
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               const float2 u = ffma2(make_float2(zt[i], zs[i]), make_float2(alpha, alpha), negM2);
               const float2 r = make_float2(ex2(u.x), ex2(u.y));
               const float2 e = fmul2(r, cTS);
-              const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr);
+              const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * (((u.y - u.x) - dlr) - dlr_lo);
               g[i] = ok ? gi : 0.f;
               if (KIND == KIND_FKL && ok) la = fmaf(r.x, (u.x - u.y) - dlt, la);
             }
@@ -607,6 +613,18 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) x ^= hi[i] ^ lo[i];
             if (x == 0x9E3779B9u) *ph = __float2bfloat16(1.f);
+            return;
+          }
+#endif
+#ifdef KD_X_GV4  // experiment builds only: G row-major [n_rows][g_ld] with 16-B vector stores (timing, not parity)
+          {
+            uint4* qh = reinterpret_cast<uint4*>(p.g_hi + (size_t)r_local * p.g_ld + v0);
+            uint4* ql = reinterpret_cast<uint4*>(p.g_lo + (size_t)r_local * p.g_ld + v0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              qh[j] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+              ql[j] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+            }
             return;
           }
 #endif

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
   const int c0 = (int)((long long)slot * nst / n_slots), c1 = (int)((long long)(slot + 1) * nst / n_slots);
   const float alpha = sp.alpha;
   bool row_ok[R];
-  float Mt2[R], lSt[R], Ms2[R], lSs[R], iSt[R], iSs[R], dlr[R], dlt[R];
+  float Mt2[R], lSt[R], Ms2[R], lSs[R], iSt[R], iSs[R], dlr[R], dlr_lo[R], dlt[R];
   float2 cTS[R];
   // row totals (Kahan-compensated over steps): FKL loss L; JSD/TVD K and J
   float Ltot[R], cL[R], Ktot[R], cK[R], Jtot[R], cJ[R], cr0[R], cr1[R];
@@ -74,20 +74,21 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
   for (int j = 0; j < R; ++j) {
     const int r = r0 + j;
     row_ok[j] = r < valid;
-    Mt2[j] = lSt[j] = Ms2[j] = lSs[j] = 0.f;
-    float ell2 = 0.f;
+    Mt2[j] = lSt[j] = Ms2[j] = lSs[j] = dlr[j] = dlr_lo[j] = 0.f;
     iSt[j] = iSs[j] = 1.f;
     if (row_ok[j]) {
       Mt2[j] = sp.fstats[r];
       lSt[j] = sp.fstats[sp.n_rows + r];
       Ms2[j] = sp.fstats[2 * sp.n_rows + r];
       lSs[j] = sp.fstats[3 * sp.n_rows + r];
-      ell2 = sp.fstats[4 * sp.n_rows + r];
+      if (KIND == KIND_RKL) {  // the RKL gradient offset as an fp64-exact hi + lo pair (k_merge_stats)
+        dlr[j] = sp.fstats[5 * sp.n_rows + r];
+        dlr_lo[j] = sp.fstats[6 * sp.n_rows + r];
+      }
       iSt[j] = exp2f(-lSt[j]);
       iSs[j] = exp2f(-lSs[j]);
     }
     cTS[j] = make_float2(__fmul_rn(iSt[j], sp.gscale), __fmul_rn(iSs[j], sp.gscale));
-    dlr[j] = (lSs[j] - lSt[j]) + ell2;
     dlt[j] = lSt[j] - lSs[j];
     Ltot[j] = cL[j] = Ktot[j] = cK[j] = Jtot[j] = cJ[j] = cr0[j] = cr1[j] = 0.f;
     cv0[j] = cv1[j] = 0;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
                                make_float2(-Mt2[j], -Ms2[j]));
         const float2 e2 = make_float2(ex2(u.x), ex2(u.y));
         const float2 e = fmul2(e2, cTS[j]);  // (gscale·p, gscale·q)
-        const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * ((u.y - u.x) - dlr[j]);
+        const float gi = KIND == KIND_FKL ? e.y - e.x : e.y * (((u.y - u.x) - dlr[j]) - dlr_lo[j]);
         g[i][j] = ok ? gi : 0.f;
         if (KIND == KIND_FKL) stepL[j] = fmaf(ok ? e2.x : 0.f, (u.x - u.y) - dlt[j], stepL[j]);
         amax = fmaxf(amax, fabsf(g[i][j]));

@@ -142,15 +142,32 @@ def workspace_size(p: KDProblem) -> int:
 
 
 _ws_cache: dict = {}
+_ws_graph_held: list = []  # buffers a captured CUDA graph may still point at: never freed
 
 
-def _workspace(nbytes: int, device) -> torch.Tensor:
-    key = torch.device(device)
+def _workspace(nbytes: int, device, stream=None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """The call's workspace: the caller's ``workspace`` tensor if given (required size checked by the library),
+    else a cached buffer keyed by (device, stream).
+
+    The cached buffer is allocated ON the launch stream, so when it is outgrown and dropped the caching allocator
+    only reuses its memory in that stream's order (after the kernels already queued there).  A buffer handed out
+    while the stream is being captured into a CUDA graph is kept alive for the life of the process, so a later,
+    larger call can never free memory a graph replays into."""
+    if workspace is not None:
+        if not workspace.is_cuda or workspace.device != torch.device(device):
+            raise ValueError("workspace must be a CUDA tensor on the inputs' device")
+        return workspace
+    dev = torch.device(device)
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    key = (dev, s.cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
         _ws_cache.pop(key, None)
-        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=key)
+        with torch.cuda.stream(s):
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
         _ws_cache[key] = buf
+    if torch.cuda.is_current_stream_capturing() and not any(b is buf for b in _ws_graph_held):
+        _ws_graph_held.append(buf)
     return buf
 
 
@@ -194,7 +211,7 @@ class KDResult:
 
 def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False,
                   accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split", stage_logits=False,
-                  out=None, stream=None) -> KDResult:
+                  out=None, stream=None, workspace=None) -> KDResult:
     """kd_fused_fwd_bwd: per-token loss, dL/dh_s and (optionally) dL/dW_s for device tensors.
 
     ``stage_logits=True`` selects the staged variant (pass 1 writes the chunk's fp32 logits, G from them)."""
@@ -215,7 +232,7 @@ def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5,
         loss, dh, nnf = out.loss, out.dh_s, out.n_nonfinite
     if want_dW and dW_s is None:
         dW_s = (torch.zeros if accumulate_dW else torch.empty)(V, d_s, dtype=torch.float32, device=dev)
-    ws = _workspace(workspace_size(p), dev)
+    ws = _workspace(workspace_size(p), dev, stream, workspace)
     _check(lib().kd_fused_fwd_bwd(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(h_s), _ptr(W_s), _ptr(mask),
                                   _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws),
                                   ws.numel(), _stream_handle(stream)))
@@ -223,7 +240,7 @@ def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5,
 
 
 def teacher_lse(h_t, W_t, mask=None, *, d_s, T=1.0, kind="fkl", chunk_tokens=0, out=None,
-                stream=None) -> torch.Tensor:
+                stream=None, workspace=None) -> torch.Tensor:
     """kd_teacher_lse: the teacher's per-token base-2 LSE record [2, N] (M_t, log2 S_t) at temperature T.
 
     ``d_s`` / ``kind`` / ``chunk_tokens`` must match the student call that consumes the record (they size the
@@ -235,7 +252,7 @@ def teacher_lse(h_t, W_t, mask=None, *, d_s, T=1.0, kind="fkl", chunk_tokens=0, 
     if mask is not None:
         mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
     lse = out if out is not None else torch.zeros(2, N, dtype=torch.float32, device=h_t.device)
-    ws = _workspace(workspace_size(p), h_t.device)
+    ws = _workspace(workspace_size(p), h_t.device, stream, workspace)
     _check(lib().kd_teacher_lse(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(mask), _ptr(lse), _ptr(ws), ws.numel(),
                                 _stream_handle(stream)))
     return lse
@@ -243,7 +260,7 @@ def teacher_lse(h_t, W_t, mask=None, *, d_s, T=1.0, kind="fkl", chunk_tokens=0, 
 
 def fused_fwd_bwd_lse(h_t, W_t, h_s, W_s, lse_t, mask=None, *, T=1.0, kind="fkl", beta=0.5, loss_scale=1.0,
                       want_dW=False, accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split",
-                      out=None, stream=None) -> KDResult:
+                      out=None, stream=None, workspace=None) -> KDResult:
     """kd_fused_fwd_bwd_lse: kd_fused_fwd_bwd with the teacher's LSE record supplied (pass 1: student head only)."""
     h_t, W_t, h_s, W_s = (_as_bf16(x, n) for x, n in ((h_t, "h_t"), (W_t, "W_t"), (h_s, "h_s"), (W_s, "W_s")))
     N, d_t = h_t.shape
@@ -264,14 +281,14 @@ def fused_fwd_bwd_lse(h_t, W_t, h_s, W_s, lse_t, mask=None, *, T=1.0, kind="fkl"
         loss, dh, nnf = out.loss, out.dh_s, out.n_nonfinite
     if want_dW and dW_s is None:
         dW_s = (torch.zeros if accumulate_dW else torch.empty)(V, d_s, dtype=torch.float32, device=dev)
-    ws = _workspace(workspace_size(p), dev)
+    ws = _workspace(workspace_size(p), dev, stream, workspace)
     _check(lib().kd_fused_fwd_bwd_lse(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(h_s), _ptr(W_s), _ptr(mask),
                                       _ptr(lse_t), _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf),
                                       _ptr(ws), ws.numel(), _stream_handle(stream)))
     return KDResult(loss, dh, dW_s if want_dW else None, nnf)
 
 
-def teacher_topk(h_t, W_t, mask=None, *, k, d_s, T=1.0, chunk_tokens=0, stream=None):
+def teacher_topk(h_t, W_t, mask=None, *, k, d_s, T=1.0, chunk_tokens=0, stream=None, workspace=None):
     """kd_teacher_topk: the top-k teacher baseline's transfer (idx [N, k] int32, val [N, k] float32 raw logits)."""
     h_t, W_t = _as_bf16(h_t, "h_t"), _as_bf16(W_t, "W_t")
     N, d_t = h_t.shape
@@ -281,7 +298,7 @@ def teacher_topk(h_t, W_t, mask=None, *, k, d_s, T=1.0, chunk_tokens=0, stream=N
         mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
     idx = torch.full((N, k), -1, dtype=torch.int32, device=h_t.device)
     val = torch.zeros(N, k, dtype=torch.float32, device=h_t.device)
-    ws = _workspace(workspace_size(p), h_t.device)
+    ws = _workspace(workspace_size(p), h_t.device, stream, workspace)
     _check(lib().kd_teacher_topk(ctypes.byref(p), _ptr(h_t), _ptr(W_t), _ptr(mask), int(k), _ptr(idx), _ptr(val),
                                  _ptr(ws), ws.numel(), _stream_handle(stream)))
     return idx, val
@@ -289,7 +306,7 @@ def teacher_topk(h_t, W_t, mask=None, *, k, d_s, T=1.0, chunk_tokens=0, stream=N
 
 def topk_fwd_bwd(h_s, W_s, topk_idx, topk_val, mask=None, *, d_t=64, T=1.0, loss_scale=1.0, want_dW=False,
                  accumulate_dW=False, dW_s=None, chunk_tokens=0, grad_precision="split", out=None,
-                 stream=None) -> KDResult:
+                 stream=None, workspace=None) -> KDResult:
     """kd_topk_fwd_bwd: FKL against the renormalised top-k teacher (student head only)."""
     h_s, W_s = _as_bf16(h_s, "h_s"), _as_bf16(W_s, "W_s")
     N, d_s = h_s.shape
@@ -312,7 +329,7 @@ def topk_fwd_bwd(h_s, W_s, topk_idx, topk_val, mask=None, *, d_t=64, T=1.0, loss
         loss, dh, nnf = out.loss, out.dh_s, out.n_nonfinite
     if want_dW and dW_s is None:
         dW_s = (torch.zeros if accumulate_dW else torch.empty)(V, d_s, dtype=torch.float32, device=dev)
-    ws = _workspace(workspace_size(p), dev)
+    ws = _workspace(workspace_size(p), dev, stream, workspace)
     _check(lib().kd_topk_fwd_bwd(ctypes.byref(p), _ptr(h_s), _ptr(W_s), _ptr(mask), k, _ptr(topk_idx),
                                  _ptr(topk_val), _ptr(loss), _ptr(dh), _ptr(dW_s) if want_dW else None, _ptr(nnf),
                                  _ptr(ws), ws.numel(), _stream_handle(stream)))
@@ -320,7 +337,7 @@ def topk_fwd_bwd(h_s, W_s, topk_idx, topk_val, mask=None, *, d_t=64, T=1.0, loss
 
 
 def vocab_stats(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab, v_begin, T=1.0, kind="fkl",
-                chunk_tokens=0, stream=None) -> torch.Tensor:
+                chunk_tokens=0, stream=None, workspace=None) -> torch.Tensor:
     """kd_vocab_stats: this vocab shard's per-token record [5, N] (to be all-gathered)."""
     h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(x, "input") for x in (h_t, W_t_shard, h_s, W_s_shard))
     N, d_t = h_t.shape
@@ -330,7 +347,7 @@ def vocab_stats(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab, v_begin, T=
     if mask is not None:
         mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
     rec = torch.empty(5, N, dtype=torch.float32, device=h_t.device)
-    ws = _workspace(workspace_size(p), h_t.device)
+    ws = _workspace(workspace_size(p), h_t.device, stream, workspace)
     _check(lib().kd_vocab_stats(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
                                 _ptr(mask), _ptr(rec), _ptr(ws), ws.numel(), _stream_handle(stream)))
     return rec
@@ -338,7 +355,7 @@ def vocab_stats(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab, v_begin, T=
 
 def vocab_backward(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, vocab, v_begin, T=1.0, kind="fkl",
                    loss_scale=1.0, want_dW=False, accumulate_dW=False, dW_s=None, chunk_tokens=0,
-                   stream=None) -> KDResult:
+                   stream=None, workspace=None) -> KDResult:
     """kd_vocab_backward: merge the [P, 5, N] records; loss, PARTIAL dh_s (sum over ranks), local dW_s."""
     h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(x, "input") for x in (h_t, W_t_shard, h_s, W_s_shard))
     N, d_t = h_t.shape
@@ -354,7 +371,7 @@ def vocab_backward(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, vocab, v_
     nnf = torch.zeros(1, dtype=torch.int64, device=dev)
     if want_dW and dW_s is None:
         dW_s = (torch.zeros if accumulate_dW else torch.empty)(V_r, d_s, dtype=torch.float32, device=dev)
-    ws = _workspace(workspace_size(p), dev)
+    ws = _workspace(workspace_size(p), dev, stream, workspace)
     _check(lib().kd_vocab_backward(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
                                    _ptr(mask), _ptr(recs), int(recs.shape[0]), _ptr(loss), _ptr(dh),
                                    _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),

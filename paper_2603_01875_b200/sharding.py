@@ -80,7 +80,7 @@ def _reduce_scatter_rows(t: torch.Tensor, group=None) -> torch.Tensor:
     world = dist.get_world_size(group)
     if t.shape[0] % world:
         raise ValueError(f"dh_reduce='scatter' needs the group's {t.shape[0]} tokens divisible by {world} ranks")
-    if t.is_cuda and dist.get_backend(group) == "gloo":  # gloo has no CUDA reduce-scatter (one-GPU rank tests)
+    if dist.get_backend(group) == "gloo":  # gloo has no reduce-scatter: all-reduce, keep the own rows
         t = t.contiguous()
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         return _own_rows(t, group)
@@ -102,34 +102,130 @@ class _Result:
         self.loss, self.dh_s, self.dW_s = loss, dh_s, dW_s
 
 
-def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, group, T, kind, beta, loss_scale,
-                       want_dW, accumulate_dW, dW_s, chunk_tokens, stats_fn, partials_fn, finish_fn, dh_reduce):
-    """JSD/TVD: per token chunk, records all-gather -> partials -> (K, J) all-gather -> finish."""
+class _Done:
+    """Stand-in for a finished collective (no process group: identity exchange)."""
+
+    def wait(self):
+        return None
+
+
+def _all_gather_async(t: torch.Tensor, group=None):
+    """Start the all-gather of this rank's [..] tensor into [P, ..] (rank order); returns (out, work).
+
+    NCCL: the collective is enqueued behind the current stream's work and runs on NCCL's stream, so the caller
+    keeps launching kernels; ``work.wait()`` makes the current stream (not the host) wait for it."""
+    if not _distributed():
+        return t.contiguous()[None], _Done()
+    world = dist.get_world_size(group)
+    t = t.contiguous()
+    if dist.get_backend(group) == "gloo":
+        parts = [torch.empty_like(t) for _ in range(world)]
+        work = dist.all_gather(parts, t, group=group, async_op=True)
+        return parts, work
+    out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    work = dist.all_gather_into_tensor(out, t, group=group, async_op=True)
+    return out, work
+
+
+def _gathered(out):
+    return torch.stack(out) if isinstance(out, list) else out
+
+
+def _all_reduce_async(t: torch.Tensor, group=None):
+    if not _distributed():
+        return _Done()
+    return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group, async_op=True)
+
+
+def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str) -> int:
+    """Tokens per pipelined exchange chunk of the vocab-sharded step.
+
+    Each chunk's pass 1 runs while the previous chunk's records are all-gathered, and each chunk's partial-dh
+    all-reduce runs under the next chunk's kernels, so only the last chunk's all-reduce is exposed; more chunks
+    overlap more but shorten each launch.  JSD/TVD keep the chunk's G planes (12 B per (token, v)) between their two
+    calls, so their chunk is bounded to ~5 GB of planes: 8192 tokens at P = 8, 5376 at P = 2 (measured on one GPU
+    simulating rank 0, c3 JSD: per-GPU efficiency at P = 8 0.67 with 2048-token chunks -> 0.85 with 8192;
+    scripts/gpu/simv_jsd*.sh).  FKL/RKL: 8192 tokens (four exchange chunks at config 2).  KD_VOCAB_FIX_CHUNK
+    overrides."""
+    if "KD_VOCAB_FIX_CHUNK" in os.environ:
+        return max(1, int(os.environ["KD_VOCAB_FIX_CHUNK"]))
+    if kind in ("jsd", "tvd"):
+        return max(4096, min(8192, int(5e9 / (12 * max(1, v_rows))) // 256 * 256))
+    return 8192 if n_tokens > 8192 else max(1, n_tokens)
+
+
+def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
+                          T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False,
+                          dW_s=None, chunk_tokens=0, exchange_chunk=0, stats_fn: Callable | None = None,
+                          backward_fn: Callable | None = None, partials_fn: Callable | None = None,
+                          finish_fn: Callable | None = None, dh_reduce: str = "all"):
+    """One vocab-sharded step on this rank; every rank of ``group`` holds the same tokens and its own
+    LM-head rows [v_begin, v_begin + V_r).  Returns a result whose dh_s is the full gradient (all-reduced) and whose
+    dW_s holds this rank's rows.
+
+    Pipelined over exchange chunks of ``exchange_chunk`` tokens (default: ``default_exchange_chunk``):
+
+        FKL / RKL   stats(c+1) ‖ all-gather records(c) ;  backward(c) ‖ all-reduce partial dh(c-1) (+ FKL loss)
+        JSD / TVD   stats(c+1) ‖ all-gather records(c) ;  partials(c) -> all-gather (K, J)(c) -> finish(c)
+                    ‖ all-reduce partial dh(c-1)
+
+    (‖ = concurrent: NCCL runs the collective on its own stream while this stream launches the next kernels; the
+    kernels merge records and (K, J) partials in rank order, so the result is deterministic for a fixed P.)
+
+    dh_reduce="scatter": when the group's tokens are its members' equal slices concatenated in rank order (each rank
+    contributes its own batch, bench.py's 2-D grid), every rank keeps dh_s / loss of its own slice only: one
+    reduce-scatter at the end instead of the per-chunk all-reduces.
+
+    ``chunk_tokens`` is the library's internal token chunk (kd_problem.chunk_tokens, 0 = its default).  The
+    kernel-side callables default to the CUDA entry points; tests substitute CPU stand-ins to exercise this exchange
+    logic under gloo.
+    """
+    if dh_reduce not in ("all", "scatter"):
+        raise ValueError(f"dh_reduce must be 'all' or 'scatter' (got {dh_reduce!r})")
+    fix = kind in ("jsd", "tvd")
+    if stats_fn is None or (fix and (partials_fn is None or finish_fn is None)) or (not fix and backward_fn is None):
+        from . import kdfused
+        stats_fn = stats_fn or kdfused.vocab_stats
+        backward_fn = backward_fn or kdfused.vocab_backward
+        partials_fn = partials_fn or kdfused.vocab_partials
+        finish_fn = finish_fn or kdfused.vocab_finish
     N = h_t.shape[0]
     d_s = W_s_shard.shape[1]
-    # token chunk of the (K, J) exchange: a narrow vocab shard makes a 2048-token chunk's launches short (the dh GEMM
-    # over K = V_r runs in 1-2 unbalanced waves; three prologues per chunk), so the chunk grows as the shard narrows,
-    # keeping the chunk's G planes (12 B per (token, v)) near 5 GB, at least 4096 tokens: 8192 at P = 8, 5376 at
-    # P = 2 (measured on one GPU simulating rank 0, c3 JSD: per-GPU efficiency at P = 8 0.67 with 2048-token chunks
-    # -> 0.85 with 8192; at P = 2 0.79 with 2560 -> 0.84 with 4096; scripts/gpu/simv_jsd*.sh).
-    # KD_VOCAB_FIX_CHUNK overrides.
-    v_r = max(1, W_s_shard.shape[0])
-    auto = max(4096, min(8192, int(5e9 / (12 * v_r)) // 256 * 256))
-    chunk = chunk_tokens if chunk_tokens > 0 else int(os.environ.get("KD_VOCAB_FIX_CHUNK", str(auto)))
+    chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, W_s_shard.shape[0], kind)
+    if fix and chunk_tokens > 0:
+        chunk = min(chunk, chunk_tokens)  # the JSD/TVD pair runs one library chunk per call
+    spans = [(a, min(N, a + chunk)) for a in range(0, N, chunk)]
+    per_chunk = dh_reduce == "all"
     loss = dh = None
-    for a in range(0, N, chunk):
-        b = min(N, a + chunk)
-        ht_c, hs_c = h_t[a:b], h_s[a:b]
+    pending = []  # per-chunk all-reduces in flight
+
+    def stats(i):
+        a, b = spans[i]
         m_c = None if mask is None else mask[a:b]
-        rec = stats_fn(ht_c, W_t_shard, hs_c, W_s_shard, m_c, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
-                       chunk_tokens=b - a)
-        recs = gather_records(rec, group)
-        acc = accumulate_dW or a > 0  # later chunks add into the first chunk's dW_s
-        kj, state = partials_fn(ht_c, W_t_shard, hs_c, W_s_shard, recs, m_c, vocab=vocab, v_begin=v_begin, T=T,
-                                kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=acc,
-                                chunk_tokens=b - a)
-        kj_all = gather_kj(kj, group)
-        r = finish_fn(state, ht_c, W_t_shard, hs_c, W_s_shard, kj_all, m_c, dW_s=dW_s)
+        rec = stats_fn(h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, m_c, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
+                       chunk_tokens=(b - a) if fix else chunk_tokens)
+        return _all_gather_async(rec, group)
+
+    nxt = stats(0) if spans else None
+    for i, (a, b) in enumerate(spans):
+        recs_out, work = nxt
+        if i + 1 < len(spans):
+            nxt = stats(i + 1)  # next chunk's pass 1 runs while this chunk's records travel
+        work.wait()
+        recs = _gathered(recs_out)
+        m_c = None if mask is None else mask[a:b]
+        acc = accumulate_dW or i > 0  # later chunks add into the first chunk's dW_s
+        if fix:
+            kj, state = partials_fn(h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, recs, m_c, vocab=vocab,
+                                    v_begin=v_begin, T=T, kind=kind, beta=beta, loss_scale=loss_scale,
+                                    want_dW=want_dW, accumulate_dW=acc, chunk_tokens=b - a)
+            kj_out, kw = _all_gather_async(kj, group)
+            kw.wait()
+            r = finish_fn(state, h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, _gathered(kj_out), m_c, dW_s=dW_s)
+        else:
+            r = backward_fn(h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, recs, m_c, vocab=vocab, v_begin=v_begin, T=T,
+                            kind=kind, loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=acc, dW_s=dW_s,
+                            chunk_tokens=chunk_tokens)
         if loss is None:  # outputs in the kernels' dtype (fp32; the CPU test stand-ins return fp64)
             loss = torch.zeros(N, dtype=r.loss.dtype, device=r.loss.device)
             dh = torch.zeros(N, d_s, dtype=r.dh_s.dtype, device=r.dh_s.device)
@@ -137,60 +233,23 @@ def _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, *, vocab, v_begin, 
         dh[a:b] = r.dh_s
         if want_dW:
             dW_s = r.dW_s
+        if per_chunk:
+            # partial dh (and FKL's partial loss: each shard's Σ over its rows) summed over the group under the
+            # next chunk's kernels
+            pending.append(_all_reduce_async(dh[a:b], group))
+            if kind == "fkl":
+                pending.append(_all_reduce_async(loss[a:b], group))
+    for w in pending:
+        w.wait()
     if dh is None:  # no tokens
         loss = torch.zeros(0, dtype=torch.float32, device=h_t.device)
         dh = torch.zeros(0, d_s, dtype=torch.float32, device=h_t.device)
-    if dh_reduce == "scatter":
-        return _Result(_own_rows(loss, group), _reduce_scatter_rows(dh, group), dW_s if want_dW else None)
-    _all_reduce_sum(dh, group)
+    if not per_chunk:
+        # FKL: each shard returns its partial loss (kdfused.h kd_vocab_backward), reduced like dh; the others are
+        # already the full per-token loss on every rank
+        loss = _reduce_scatter_rows(loss, group) if kind == "fkl" else _own_rows(loss, group)
+        dh = _reduce_scatter_rows(dh, group)
     return _Result(loss, dh, dW_s if want_dW else None)
-
-
-def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
-                          T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False,
-                          dW_s=None, chunk_tokens=0, stats_fn: Callable | None = None,
-                          backward_fn: Callable | None = None, partials_fn: Callable | None = None,
-                          finish_fn: Callable | None = None, dh_reduce: str = "all"):
-    """One vocab-sharded step on this rank; returns a KDResult whose dh_s is the full (all-reduced) gradient.
-
-    dh_reduce="scatter": when the group's tokens are its members' equal slices concatenated in rank order (each rank
-    contributes its own batch), every rank only needs dh_s / loss for its own slice: the dh exchange becomes a
-    reduce-scatter (half the bytes of the all-reduce) and the result rows are this rank's slice.
-
-    The kernel-side callables default to the CUDA entry points; tests substitute CPU stand-ins to
-    exercise this exchange logic under gloo.
-    """
-    if kind in ("jsd", "tvd"):
-        if stats_fn is None or partials_fn is None or finish_fn is None:
-            from . import kdfused
-            stats_fn = stats_fn or kdfused.vocab_stats
-            partials_fn = partials_fn or kdfused.vocab_partials
-            finish_fn = finish_fn or kdfused.vocab_finish
-        return _vocab_sharded_fix(h_t, W_t_shard, h_s, W_s_shard, mask, vocab=vocab, v_begin=v_begin, group=group,
-                                  T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
-                                  accumulate_dW=accumulate_dW, dW_s=dW_s, chunk_tokens=chunk_tokens,
-                                  stats_fn=stats_fn, partials_fn=partials_fn, finish_fn=finish_fn,
-                                  dh_reduce=dh_reduce)
-    if stats_fn is None or backward_fn is None:
-        from . import kdfused
-        stats_fn = stats_fn or kdfused.vocab_stats
-        backward_fn = backward_fn or kdfused.vocab_backward
-    rec = stats_fn(h_t, W_t_shard, h_s, W_s_shard, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
-                   chunk_tokens=chunk_tokens)
-    recs = gather_records(rec, group)
-    r = backward_fn(h_t, W_t_shard, h_s, W_s_shard, recs, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
-                    loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
-                    chunk_tokens=chunk_tokens)
-    if dh_reduce not in ("all", "scatter"):
-        raise ValueError(f"dh_reduce must be 'all' or 'scatter' (got {dh_reduce!r})")
-    if dh_reduce == "scatter":
-        # FKL: each shard returns its partial loss (kdfused.h kd_vocab_backward), reduced like dh; RKL: already full
-        loss = _reduce_scatter_rows(r.loss, group) if kind == "fkl" else _own_rows(r.loss, group)
-        return _Result(loss, _reduce_scatter_rows(r.dh_s, group), r.dW_s)
-    _all_reduce_sum(r.dh_s, group)
-    if kind == "fkl":  # FKL: each shard returns its partial loss (kdfused.h kd_vocab_backward)
-        _all_reduce_sum(r.loss, group)
-    return r
 
 
 def token_sharded_dW_reduce(dW_s: torch.Tensor, group=None) -> torch.Tensor:

@@ -60,68 +60,33 @@ def assert_kd_close(name, got, ref, rtol, atol, max_report=5):
                              f"max|d| = {np.abs(got - ref).max():.3e}; first: {details}")
 
 
-STRICT_FRACTION_MAX = 1e-5  # strict element-wise violations tolerated (ill-conditioned elements only)
+def assert_grad_close(name, got, ref, rtol=GRAD_RTOL, atol=GRAD_ATOL, allow=0, max_ratio=1.0):
+    """Gradient parity at the BASELINE.json north_star tolerance, element by element: |Δ| <= rtol·|ref| + atol.
 
-# Scale of the fp32 accumulation error of tcgen05 LM-head logits (K = 4096, bf16 operands), measured on B200 by
-# scripts/probe_accum.py: rms 5.6e-6, max 6.3e-5 over 256 x 151936 logits (K fed last-to-first, as kd_pass does).
-LOGIT_SIGMA = 2e-5
-FLOOR_SIGMAS = 6.0
-FLOOR_DRAWS = 6
-
-
-def oracle_grad_floor(inp, *, T, kind, beta=0.5, loss_scale=1.0, want_dW=False, rows=None, seed=1234):
-    """1-sigma spread of the ORACLE's dh_s (and dW_s) when its logits carry independent N(0, LOGIT_SIGMA²)
-    errors — the conditioning floor of the arithmetic the north star prescribes (bf16 tensor-core GEMM, fp32
-    accumulate).  Computed with oracle functions only (reading R14)."""
-    from oracle.kd_oracle import kd_loss_from_logits, lm_head_logits
-    ht, hs = f64(inp.H_t), f64(inp.H_s)
-    mask = inp.mask
-    if rows is not None:
-        ht, hs = ht[rows], hs[rows]
-        mask = None if mask is None else mask[rows]
-    Wt, Ws = f64(inp.W_t), f64(inp.W_s)
-    live = np.arange(ht.shape[0]) if mask is None else np.flatnonzero(mask)
-    dh_var = np.zeros((ht.shape[0], Ws.shape[1]))
-    dW_var = np.zeros_like(Ws) if want_dW else None
-    rng = np.random.default_rng(seed)
-    for i in range(0, live.size, 64):
-        r = live[i:i + 64]
-        z_t, z_s = lm_head_logits(ht[r], Wt), lm_head_logits(hs[r], Ws)
-        _, G = kd_loss_from_logits(z_t, z_s, T=T, kind=kind, beta=beta, loss_scale=loss_scale)
-        for _ in range(FLOOR_DRAWS):
-            _, Gk = kd_loss_from_logits(z_t + LOGIT_SIGMA * rng.standard_normal(z_t.shape),
-                                        z_s + LOGIT_SIGMA * rng.standard_normal(z_s.shape),
-                                        T=T, kind=kind, beta=beta, loss_scale=loss_scale)
-            D = Gk - G
-            dh_var[r] += (D @ Ws) ** 2 / FLOOR_DRAWS
-            if want_dW:
-                dW_var += (D.T @ hs[r]) ** 2 / FLOOR_DRAWS
-    return np.sqrt(dh_var), (np.sqrt(dW_var) if want_dW else None)
-
-
-def assert_grad_close(name, got, ref, floor=None, rtol=GRAD_RTOL, atol=GRAD_ATOL):
-    """Gradient parity (BASELINE.json north_star tolerance + DESIGN.md reading R14).
-
-    Every element: |Δ| <= rtol·|ref| + atol + FLOOR_SIGMAS·floor, where floor is the oracle's own 1-sigma
-    sensitivity to the measured tcgen05 logit-accumulation error (oracle_grad_floor; ~0 for well-conditioned
-    elements, it only matters where the result is far smaller than its terms — e.g. the Zipf-bias column).
-    And the strict north-star form |Δ| <= rtol·|ref| + atol must hold for all but a 1e-5 fraction of elements.
-    Returns the number of strict violations.
-    """
+    Fails closed.  ``allow`` / ``max_ratio`` name, per test, the ONLY exception DESIGN.md reading R14 admits: at most
+    ``allow`` elements may exceed the bound, each by at most ``max_ratio`` × (rtol·|ref| + atol).  They are the
+    ill-conditioned elements (results ~100x smaller than their terms, e.g. the Zipf-bias column of dh_s) where the
+    prescribed arithmetic — bf16 tensor-core GEMMs with fp32 accumulation over K = d_t = 4096 — is itself outside the
+    bound (scripts/probe_parity_src.py: tcgen05 logit error up to 1.7e-4 at K = 4096, proportional to the steps per
+    accumulator).  Every such element is printed and logged (KD_PARITY_LOG); the default (allow = 0) is strict.
+    Returns the number of elements beyond the plain bound."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, (name, got.shape, ref.shape)
     d = np.abs(got - ref)
-    strict_tol = atol + rtol * np.abs(ref)
-    tol = strict_tol + (0.0 if floor is None else FLOOR_SIGMAS * np.asarray(floor))
-    bad = d > tol
+    tol = atol + rtol * np.abs(ref)
+    ratio = d / tol
+    bad = ~(ratio <= 1.0)  # NaN counts as a violation
+    _parity_log(name, got, ref, tol, False, int(bad.sum()))
     if bad.any():
-        idx = np.argwhere(bad)[:5]
-        raise AssertionError(f"{name}: {bad.sum()} / {bad.size} elements outside |d| <= {atol} + {rtol}|ref| + "
-                             f"{FLOOR_SIGMAS}*floor; first: "
-                             f"{[(tuple(i), float(got[tuple(i)]), float(ref[tuple(i)])) for i in idx]}")
-    strict = d > strict_tol
-    _parity_log(name, got, ref, strict_tol, floor is not None, int(strict.sum()))
-    frac = strict.mean()
-    assert frac <= STRICT_FRACTION_MAX, f"{name}: strict element-wise violations {strict.sum()} ({frac:.2e})"
-    return int(strict.sum())
+        idx = np.argwhere(bad)
+        order = np.argsort(-np.nan_to_num(ratio[bad], nan=np.inf))
+        listed = [(tuple(int(x) for x in idx[i]), float(got[tuple(idx[i])]), float(ref[tuple(idx[i])]),
+                   float(ratio[tuple(idx[i])])) for i in order[:20]]
+        print(f"[parity] {name}: {int(bad.sum())} element(s) beyond |d| <= {atol} + {rtol}|ref| "
+              f"(allowed {allow} up to {max_ratio}x): {listed}")
+        worst = float(np.nan_to_num(ratio, nan=np.inf).max())
+        assert int(bad.sum()) <= allow and worst <= max_ratio, (
+            f"{name}: {int(bad.sum())} / {bad.size} elements outside |d| <= {atol} + {rtol}|ref| "
+            f"(worst {worst:.3f}x; allowed {allow} element(s) up to {max_ratio}x); worst first: {listed[:5]}")
+    return int(bad.sum())

@@ -10,7 +10,7 @@ import torch
 
 import kd_inputs as KI
 from tests.kdtest_util import (GRAD_ATOL, GRAD_RTOL, LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close,
-                               dev_bf16, f64, oracle_grad_floor, oracle_run)
+                               dev_bf16, f64, oracle_run)
 
 pytestmark = pytest.mark.gpu
 
@@ -46,11 +46,10 @@ def run(inp, mask=None, **kw):
 
 def _sampled_check(inp, r, rows, *, T, kind, beta=0.5):
     loss, dh, _ = oracle_run(inp, T=T, kind=kind, beta=beta, rows=rows)
-    fl, _ = oracle_grad_floor(inp, T=T, kind=kind, beta=beta, rows=rows)
     got_loss = r.loss.cpu().numpy()[rows]
     got_dh = r.dh_s.cpu().numpy()[rows]
     assert_kd_close("loss", got_loss, loss, LOSS_RTOL, LOSS_ATOL)
-    assert_grad_close("dh_s", got_dh, dh, fl)
+    assert_grad_close("dh_s", got_dh, dh)
 
 
 # ------------------------------------------------------------------ full sizes, bench launch configuration
@@ -89,6 +88,14 @@ def test_config3_full_size_masked_sampled(name):
         assert np.all(r.loss.cpu().numpy() <= np.log(2) + 1e-5)
 
 
+# The only elements allowed beyond the plain north-star bound (R14, tests/kdtest_util.assert_grad_close):
+# (allowed count, max ratio) per (config, output), from the committed parity record (profiles/r02_parity.md).  They are
+# logit-accuracy-limited elements of fp32-accumulated K = d_t bf16 GEMMs (scripts/probe_parity_src.py); every other
+# element of these runs — and every element of every other test — meets the plain bound.
+R14_ALLOW = {("c2", "dh_s"): (1, 1.7), ("c2", "dW_s"): (3, 1.15), ("c4", "dW_s"): (1, 1.05),
+             ("c3_rkl", "dW_s"): (2, 1.25)}
+
+
 @pytest.mark.parametrize("cfg_name,n", [("c2", 512), ("c4", 512), ("c3_rkl", 384)])
 def test_reduced_n_full_vocab_with_dW(cfg_name, n):
     """Config shapes at N=512 (full V, full d) including dW_s over all rows."""
@@ -98,10 +105,10 @@ def test_reduced_n_full_vocab_with_dW(cfg_name, n):
     inp = KI.KDInputs(H_t, W_t, H_s, W_s, None)
     r = run(inp, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, want_dW=True)
     loss, dh, dW = oracle_run(inp, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, want_dW=True)
-    fh, fW = oracle_grad_floor(inp, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, want_dW=True)
     assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
-    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh, fh)
-    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW, fW)
+    for name, got, ref in (("dh_s", r.dh_s, dh), ("dW_s", r.dW_s, dW)):
+        allow, mr = R14_ALLOW.get((cfg_name, name), (0, 1.0))
+        assert_grad_close(name, got.cpu().numpy(), ref, allow=allow, max_ratio=mr)
 
 
 def test_config5_ragged_accumulate_dW():
@@ -123,9 +130,8 @@ def test_config5_ragged_accumulate_dW():
     whole = kd().fused_fwd_bwd(Ht, Wt, Hs, Ws, m, T=1.0, kind="rkl", want_dW=True, chunk_tokens=256)
     torch.cuda.synchronize()
     _, _, dW_ref = oracle_run(inp, T=1.0, kind="rkl", want_dW=True)
-    _, fW = oracle_grad_floor(inp, T=1.0, kind="rkl", want_dW=True)
-    assert_grad_close("dW accumulated", dW.cpu().numpy(), dW_ref, fW)
-    assert_grad_close("dW whole", whole.dW_s.cpu().numpy(), dW_ref, fW)
+    assert_grad_close("dW accumulated", dW.cpu().numpy(), dW_ref)
+    assert_grad_close("dW whole", whole.dW_s.cpu().numpy(), dW_ref)
 
 
 # ------------------------------------------------------------------ edge cases
@@ -345,9 +351,8 @@ def test_vocab_sharded_jsd_tvd_equals_single(P, kind, chunk):
 def test_grad_precision_bf16_within_its_bound(kind):
     """KD_GRAD_BF16 (one bf16 G plane, kdfused.h): not parity-grade, so it is held to its own rounding bound.
     Each G entry is rounded once to bf16 (|δ_v| <= 2^-8 |g_v|, the unit roundoff; the residual fix restores the largest exactly),
-    so |Δdh_j| <= 2^-8 (|G|·|W_s|)_j and |ΔdW_vj| <= 2^-8 (|G|ᵀ·|H_s|)_vj, plus the north-star terms and the
-    R14 floor for the fp32 accumulation the split path also has.  The loss does not depend on G: it must stay
-    within the north-star loss tolerance."""
+    so |Δdh_j| <= 2^-8 (|G|·|W_s|)_j and |ΔdW_vj| <= 2^-8 (|G|ᵀ·|H_s|)_vj, plus the north-star terms.  The loss does
+    not depend on G: it must stay within the north-star loss tolerance."""
     from oracle.kd_oracle import grad_student_logits, lm_head_logits
     cfg = KI.CONFIGS["c2"]
     W_t, W_s = heads(cfg.vocab, cfg.d_t, cfg.d_s)
@@ -357,19 +362,18 @@ def test_grad_precision_bf16_within_its_bound(kind):
     T = 2.0 if kind != "fkl" else 1.0
     r = run(inp, T=T, kind=kind, want_dW=True, grad_precision="bf16")
     loss, dh, dW = oracle_run(inp, T=T, kind=kind, want_dW=True)
-    fh, fW = oracle_grad_floor(inp, T=T, kind=kind, want_dW=True)
     Ws64, Hs64 = f64(W_s), f64(H_s)
     G = grad_student_logits(kind, lm_head_logits(f64(H_t), f64(W_t)), lm_head_logits(Hs64, Ws64), T, 0.5)
     bh = 2.0 ** -8 * (np.abs(G) @ np.abs(Ws64))
     bW = 2.0 ** -8 * (np.abs(G).T @ np.abs(Hs64))
     assert_kd_close("loss (bf16 G)", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
-    for name, got, ref, fl, b in (("dh_s (bf16 G)", r.dh_s, dh, fh, bh), ("dW_s (bf16 G)", r.dW_s, dW, fW, bW)):
+    for name, got, ref, b in (("dh_s (bf16 G)", r.dh_s, dh, bh), ("dW_s (bf16 G)", r.dW_s, dW, bW)):
         got = got.cpu().numpy().astype(np.float64)
         d = np.abs(got - ref)
-        tol = b + GRAD_ATOL + GRAD_RTOL * np.abs(ref) + 6 * fl
+        tol = b + GRAD_ATOL + GRAD_RTOL * np.abs(ref)
         i = np.unravel_index(np.argmax(d / tol), d.shape)
         assert np.all(d <= tol), (name, float((d / tol).max()), i, float(got[i]), float(ref[i]), float(b[i]),
-                                  float(fl[i]), int((d > tol).sum()))
+                                  int((d > tol).sum()))
     # and it is a real approximation: measurably worse than the split planes somewhere, never better by design
     r2 = run(inp, T=T, kind=kind, want_dW=True)
     e_fast = np.abs(r.dh_s.cpu().numpy() - dh).max()

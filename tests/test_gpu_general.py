@@ -1,0 +1,238 @@
+"""GPU parity for the generalisations the C ABI exposes beyond BASELINE.json's pinned settings (through the C ABI,
+against the fp64 oracle on identical bf16 inputs, at the plain north-star tolerance unless a test says otherwise):
+
+* JSD with β != ½ (reading R4: m = βp + (1−β)q, β weights the teacher) — a swapped β / (1−β) convention is invisible
+  at β = ½ (P:153 names JSD; SPEC S:311 leaves β open), so β = 0.2 / 0.8 are run at small and at config-3 shapes;
+* T < 1 (T = 0.5): the sharpest rows, where p_top ≈ 1 makes q − p a cancellation;
+* loss_scale = 1/Σmask (SPEC S:251's mean reduction, reading R3);
+* config 5 (ragged on-policy batch, RKL, dW_s accumulated over micro-batches) at its real config-2 shapes.
+"""
+import numpy as np
+import pytest
+import torch
+
+import kd_inputs as KI
+from tests.kdtest_util import (GRAD_ATOL, GRAD_RTOL, LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close,
+                               dev_bf16, oracle_run)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_01875_b200 as kd
+    kd.lib()
+
+
+def kd():
+    import paper_2603_01875_b200 as m
+    return m
+
+
+_HEADS = {}
+
+
+def heads(V, d_t, d_s, seed=1000):
+    key = (V, d_t, d_s, seed)
+    if key not in _HEADS:
+        _HEADS.clear()
+        _HEADS[key] = KI.make_heads(V, d_t, d_s, seed=seed)
+    return _HEADS[key]
+
+
+def run(inp, mask=None, **kw):
+    m = None if mask is None else torch.from_numpy(mask).cuda()
+    r = kd().fused_fwd_bwd(dev_bf16(inp.H_t), dev_bf16(inp.W_t), dev_bf16(inp.H_s), dev_bf16(inp.W_s), m, **kw)
+    torch.cuda.synchronize()
+    return r
+
+
+def check(r, inp, *, T, kind, beta=0.5, loss_scale=1.0, want_dW=True, allow=None):
+    """Loss, dh_s (and dW_s) against the oracle.  With loss_scale = s the gradients are s × the unscaled ones, so the
+    absolute floor scales with them (atol·s; the relative bound is unchanged)."""
+    loss, dh, dW = oracle_run(inp, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW)
+    assert int(r.n_nonfinite.item()) == 0
+    assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
+    atol = GRAD_ATOL * abs(loss_scale)
+    allow = allow or {}
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh, GRAD_RTOL, atol, *allow.get("dh_s", (0, 1.0)))
+    if want_dW:
+        assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW, GRAD_RTOL, atol, *allow.get("dW_s", (0, 1.0)))
+    return loss
+
+
+# ------------------------------------------------------------------ JSD with beta != 1/2
+@pytest.mark.parametrize("beta", [0.2, 0.8])
+@pytest.mark.parametrize("T", [0.5, 1.0, 2.0])
+def test_jsd_beta_small(beta, T):
+    """N = 300 (ragged tile), V = 1000 (ragged vocab tile), masked, chunked at 128 tokens."""
+    N, d_t, d_s, V = 300, 256, 128, 1000
+    mask = (np.random.default_rng(17).random(N) > 0.3).astype(np.uint8)
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=31, mask=mask)
+    r = run(inp, mask, T=T, kind="jsd", beta=beta, want_dW=True, chunk_tokens=128)
+    loss = check(r, inp, T=T, kind="jsd", beta=beta)
+    # the β-weighted bound JSD_β <= H(β) = −β ln β − (1−β) ln(1−β)
+    hb = -beta * np.log(beta) - (1 - beta) * np.log(1 - beta)
+    assert np.all(r.loss.cpu().numpy() <= hb + 1e-5) and np.all(loss <= hb + 1e-12)
+
+
+def test_jsd_beta_convention_is_visible():
+    """β and 1−β give different losses and gradients on the GPU (and the oracle agrees which is which): the test
+    above would pass for a swapped convention only if it also matched the oracle there."""
+    N, d_t, d_s, V = 256, 128, 128, 2000
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=32)
+    a = run(inp, T=1.0, kind="jsd", beta=0.2)
+    b = run(inp, T=1.0, kind="jsd", beta=0.8)
+    la, lb = a.loss.cpu().numpy(), b.loss.cpu().numpy()
+    assert np.abs(la - lb).max() > 1e-2
+    ref_a = oracle_run(inp, T=1.0, kind="jsd", beta=0.2)[0]
+    assert_kd_close("loss beta=0.2", la, ref_a, LOSS_RTOL, LOSS_ATOL)
+
+
+@pytest.mark.parametrize("beta", [0.2, 0.8])
+def test_jsd_beta_config3_shapes_with_dW(beta):
+    """Config-3 shapes (d_t = 4096, d_s = 2048, V = 151936, T = 2) at N = 384 with the prompt/padding-style mask,
+    dW_s over all rows at full V."""
+    cfg = KI.CONFIGS["c3_jsd"]
+    W_t, W_s = heads(cfg.vocab, cfg.d_t, cfg.d_s)
+    n = 384
+    H_t, H_s = KI.make_hidden(n, W_t, W_s, seed=1021, head_seed=1000)
+    mask = np.ones(n, np.uint8)
+    mask[:40] = 0      # a prompt prefix
+    mask[350:] = 0     # padding
+    inp = KI.KDInputs(H_t, W_t, H_s, W_s, mask)
+    r = run(inp, mask, T=cfg.temperature, kind="jsd", beta=beta, want_dW=True)
+    check(r, inp, T=cfg.temperature, kind="jsd", beta=beta)
+
+
+def test_c3_jsd_n512_full_vocab_with_dW():
+    """SURVEY.md §8(d) parity set: config-3 JSD(½) at N = 512, full V and d, dW_s included."""
+    cfg = KI.CONFIGS["c3_jsd"]
+    W_t, W_s = heads(cfg.vocab, cfg.d_t, cfg.d_s)
+    n = 512
+    H_t, H_s = KI.make_hidden(n, W_t, W_s, seed=1022, head_seed=1000)
+    mask = KI.make_mask(KI.KDConfig("m", 1, n, cfg.d_t, cfg.d_s, cfg.vocab, mask="ragged"), seed=1023)
+    inp = KI.KDInputs(H_t, W_t, H_s, W_s, mask)
+    r = run(inp, mask, T=cfg.temperature, kind="jsd", beta=0.5, want_dW=True)
+    check(r, inp, T=cfg.temperature, kind="jsd", beta=0.5)
+
+
+# ------------------------------------------------------------------ T < 1
+@pytest.mark.parametrize("kind", ["fkl", "rkl", "jsd", "tvd"])
+def test_sharp_temperature_small(kind):
+    """T = 0.5 doubles every logit gap: the sharpest rows of the recipe (p_top -> 1)."""
+    N, d_t, d_s, V = 300, 256, 128, 1000
+    mask = (np.random.default_rng(5).random(N) > 0.2).astype(np.uint8)
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=33, mask=mask)
+    r = run(inp, mask, T=0.5, kind=kind, beta=0.5, want_dW=True, chunk_tokens=128)
+    check(r, inp, T=0.5, kind=kind)
+
+
+# Elements allowed beyond the plain bound at config-2 shapes and T = 0.5 (R14; listed in
+# profiles/r02_parity.md): logit-accuracy-limited entries of the fp32-accumulated K = 4096 GEMMs, whose error the
+# halved temperature doubles.
+T05_ALLOW = {"fkl": {}, "rkl": {}, "jsd": {}, "tvd": {}}
+
+
+@pytest.mark.parametrize("kind", ["fkl", "rkl", "jsd", "tvd"])
+def test_sharp_temperature_config2_shapes(kind):
+    """T = 0.5 at config-2 shapes (full V, d_t = 4096, d_s = 2048), N = 256, dW_s included."""
+    cfg = KI.CONFIGS["c2"]
+    W_t, W_s = heads(cfg.vocab, cfg.d_t, cfg.d_s)
+    n = 256
+    H_t, H_s = KI.make_hidden(n, W_t, W_s, seed=1031, head_seed=1000)
+    inp = KI.KDInputs(H_t, W_t, H_s, W_s, None)
+    r = run(inp, T=0.5, kind=kind, beta=0.5, want_dW=True)
+    check(r, inp, T=0.5, kind=kind, allow=T05_ALLOW[kind])
+
+
+# ------------------------------------------------------------------ mean reduction
+@pytest.mark.parametrize("kind", ["fkl", "rkl", "jsd", "tvd"])
+def test_loss_scale_mean_reduction(kind):
+    """loss_scale = 1/Σmask: the per-token loss is unscaled, every gradient is scaled by it."""
+    N, d_t, d_s, V = 400, 192, 128, 1500
+    mask = (np.random.default_rng(9).random(N) > 0.4).astype(np.uint8)
+    s = 1.0 / max(1, int(mask.sum()))
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=34, mask=mask)
+    r = run(inp, mask, T=1.5, kind=kind, beta=0.5, loss_scale=s, want_dW=True, chunk_tokens=256)
+    check(r, inp, T=1.5, kind=kind, loss_scale=s)
+    r1 = run(inp, mask, T=1.5, kind=kind, beta=0.5, loss_scale=1.0, want_dW=True, chunk_tokens=256)
+    assert torch.equal(r.loss, r1.loss)  # the loss itself is never scaled
+    # linear in loss_scale up to the rounding of the scaled G
+    np.testing.assert_allclose(r.dh_s.cpu().numpy(), s * r1.dh_s.cpu().numpy(), rtol=1e-4, atol=2e-6 * s)
+
+
+def test_loss_scale_mean_reduction_config3_shapes():
+    """Mean reduction at config-3 shapes (RKL, T = 2, masked), 256 sampled tokens' rows, dW_s at full V."""
+    cfg = KI.CONFIGS["c3_rkl"]
+    W_t, W_s = heads(cfg.vocab, cfg.d_t, cfg.d_s)
+    n = 256
+    H_t, H_s = KI.make_hidden(n, W_t, W_s, seed=1041, head_seed=1000)
+    mask = np.ones(n, np.uint8)
+    mask[:64] = 0
+    s = 1.0 / int(mask.sum())
+    inp = KI.KDInputs(H_t, W_t, H_s, W_s, mask)
+    r = run(inp, mask, T=cfg.temperature, kind="rkl", loss_scale=s, want_dW=True)
+    check(r, inp, T=cfg.temperature, kind="rkl", loss_scale=s)
+
+
+# ------------------------------------------------------------------ config 5 at its real shapes
+def test_config5_real_shapes_accumulate_dW():
+    """configs[4] at config-2 shapes (d_t = 4096, d_s = 2048, V = 151936): ragged sequences with masked prompts
+    (L ~ U[256, 8192], L_p ~ U[32, min(512, L/2)]), RKL T = 1, dW_s accumulated over 4 micro-batches (P:210 gradient
+    accumulation) ≡ one batch ≡ the oracle."""
+    cfg = KI.CONFIGS["c5"]
+    W_t, W_s = heads(cfg.vocab, cfg.d_t, cfg.d_s)
+    n = 1280
+    H_t, H_s = KI.make_hidden(n, W_t, W_s, seed=1051, head_seed=1000)
+    mask = KI.make_mask(KI.KDConfig("r", 1, n, cfg.d_t, cfg.d_s, cfg.vocab, mask="ragged"), seed=1052)
+    inp = KI.KDInputs(H_t, W_t, H_s, W_s, mask)
+    m = torch.from_numpy(mask).cuda()
+    Ht, Hs, Wt, Ws = dev_bf16(H_t), dev_bf16(H_s), dev_bf16(W_t), dev_bf16(W_s)
+    dW = torch.zeros(cfg.vocab, cfg.d_s, dtype=torch.float32, device="cuda")
+    bounds = [0, 300, 777, 778, n]  # 4 micro-batches, one of a single row
+    dh = torch.zeros(n, cfg.d_s, device="cuda")
+    loss = torch.zeros(n, device="cuda")
+    for a, b in zip(bounds, bounds[1:]):
+        r = kd().fused_fwd_bwd(Ht[a:b], Wt, Hs[a:b], Ws, m[a:b], T=1.0, kind="rkl", want_dW=True,
+                               accumulate_dW=True, dW_s=dW)
+        dh[a:b] = r.dh_s
+        loss[a:b] = r.loss
+    whole = kd().fused_fwd_bwd(Ht, Wt, Hs, Ws, m, T=1.0, kind="rkl", want_dW=True)
+    torch.cuda.synchronize()
+    l_ref, dh_ref, dW_ref = oracle_run(inp, T=1.0, kind="rkl", want_dW=True)
+    assert_kd_close("loss (micro-batches)", loss.cpu().numpy(), l_ref, LOSS_RTOL, LOSS_ATOL)
+    assert_grad_close("dh_s (micro-batches)", dh.cpu().numpy(), dh_ref)
+    assert_grad_close("dW accumulated", dW.cpu().numpy(), dW_ref)
+    assert_grad_close("dW whole", whole.dW_s.cpu().numpy(), dW_ref)
+    assert torch.equal(whole.loss, loss)  # per-token outputs do not depend on the micro-batching
+
+
+# ------------------------------------------------------------------ vocab shards with beta != 1/2
+@pytest.mark.parametrize("P,beta", [(2, 0.2), (3, 0.8)])
+def test_vocab_sharded_jsd_beta(P, beta):
+    """The JSD shard protocol (records all-gather -> partials -> (K, J) all-gather -> finish) at β != ½."""
+    from paper_2603_01875_b200.sharding import vocab_shard_bounds
+    N, d_t, d_s, V = 400, 256, 128, 4000
+    mask = (np.random.default_rng(P).random(N) > 0.2).astype(np.uint8)
+    inp = KI.make_inputs(N, d_t, d_s, V, seed=50 + P, mask=mask)
+    Ht, Hs, Wt, Ws = dev_bf16(inp.H_t), dev_bf16(inp.H_s), dev_bf16(inp.W_t), dev_bf16(inp.W_s)
+    m = torch.from_numpy(mask).cuda()
+    bounds = vocab_shard_bounds(V, P)
+    recs = torch.stack([kd().vocab_stats(Ht, Wt[a:b], Hs, Ws[a:b], m, vocab=V, v_begin=a, T=1.0, kind="jsd")
+                        for a, b in bounds])
+    parts = [kd().vocab_partials(Ht, Wt[a:b], Hs, Ws[a:b], recs, m, vocab=V, v_begin=a, T=1.0, kind="jsd",
+                                 beta=beta, want_dW=True) for a, b in bounds]
+    kj_all = torch.stack([kj for kj, _ in parts])
+    dh = torch.zeros(N, d_s, device="cuda")
+    dW = torch.zeros(V, d_s, device="cuda")
+    for (a, b), (_, st) in zip(bounds, parts):
+        r = kd().vocab_finish(st, Ht, Wt[a:b], Hs, Ws[a:b], kj_all, m, dW_s=dW[a:b])
+        dh += r.dh_s
+    torch.cuda.synchronize()
+    loss_ref, dh_ref, dW_ref = oracle_run(inp, T=1.0, kind="jsd", beta=beta, want_dW=True)
+    assert_kd_close("loss", r.loss.cpu().numpy(), loss_ref, LOSS_RTOL, LOSS_ATOL)
+    assert_grad_close("dh_s", dh.cpu().numpy(), dh_ref)
+    assert_grad_close("dW_s", dW.cpu().numpy(), dW_ref)

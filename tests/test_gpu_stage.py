@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import kd_inputs as KI
-from tests.kdtest_util import (LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close, dev_bf16, oracle_grad_floor,
+from tests.kdtest_util import (LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close, dev_bf16,
                                oracle_run)
 
 pytestmark = pytest.mark.gpu
@@ -134,9 +134,8 @@ def test_staged_full_size_sampled(name):
         rows[0], rows[-1] = 0, cfg.n_tokens - 1
     kw = dict(T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta)
     loss, dh, _ = oracle_run(inp, rows=rows, **kw)
-    fl, _ = oracle_grad_floor(inp, rows=rows, **kw)
     assert_kd_close("loss", r.loss.cpu().numpy()[rows], loss, LOSS_RTOL, LOSS_ATOL)
-    assert_grad_close("dh_s", r.dh_s.cpu().numpy()[rows], dh, fl)
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy()[rows], dh)
     if mask is not None:
         assert np.all(r.loss.cpu().numpy()[mask == 0] == 0)
 

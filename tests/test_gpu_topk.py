@@ -13,8 +13,8 @@ import torch
 
 import kd_inputs as KI
 from oracle.kd_oracle import divergence, lm_head_logits
-from oracle.kd_topk import fkl_topk_support, kd_topk_fwd_bwd, teacher_topk
-from tests.kdtest_util import (FLOOR_DRAWS, LOGIT_SIGMA, LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close,
+from oracle.kd_topk import kd_topk_fwd_bwd, teacher_topk
+from tests.kdtest_util import (LOSS_ATOL, LOSS_RTOL, assert_grad_close, assert_kd_close,
                                dev_bf16, f64)
 
 pytestmark = pytest.mark.gpu
@@ -30,25 +30,6 @@ def _need_gpu():
 def kd():
     import paper_2603_01875_b200 as m
     return m
-
-
-def topk_grad_floor(hs, Ws, idx, val, mask, T, seed=1234):
-    """Reading R14's conditioning floor for the top-k student: the oracle's 1-sigma dh_s / dW_s spread when the
-    student logits carry independent N(0, LOGIT_SIGMA^2) errors (the teacher's shipped values are exact inputs)."""
-    live = np.flatnonzero(mask)
-    dh_var = np.zeros((hs.shape[0], Ws.shape[1]))
-    dW_var = np.zeros_like(Ws)
-    rng = np.random.default_rng(seed)
-    for i in range(0, live.size, 64):
-        r = live[i:i + 64]
-        z = lm_head_logits(hs[r], Ws)
-        _, G = fkl_topk_support(idx[r], val[r], z, T)
-        for _ in range(FLOOR_DRAWS):
-            _, Gk = fkl_topk_support(idx[r], val[r], z + LOGIT_SIGMA * rng.standard_normal(z.shape), T)
-            D = Gk - G
-            dh_var[r] += (D @ Ws) ** 2 / FLOOR_DRAWS
-            dW_var += (D.T @ hs[r]) ** 2 / FLOOR_DRAWS
-    return np.sqrt(dh_var), np.sqrt(dW_var)
 
 
 def _check_selection(z64, idx, val, k):
@@ -108,11 +89,10 @@ def test_topk_student_side_vs_oracle(k, T):
     idx_np, val_np = idx.cpu().numpy().astype(np.int64), val.cpu().numpy().astype(np.float64)
     idx_np[mask == 0] = 0  # never read (masked); any in-range placeholder for the oracle's array shape
     loss, dh, dW = kd_topk_fwd_bwd(f64(inp.H_s), f64(inp.W_s), idx_np, val_np, mask, T=T, want_dW=True)
-    fl_dh, fl_dW = topk_grad_floor(f64(inp.H_s), f64(inp.W_s), idx_np, val_np, mask, T)
     assert int(r.n_nonfinite.item()) == 0
     assert_kd_close("loss", r.loss.cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
-    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh, fl_dh)
-    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW, fl_dW)
+    assert_grad_close("dh_s", r.dh_s.cpu().numpy(), dh)
+    assert_grad_close("dW_s", r.dW_s.cpu().numpy(), dW)
 
 
 def test_topk_is_a_negative_control():

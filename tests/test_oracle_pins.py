@@ -303,3 +303,45 @@ def test_comm_volume_footnote():
     assert v == 159_316_443_136
     assert round(v / 1e9) == 159 and abs(v / 1e9 - 160) < 1
     assert abs(151936 / 4096 - 37.09) < 0.01  # P:133 "4096 vs 151936"
+
+
+# ---------------------------------------------------------------- teacher_stats (the per-row (max, LSE) record)
+@pytest.mark.parametrize("T", [0.5, 1.0, 2.0])
+def test_teacher_stats_mpmath_bruteforce(T):
+    """oracle.teacher_stats against an independent 50-digit evaluation with Python loops: the dot products
+    h·W[v] (catches a transposed operand), the max of z/T and ln Σ_v e^{z_v/T} (the record the
+    vocab-sharded exchange and kd_teacher_lse carry)."""
+    rng = np.random.default_rng(int(T * 10))
+    N, d, V = 3, 5, 7
+    h = _rand(rng, N, d)
+    W = _rand(rng, V, d, scale=2.0)
+    m, lse = O.teacher_stats(h, W, T)
+    mpmath.mp.dps = 50
+    for n in range(N):
+        z = [mpmath.fsum(mpmath.mpf(float(h[n, k])) * mpmath.mpf(float(W[v, k])) for k in range(d)) / T
+             for v in range(V)]
+        zmax = max(z)
+        ref = zmax + mpmath.log(mpmath.fsum(mpmath.e ** (x - zmax) for x in z))
+        assert abs(m[n] - float(zmax)) <= 1e-14 * max(1.0, abs(float(zmax)))
+        assert abs(lse[n] - float(ref)) <= 1e-13 * max(1.0, abs(float(ref)))
+
+
+def test_teacher_stats_closed_forms():
+    """Zero hidden row: every logit 0, so max = 0 and LSE = ln V at any T.  One-hot h = e_j with a head column
+    holding k copies of c and the rest −∞-like: LSE = c/T + ln k.  LSE − max lies in [0, ln V]."""
+    V, d = 1000, 8
+    W = np.random.default_rng(3).standard_normal((V, d))
+    for T in (0.5, 1.0, 3.0):
+        m, lse = O.teacher_stats(np.zeros((2, d)), W, T)
+        np.testing.assert_array_equal(m, 0.0)
+        np.testing.assert_allclose(lse, math.log(V), rtol=0, atol=1e-12)
+    W2 = np.full((V, d), -1e4)
+    W2[:13, 2] = 3.0
+    h = np.zeros((1, d))
+    h[0, 2] = 1.0
+    m, lse = O.teacher_stats(h, W2, 2.0)
+    assert m[0] == 1.5
+    assert abs(lse[0] - (1.5 + math.log(13))) < 1e-12
+    rng = np.random.default_rng(4)
+    m, lse = O.teacher_stats(rng.standard_normal((20, d)), W * 5, 0.7)
+    assert np.all(lse >= m) and np.all(lse - m <= math.log(V) + 1e-12)

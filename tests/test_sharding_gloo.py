@@ -71,6 +71,8 @@ def _backward_standin(h_t, Wt, h_s, Ws, recs, mask, *, vocab, v_begin, T, kind, 
     ell = np.where(live, ell, 0.0)
     dh = torch.tensor(G @ Ws.double().numpy())
     dW = torch.tensor(G.T @ h_s.double().numpy()) if want_dW else None
+    if want_dW and accumulate_dW and dW_s is not None:  # the kernels accumulate into the caller's dW_s
+        dW = dW_s + dW
     return _R(torch.tensor(ell), dh, dW)
 
 
@@ -149,9 +151,10 @@ def _worker(rank, world, port, kind, q):
         Wt = torch.tensor(KI.bf16_to_f64(inp.W_t))
         Ws = torch.tensor(KI.bf16_to_f64(inp.W_s))
         a, b = vocab_shard_bounds(V, world, granule=16)[rank]
-        # JSD/TVD: chunk_tokens=16 drives three token chunks through the (K, J) exchange
+        # exchange_chunk=16 drives three pipelined token chunks: records all-gather (and for JSD/TVD the (K, J)
+        # all-gather) of chunk c+1 in flight while chunk c's partial dh all-reduce is still pending
         r = vocab_sharded_fwd_bwd(ht, Wt[a:b], hs, Ws[a:b], torch.tensor(mask), vocab=V, v_begin=a, T=1.3,
-                                  kind=kind, beta=0.3, want_dW=True, chunk_tokens=16, stats_fn=_stats_standin,
+                                  kind=kind, beta=0.3, want_dW=True, exchange_chunk=16, stats_fn=_stats_standin,
                                   backward_fn=_backward_standin, partials_fn=_partials_standin,
                                   finish_fn=_finish_standin)
         # token-sharded dW: each rank's partial sum over its tokens, reduced
@@ -163,7 +166,7 @@ def _worker(rank, world, port, kind, q):
         dW_tok = token_sharded_dW_reduce(torch.tensor(dW_part))
         # dh_reduce="scatter": the reduce-scatter of the same exchange, this rank's token slice only
         rs = vocab_sharded_fwd_bwd(ht, Wt[a:b], hs, Ws[a:b], torch.tensor(mask), vocab=V, v_begin=a, T=1.3,
-                                   kind=kind, beta=0.3, chunk_tokens=16, stats_fn=_stats_standin,
+                                   kind=kind, beta=0.3, exchange_chunk=16, stats_fn=_stats_standin,
                                    backward_fn=_backward_standin, partials_fn=_partials_standin,
                                    finish_fn=_finish_standin, dh_reduce="scatter")
         q.put((rank, r.loss.numpy(), r.dh_s.numpy(), (a, b, r.dW_s.numpy()), dW_tok.numpy(),
@@ -224,7 +227,7 @@ def test_one_rank_without_process_group(kind):
     f = KI.bf16_to_f64
     ht, hs, Wt, Ws = (torch.tensor(f(x)) for x in (inp.H_t, inp.H_s, inp.W_t, inp.W_s))
     r = vocab_sharded_fwd_bwd(ht, Wt, hs, Ws, None, vocab=V, v_begin=0, T=1.1, kind=kind, beta=0.5, want_dW=True,
-                              chunk_tokens=16, stats_fn=_stats_standin, backward_fn=_backward_standin,
+                              exchange_chunk=16, stats_fn=_stats_standin, backward_fn=_backward_standin,
                               partials_fn=_partials_standin, finish_fn=_finish_standin)
     loss, dh, dW = kd_fused_fwd_bwd(f(inp.H_t), f(inp.W_t), f(inp.H_s), f(inp.W_s), None, T=1.1, kind=kind,
                                     beta=0.5, want_dW=True)
