@@ -79,6 +79,9 @@ def parse():
                          "chunk's fp32 logits, an HBM-bound kernel forms G from them (no second tensor sweep)")
     ap.add_argument("--no-variants", action="store_true", help="skip the staged-variant leg of the default run")
     ap.add_argument("--graph", action="store_true", help="also time the step captured into a CUDA graph")
+    ap.add_argument("--handoff-peer", type=int, default=-1,
+                    help="with --handoff: the teacher process owns H_t on this GPU (another device of the node: the "
+                         "student maps it over NVLink; -1 = the student's own GPU)")
     ap.add_argument("--handoff", action="store_true",
                     help="add the hidden-state hand-off leg (SURVEY NEXT-4): teacher process -> student via CUDA IPC")
     ap.add_argument("--no-e2e", action="store_true")
@@ -384,13 +387,18 @@ def handoff_leg(args, cfg, kd, H_t_bits, Ht_local, Wt, Hs, Ws, mask, kw, out, dW
     import torch
     ctx = mp.get_context("spawn")
     parent, child = ctx.Pipe()
-    proc = ctx.Process(target=_handoff_teacher, args=(child, H_t_bits, cfg.vocab, local))
+    import torch as _t
+    peer = args.handoff_peer if args.handoff_peer >= 0 else local
+    if peer >= _t.cuda.device_count():
+        return {"skipped": f"--handoff-peer {peer}: this box has {_t.cuda.device_count()} GPU(s)"}
+    proc = ctx.Process(target=_handoff_teacher, args=(child, H_t_bits, cfg.vocab, peer))
     proc.start()
     try:
         h_ht, s_ht, h_lg, s_lg = parent.recv()
-        m_ht = kd.HandoffTensor(h_ht, s_ht, torch.bfloat16)
-        m_lg = kd.HandoffTensor(h_lg, s_lg, torch.bfloat16)
-        assert torch.equal(m_ht.tensor, Ht_local)
+        # the mapped buffers live on the teacher's GPU (the peer's memory, reached over NVLink, when peer != local)
+        m_ht = kd.HandoffTensor(h_ht, s_ht, torch.bfloat16, device=peer)
+        m_lg = kd.HandoffTensor(h_lg, s_lg, torch.bfloat16, device=peer)
+        assert torch.equal(m_ht.tensor.to(Ht_local.device), Ht_local)
         dst_ht = torch.empty_like(Ht_local)
         dst_lg = torch.empty(s_lg, dtype=torch.bfloat16, device=Ht_local.device)
 
@@ -417,8 +425,11 @@ def handoff_leg(args, cfg, kd, H_t_bits, Ht_local, Wt, Hs, Ws, mask, kw, out, dW
     finally:
         parent.send("done")
         proc.join(timeout=120)
-    return {"transport": "kd_handoff_export/open (CUDA IPC); teacher and student are separate processes on the same "
-                         "B200 — pulls are D2D copies through the exporter's mapping (read + write of the bytes)",
+    where = ("the same B200 — pulls are D2D copies through the exporter's mapping (read + write of the bytes)"
+             if peer == local else f"GPU {peer} (teacher) and GPU {local} (student) — pulls are peer copies over "
+             f"NVLink, the zero-copy step's TMA loads read the peer's H_t over NVLink")
+    return {"transport": "kd_handoff_export/open (CUDA IPC); teacher and student are separate processes on " + where,
+            "teacher_gpu": peer, "student_gpu": local,
             "h_t_bytes_per_step": b_ht, "full_logits_bytes_per_step": b_lg, "volume_ratio": b_lg / b_ht,
             "pull_h_t_ms": t_ht, "pull_logits_ms": t_lg, "time_ratio": t_lg / t_ht,
             "pull_h_t_GBps": b_ht / (t_ht / 1e3) / 1e9, "pull_logits_GBps": b_lg / (t_lg / 1e3) / 1e9,

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -43,6 +44,8 @@ cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, c
 cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, const int* idx,
                            float* kj, long long N, cudaStream_t s);
 cudaError_t launch_stage_grad(int kind, const StageParams& sp, int n_slots, cudaStream_t s);
+cudaError_t launch_die_probe(const unsigned* buf, const long long* line_off, int n_lines, int steps, unsigned* out,
+                             int sms, int smem_bytes, cudaStream_t s);
 int stage_rows();
 int stage_cols();
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
@@ -50,6 +53,8 @@ cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_sp
                              int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v = nullptr,
                              const float* corr2_r = nullptr, int n_slots2 = 0);
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
+cudaError_t launch_extract_zero(const int* corr_v, const float* corr_r, int n_slots, int n_rows, int row0,
+                                const int* n_eff, __nv_bfloat16* ghi, __nv_bfloat16* glo, cudaStream_t s);
 cudaError_t launch_topk_merge(const float* tk_val, const int* tk_idx, int n_slots, int n_rows, int row0,
                               const int* n_eff, const int* idx, int k, int v_base, int* out_idx, float* out_val,
                               cudaStream_t s);
@@ -201,11 +206,10 @@ static int device_sms() {
 }
 
 // Backward GEMMs flush their TMEM accumulator into the fp32 output every kKbPerAcc K blocks (see kd_gemm.cu).
-// 16 (1024 K values, 64 MMA steps per accumulator): the dh GEMM sums K = V = 151936 products into results ~100x smaller
-// than its terms (the bias column), and the truncating tcgen05 accumulation grows with the steps per accumulator —
-// at 64 the config-4 dh_s bias column reached 4.1x the north-star bound, at 16 0.80x (scripts/probe_parity_src.py,
-// profiles/r02_parity.md).  The promotion adds are overlapped with the next piece's MMAs (double-buffered TMEM).
-constexpr int kKbPerAccDefault = 16;
+// 64 (4096 K values per accumulator).  The dh GEMM's ill-conditioned outputs (the Zipf-bias column: results ~100x
+// smaller than their terms) are protected by taking pass 2's largest entries out of its G instead (k_extract_zero):
+// shorter pieces would cost a read-modify-write of the fp32 output per piece — 16 measured +18 ms per config-2 step.
+constexpr int kKbPerAccDefault = 64;
 static int kb_per_acc() {  // KD_KB_PER_ACC overrides the promotion period (precision experiments)
   static int v = [] {
     const char* e = getenv("KD_KB_PER_ACC");
@@ -227,9 +231,13 @@ struct Plan {
   bool stage;    // staged variant (kd_problem.stage_logits): pass 1 writes the chunk's logits, k_stage_grad makes G
   int n_gslots;  // per-row slots of the G step's partials (loss / (K, J) / residual fix): pass 2's n_split * parts,
                  // or the staged kernel's vocab slots
+  // die-aware unit placement of the fused passes (PassParams::die_map): die_map != NULL when on; die_w0 = worker slots
+  // of die 0; die_s0 = first vocab split of die 1
+  const uint8_t* die_map;
+  int die_w0, die_s0;
   size_t off_neff, off_nonfinite, off_idx, off_ht, off_hs, off_part, off_fstats, off_kpart, off_kfin, off_ghi,
       off_glo, off_ga, off_gb, off_dhp, off_corr_v, off_corr_r, off_zscr, off_tkv, off_tki, off_tkr_v, off_tkr_r,
-      off_zst, total;
+      off_zst, off_sched, total;
 };
 
 // Static round-robin of units over a persistent grid: makespan in tiles (+ per-unit refill cost).
@@ -246,6 +254,191 @@ static double pass_makespan(int m_tiles, int s, int v_tiles, int sms) {
     if (t > worst) worst = t;
   }
   return worst;
+}
+
+// ------------------------------------------------------------------------------------ SM -> die map
+// B200 has two dies, each with its own L2 partition.  The fused passes read every vocab tile of the heads once per
+// token tile of the chunk; the token tiles of one vocab split run concurrently, so when their SM pairs sit on both
+// dies each die's L2 misses on the same head rows and the heads come from DRAM ~2x (profiles/r01_ncu_full_final.md).
+// The map is measured once per device (k_die_probe: per-SM L2 latency to lines homed on either partition; the two
+// near-sets are the dies) and then steers each pair to a worker slot of its own die (PassParams::die_map).  A map
+// that does not look like two equal halves of SM pairs is discarded (plain round-robin placement).  The probe
+// allocates ~32 MB once per device at the first call (not on the hot path).  Opt-in (KD_DIE_SCHED=1): measured at
+// config 2 it cuts pass 1's DRAM reads 3.5 -> 3.1 GB per launch (pass 2: 4.0 -> 3.8) with no change in step time
+// (profiles/r02_die_sched.md), so the default keeps the plain round-robin placement.
+namespace {
+struct DieMap {
+  bool tried = false;
+  uint8_t* dev = nullptr;  // [256] die of each %smid, device memory
+  int pairs0 = 0, pairs1 = 0;
+};
+}  // namespace
+static std::mutex g_die_mu;
+static DieMap g_die[64];
+
+static void probe_die_map(DieMap& m, int sms) {
+  constexpr int kLines = 16, kSteps = 256, kWords = (32 << 20) / 4;
+  unsigned* buf = nullptr;
+  long long* d_off = nullptr;
+  unsigned* d_out = nullptr;
+  cudaStream_t st = nullptr;
+  std::vector<unsigned> out((size_t)sms * (kLines + 1));
+  // every SM must be free for one probe CTA: drain the device first (first call only)
+  bool ok = cudaDeviceSynchronize() == cudaSuccess &&
+            cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMalloc(&buf, (size_t)kWords * 4) == cudaSuccess &&
+            cudaMalloc(&d_off, kLines * sizeof(long long)) == cudaSuccess &&
+            cudaMalloc(&d_out, out.size() * 4) == cudaSuccess;
+  if (ok) {
+    long long off[kLines];
+    for (int l = 0; l < kLines; ++l) off[l] = (long long)l * (kWords / kLines) + 32ll * (l * 7 % 16);
+    ok = cudaMemsetAsync(buf, 0, (size_t)kWords * 4, st) == cudaSuccess &&
+         cudaMemcpyAsync(d_off, off, sizeof off, cudaMemcpyHostToDevice, st) == cudaSuccess &&
+         launch_die_probe(buf, d_off, kLines, kSteps, d_out, sms, 200 * 1024, st) == cudaSuccess &&
+         cudaMemcpyAsync(out.data(), d_out, out.size() * 4, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+         cudaStreamSynchronize(st) == cudaSuccess;
+  }
+  if (buf) cudaFree(buf);
+  if (d_off) cudaFree(d_off);
+  if (d_out) cudaFree(d_out);
+  if (st) cudaStreamDestroy(st);
+  if (!ok) {
+    cudaGetLastError();
+    return;
+  }
+  // each line: its near set = the half of the SMs with the lowest latency (the dies are equal halves; near / far
+  // differ by ~10-15% of ~280 cycles, with a spread inside each die, so a median split rather than a gap);
+  // lines are oriented against the first one and the SMs' memberships voted
+  std::vector<int> smid(sms), vote(sms, 0);
+  for (int b = 0; b < sms; ++b) smid[b] = (int)out[(size_t)b * (kLines + 1)];
+  {
+    std::vector<int> ids(smid);
+    std::sort(ids.begin(), ids.end());
+    if (std::unique(ids.begin(), ids.end()) != ids.end()) return;  // an SM ran two probe CTAs: not one per SM
+  }
+  std::vector<std::vector<char>> nears;
+  for (int l = 0; l < kLines; ++l) {
+    std::vector<int> order(sms);
+    for (int b = 0; b < sms; ++b) order[b] = b;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      return out[(size_t)x * (kLines + 1) + 1 + l] < out[(size_t)y * (kLines + 1) + 1 + l];
+    });
+    std::vector<char> near(sms, 0);
+    for (int i = 0; i < sms / 2; ++i) near[order[i]] = 1;
+    if (env_int("KD_DIE_DEBUG", 0) > 1)
+      fprintf(stderr, "kd: die probe line %d: latency min %u median %u max %u\n", l,
+              out[(size_t)order[0] * (kLines + 1) + 1 + l], out[(size_t)order[sms / 2] * (kLines + 1) + 1 + l],
+              out[(size_t)order[sms - 1] * (kLines + 1) + 1 + l]);
+    if (!nears.empty()) {
+      int agree = 0;
+      for (int b = 0; b < sms; ++b) agree += near[b] == nears[0][b];
+      if (agree * 2 < sms)
+        for (int b = 0; b < sms; ++b) near[b] ^= 1;
+    }
+    nears.push_back(near);
+    for (int b = 0; b < sms; ++b) vote[b] += near[b] ? 1 : -1;
+  }
+  // lines must agree with the vote: a median split of a line homed evenly would be noise
+  int used = 0;
+  for (const auto& near : nears) {
+    int agree = 0;
+    for (int b = 0; b < sms; ++b) agree += (near[b] != 0) == (vote[b] > 0);
+    used += agree * 10 >= sms * 9;  // >= 90% agreement
+  }
+  if (env_int("KD_DIE_DEBUG", 0)) fprintf(stderr, "kd: die probe: %d of %d lines split the SMs in two levels\n", used, kLines);
+  if (used < 4) return;
+  uint8_t table[256] = {0};
+  int n0 = 0;
+  for (int b = 0; b < sms; ++b) {
+    if (smid[b] > 255) return;
+    table[smid[b]] = vote[b] > 0 ? 0 : 1;
+    n0 += vote[b] > 0;
+  }
+  // SM pairs (2k, 2k+1) run the clusters of two: they must share a die, and the dies must be equal halves
+  for (int b = 0; b < sms; ++b)
+    if ((smid[b] ^ 1) < 256 && table[smid[b]] != table[smid[b] ^ 1]) {
+      bool partner_seen = false;
+      for (int c = 0; c < sms; ++c) partner_seen |= smid[c] == (smid[b] ^ 1);
+      if (partner_seen) return;
+    }
+  if (n0 % 2 || (sms - n0) % 2 || std::abs(n0 - (sms - n0)) > 8) return;
+  uint8_t* d = nullptr;
+  if (cudaMalloc(&d, 256) != cudaSuccess || cudaMemcpy(d, table, 256, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (d) cudaFree(d);
+    cudaGetLastError();
+    return;
+  }
+  m.dev = d;
+  m.pairs0 = n0 / 2;
+  m.pairs1 = (sms - n0) / 2;
+  if (env_int("KD_DIE_DEBUG", 0)) {
+    fprintf(stderr, "kd: die map from %d/%d probe lines: %d + %d SMs; die of smid 0..%d:", used, kLines, n0, sms - n0,
+            sms - 1);
+    for (int i = 0; i < sms && i < 256; ++i) fprintf(stderr, "%d", table[i]);
+    fprintf(stderr, "\n");
+  }
+}
+
+// The device's die map (probed on first use), or NULL.  Not probed while `stream` is being captured into a graph
+// (the probe allocates and synchronises); the capture then runs with plain placement.
+static const DieMap* die_map_for(cudaStream_t stream, int sms) {
+  static const int enabled = env_int("KD_DIE_SCHED", 0);
+  if (!enabled) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_die_mu);
+  DieMap& m = g_die[dev & 63];
+  if (!m.tried) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    m.tried = true;
+    probe_die_map(m, sms);
+  }
+  return m.dev ? &m : nullptr;
+}
+
+// Die-aware static makespan: die d's splits [d ? s0 : 0, d ? s : s0) over its w_d worker slots, token tiles of a split
+// consecutive (the units the kernel deals to each die).
+static double pass_makespan_die(int m_tiles, int s, int s0, int v_tiles, int w0, int w1) {
+  double worst = 0;
+  for (int d = 0; d < 2; ++d) {
+    const int sb = d ? s0 : 0, se = d ? s : s0, W = d ? w1 : w0;
+    const int units = (se - sb) * m_tiles;
+    for (int c = 0; c < W && c < units; ++c) {
+      double t = 0;
+      for (int j = c; j < units; j += W) {
+        const int sp = sb + j / m_tiles;
+        t += (double)((long long)(sp + 1) * v_tiles / s - (long long)sp * v_tiles / s) + 0.1;
+      }
+      if (t > worst) worst = t;
+    }
+  }
+  return worst;
+}
+
+static void choose_split_die(int m_tiles, int v_tiles, int w0, int w1, int& best_s, int& best_s0) {
+  static std::mutex mu;
+  static std::unordered_map<long long, long long> memo;
+  const long long key = ((long long)m_tiles << 44) | ((long long)v_tiles << 20) | ((long long)w0 << 10) | w1;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) { best_s = (int)(it->second >> 20); best_s0 = (int)(it->second & 0xFFFFF); return; }
+  }
+  double best = 1e300;
+  best_s = 2;
+  best_s0 = 1;
+  const int smax = v_tiles < 160 ? v_tiles : 160;
+  for (int s = 2; s <= smax; ++s) {
+    if ((long long)s * m_tiles < w0 + w1) continue;  // every worker slot of both dies gets a unit: the grid is all SMs
+    const int base = (int)((long long)s * w0 / (w0 + w1));
+    for (int s0 = std::max(1, base - 1); s0 <= std::min(s - 1, base + 1); ++s0) {
+      const double c = pass_makespan_die(m_tiles, s, s0, v_tiles, w0, w1);
+      if (c < best * 0.999) { best = c; best_s = s; best_s0 = s0; }
+    }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  memo[key] = ((long long)best_s << 20) | best_s0;
 }
 
 static int choose_n_split_search(int m_tiles, int v_tiles, int sms);
@@ -358,7 +551,22 @@ static Plan make_plan(const kd_problem* p) {
   P.n_chunks = (P.N + nc - 1) / nc;
   P.m_tiles_c = nc / bmt;
   P.v_tiles = (P.V_r + P.bn - 1) / P.bn;
-  P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, P.num_sms / P.cg);
+  {
+    // vocab splits: die-aware placement needs both dies' worker slots filled (all SMs, an even number of pairs);
+    // its split count is planned per die even when the map turns out unavailable at run time (the workspace depends
+    // on n_split), where the same splits are then dealt round-robin
+    static const int die_env = env_int("KD_DIE_SCHED", 0);
+    const int workers = P.num_sms / P.cg;
+    P.die_map = nullptr;
+    if (die_env && P.cg == 2 && P.bn == 256 && workers % 2 == 0 && (long long)P.m_tiles_c * P.v_tiles >= 2ll * workers) {
+      choose_split_die(P.m_tiles_c, P.v_tiles, workers / 2, workers / 2, P.n_split, P.die_s0);
+      P.die_w0 = workers / 2;
+    } else {
+      P.n_split = choose_n_split(P.m_tiles_c, P.v_tiles, workers);
+      P.die_s0 = P.n_split;
+      P.die_w0 = 0;  // plain placement (pass_params: die_w0 = the grid's workers)
+    }
+  }
   P.g_ld = ((P.V_r + 63) / 64) * 64;
   P.stage = p->stage_logits != 0;
   {
@@ -396,6 +604,7 @@ static Plan make_plan(const kd_problem* p) {
   P.off_tkr_v = take((size_t)P.Nc * kTopK * 4);  // top-k baseline: residual slots of the k support entries
   P.off_tkr_r = take((size_t)P.Nc * kTopK * 4);
   P.off_zst = take(P.stage ? (size_t)2 * P.g_ld * P.Nc * 4 : 0);  // staged logits of one chunk (2.5 GB at c2)
+  P.off_sched = take(16);  // die-aware placement counters (PassParams::sched), zeroed before each pass launch
   P.total = o;
   // kd_teacher_topk's candidate lists [n_split*parts][Nc][kTopK] (values, indices) reuse the G / dh scratch, which
   // that call does not touch (extended only if a tiny vocabulary makes the scratch smaller than the lists)
@@ -477,6 +686,12 @@ static kd_status prologue(Ctx& c, const void* h_t, const void* W_t, const void* 
   return KD_OK;
 }
 
+static int pass_grid(const Plan& P) {  // CTAs (a multiple of the CTA group)
+  const int units = P.m_tiles_c * P.n_split;
+  const int workers = P.num_sms / P.cg;
+  return (units < workers ? units : workers) * P.cg;
+}
+
 static PassParams pass_params(const Ctx& c, int row0) {
   const Plan& P = c.P;
   const kd_problem* p = c.p;
@@ -512,14 +727,30 @@ static PassParams pass_params(const Ctx& c, int row0) {
   pp.side_hi = 2;
   pp.tk_val = ws_at<float>(c.ws, P.off_tkv);
   pp.tk_idx = ws_at<int>(c.ws, P.off_tki);
+  pp.sched = ws_at<int>(c.ws, P.off_sched);
+  pp.die_map = P.die_map;
+  pp.die_w0 = P.die_map ? P.die_w0 : pass_grid(P) / P.cg;
+  pp.die_s0 = P.die_map ? P.die_s0 : P.n_split;
   return pp;
 }
 
-static int pass_grid(const Plan& P) {  // CTAs (a multiple of the CTA group)
-  const int units = P.m_tiles_c * P.n_split;
-  const int workers = P.num_sms / P.cg;
-  return (units < workers ? units : workers) * P.cg;
+// Die-aware placement for this call when the plan allows it and the device's map matches (PassParams::die_map).
+static void attach_die(Ctx& c) {
+  if (c.P.die_w0 <= 0) return;
+  const DieMap* m = die_map_for(c.s, c.P.num_sms);
+  if (m && m->pairs0 == c.P.die_w0 && m->pairs1 == c.P.num_sms / c.P.cg - c.P.die_w0 &&
+      pass_grid(c.P) == c.P.num_sms)
+    c.P.die_map = m->dev;
 }
+
+// One fused-pass launch (the die-aware placement counters are zeroed first).
+static kd_status run_pass(Ctx& c, int pass, int kind, bool coupled, const PassParams& pp) {
+  if (pp.die_map) KD_CUDA(cudaMemsetAsync(pp.sched, 0, 16, c.s));
+  KD_LAUNCH(pass == 1 ? K_PASS1 : K_PASS2,
+            launch_pass(pass, kind, coupled, c.P.cg, c.P.bn, c.maps, pp, pass_grid(c.P), c.s));
+  return KD_OK;
+}
+
 
 // pass 2 for one chunk whose final per-token statistics are already in fstats: G (FKL/RKL) or the two JSD/TVD
 // planes + partial K, J.
@@ -528,7 +759,8 @@ static kd_status grad_chunk(Ctx& c, int row0, int side_lo = 0) {
   PassParams pp = pass_params(c, row0);
   pp.side_lo = side_lo;  // 1: student-only pass 2 (top-k baseline: G = gscale·q, the teacher put back afterwards)
   static const bool p2_coupled = env_int("KD_P2_COUPLED", 0) != 0;
-  KD_LAUNCH(K_PASS2, launch_pass(2, P.kind, p2_coupled && side_lo == 0, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+  kd_status st = run_pass(c, 2, P.kind, p2_coupled && side_lo == 0, pp);
+  if (st != KD_OK) return st;
   return KD_OK;
 }
 
@@ -547,34 +779,9 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
                           pp.g_hi, pp.g_lo, P.num_sms, kj_ranks, n_ranks, (long long)P.N, c.s));
   }
-  // dh_s rows of this chunk: [G_hi | G_lo] · W_s  (K = V_r); the scratch holds Gᵀ [g_ld][Nc], i.e. the A operand
-  // [tokens, V] is MN-major; W_s [V_r, d_s] is the MN-major B operand.  Split-K slabs, then reduce + scatter.
-  CUtensorMap mg_hi, mg_lo, mw;
   kd_status st;
-  if ((st = make_map(&mg_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK) return st;
-  if (P.g_planes == 2 && (st = make_map(&mg_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK)
-    return st;
-  if ((st = make_map(&mw, c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK) return st;
-  GemmParams gp{};
-  gp.M = P.Nc;
-  gp.N = P.d_s;
-  gp.K = P.V_r;
-  gp.dyn_dim = DYN_M;
-  gp.dyn = c.n_eff;
-  gp.dyn_base = row0;
-  gp.k_split = P.k_split;
-  gp.kb_per_acc = kb_per_acc();
-  gp.out = ws_at<float>(c.ws, P.off_dhp);
-  gp.out_ld = P.d_s;
-  gp.out_split_stride = (long long)P.Nc * P.d_s;
-  KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, P.g_planes, EPI_STORE, gemm_cg(), &mg_hi,
-                                   P.g_planes == 2 ? &mg_lo : nullptr, &mw, gp, P.num_sms, c.s));
-  KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
-                                          P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
-                                          P.n_gslots * kCorrSlots, c.Ws, c.s,
-                                          topk ? ws_at<int>(c.ws, P.off_tkr_v) : nullptr,
-                                          topk ? ws_at<float>(c.ws, P.off_tkr_r) : nullptr, topk));
   if (dW) {
+    // dW_s += Gᵀ · H_s first: it reads the full G, before the extracted entries are taken out for the dh GEMM
     CUtensorMap ma_hi, ma_lo, mh;
     // dW_s += Gᵀ · H_s: A = Gᵀ [g_ld][Nc] is K-major (K = tokens), B = H_s chunk MN-major
     if ((st = make_map(&ma_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, kBK, kBM)) != KD_OK) return st;
@@ -598,6 +805,36 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
     KD_LAUNCH(K_GEMM_DW, launch_gemm(false, true, P.g_planes, EPI_ACCUM, gemm_cg(), &ma_hi,
                                      P.g_planes == 2 ? &ma_lo : nullptr, &mh, wp, P.num_sms, c.s));
   }
+  // FKL/RKL: pass 2's largest entries per (row, slot) leave the dh GEMM (restored exactly by k_reduce_dh)
+  if (!P.fix)
+    KD_LAUNCH(K_REDUCE_DH, launch_extract_zero(pp.corr_v, pp.corr_r, P.n_gslots * kCorrSlots, P.Nc, row0, c.n_eff,
+                                               pp.g_hi, pp.g_lo, c.s));
+  // dh_s rows of this chunk: [G_hi | G_lo] · W_s  (K = V_r); the scratch holds Gᵀ [g_ld][Nc], i.e. the A operand
+  // [tokens, V] is MN-major; W_s [V_r, d_s] is the MN-major B operand.  Split-K slabs, then reduce + scatter.
+  CUtensorMap mg_hi, mg_lo, mw;
+  if ((st = make_map(&mg_hi, pp.g_hi, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK) return st;
+  if (P.g_planes == 2 && (st = make_map(&mg_lo, pp.g_lo, P.Nc, P.g_ld, (uint64_t)P.Nc * 2, 64, kBK)) != KD_OK)
+    return st;
+  if ((st = make_map(&mw, c.Ws, P.d_s, P.V_r, (uint64_t)P.d_s * 2, 64, kBK)) != KD_OK) return st;
+  GemmParams gp{};
+  gp.M = P.Nc;
+  gp.N = P.d_s;
+  gp.K = P.V_r;
+  gp.dyn_dim = DYN_M;
+  gp.dyn = c.n_eff;
+  gp.dyn_base = row0;
+  gp.k_split = P.k_split;
+  gp.kb_per_acc = kb_per_acc();
+  gp.out = ws_at<float>(c.ws, P.off_dhp);
+  gp.out_ld = P.d_s;
+  gp.out_split_stride = (long long)P.Nc * P.d_s;
+  KD_LAUNCH(K_GEMM_DH, launch_gemm(true, true, P.g_planes, EPI_STORE, gemm_cg(), &mg_hi,
+                                   P.g_planes == 2 ? &mg_lo : nullptr, &mw, gp, P.num_sms, c.s));
+  KD_LAUNCH(K_REDUCE_DH, launch_reduce_dh(gp.out, gp.out_split_stride, P.k_split, P.d_s, P.Nc, row0, c.n_eff, c.idx, dh,
+                                          P.fix ? nullptr : pp.corr_v, P.fix ? nullptr : pp.corr_r,
+                                          P.n_gslots * kCorrSlots, c.Ws, c.s,
+                                          topk ? ws_at<int>(c.ws, P.off_tkr_v) : nullptr,
+                                          topk ? ws_at<float>(c.ws, P.off_tkr_r) : nullptr, topk));
   return KD_OK;
 }
 
@@ -652,6 +889,7 @@ static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   float* dW = p->want_dW ? dW_s : nullptr;
   if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s, dW, workspace, workspace_bytes, c.P)) != KD_OK)
     return st;
@@ -670,7 +908,7 @@ static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_
     const bool coupled = P.kind == KD_RKL;
     if (lse_t) pp.side_lo = 1;  // student half-tiles only
     if (P.stage) pp.zst = ws_at<float>(c.ws, P.off_zst);
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    if ((st = run_pass(c, 1, P.kind, coupled, pp)) != KD_OK) return st;
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, (long long)P.N, c.idx, 0, c.nonfinite,
                            coupled ? 1 : 0, c.s, lse_t));
@@ -733,6 +971,7 @@ kd_status kd_teacher_lse(const kd_problem* p, const void* h_t, const void* W_t, 
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   const Plan& P = c.P;
   if (P.N > 0 && (!h_t || !lse_t)) return fail(KD_ERR_INVALID_ARG, "NULL h_t / lse_t");
   if (!W_t) return fail(KD_ERR_INVALID_ARG, "NULL W_t");
@@ -747,7 +986,7 @@ kd_status kd_teacher_lse(const kd_problem* p, const void* h_t, const void* W_t, 
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     pp.side_hi = 1;  // teacher half-tiles only (the same sweep as the teacher side of the fused decoupled pass 1)
-    KD_LAUNCH(K_PASS1, launch_pass(1, KD_FKL, false, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    if ((st = run_pass(c, 1, KD_FKL, false, pp)) != KD_OK) return st;
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, KD_FKL), P.Nc, row0,
                                     c.n_eff, KD_FKL, 2, nullptr, nullptr, lse_t, (long long)P.N, c.idx, 0,
                                     c.nonfinite, 0, c.s));
@@ -768,6 +1007,7 @@ kd_status kd_teacher_topk(const kd_problem* p, const void* h_t, const void* W_t,
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   const Plan& P = c.P;
   if (P.N > 0 && (!h_t || !topk_idx || !topk_val)) return fail(KD_ERR_INVALID_ARG, "NULL h_t / topk_idx / topk_val");
   if (!W_t) return fail(KD_ERR_INVALID_ARG, "NULL W_t");
@@ -780,7 +1020,7 @@ kd_status kd_teacher_topk(const kd_problem* p, const void* h_t, const void* W_t,
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     pp.side_hi = 1;  // teacher half-tiles only
-    KD_LAUNCH(K_PASS1, launch_pass(1, KIND_TOPK, false, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    if ((st = run_pass(c, 1, KIND_TOPK, false, pp)) != KD_OK) return st;
     KD_LAUNCH(K_TOPK, launch_topk_merge(pp.tk_val, pp.tk_idx, P.n_split * epi_parts(1, KIND_TOPK), P.Nc, row0,
                                         c.n_eff, c.idx, k, (int)p->v_begin, topk_idx, topk_val, c.s));
   }
@@ -804,6 +1044,7 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   float* dW = p->want_dW ? dW_s : nullptr;
   // h_t / W_t are not inputs of the top-k student: the student's own tensors stand in for the pointer checks
   if ((st = check_common(p, h_s, W_s, h_s, W_s, loss, dh_s, dW, workspace, workspace_bytes, c.P)) != KD_OK) return st;
@@ -820,7 +1061,7 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
     pp.side_lo = 1;  // student half-tiles only: LSE_s (the teacher's part of the record mirrors it, unused)
-    KD_LAUNCH(K_PASS1, launch_pass(1, KD_FKL, false, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    if ((st = run_pass(c, 1, KD_FKL, false, pp)) != KD_OK) return st;
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0,
                                     c.n_eff, P.kind, 0, ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 0,
                                     c.nonfinite, 0, c.s));
@@ -845,6 +1086,7 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   if (c.P.N > 0 && !rec) return fail(KD_ERR_INVALID_ARG, "rec is NULL");
   if (rec && !aligned16(rec)) return fail(KD_ERR_ALIGNMENT, "rec must be 16-byte aligned");
   if ((st = check_common(p, h_t, W_t, h_s, W_s, rec, rec, nullptr, workspace, workspace_bytes, c.P)) != KD_OK)
@@ -861,7 +1103,7 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
     // before pass 2.  FKL (loss partials from pass 2, summed by the caller), JSD/TVD (loss from the (K, J) exchange)
     // need the two LSEs only: the decoupled pass 1, as the fused path
     const bool coupled = P.kind == KD_RKL;
-    KD_LAUNCH(K_PASS1, launch_pass(1, P.kind, coupled, P.cg, P.bn, c.maps, pp, pass_grid(P), c.s));
+    if ((st = run_pass(c, 1, P.kind, coupled, pp)) != KD_OK) return st;
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
                            nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, 0, c.s));
   }
@@ -884,6 +1126,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   float* dW = p->want_dW ? dW_s : nullptr;
   if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s_partial, dW, workspace, workspace_bytes, c.P)) != KD_OK)
     return st;
@@ -925,6 +1168,7 @@ static kd_status vocab_fix_setup(Ctx& c, const kd_problem* p, void* workspace, s
   c.P = make_plan(p);
   c.s = static_cast<cudaStream_t>(stream);
   c.ws = workspace;
+  attach_die(c);
   if (c.P.n_chunks > 1)
     return fail(KD_ERR_SHAPE, "JSD/TVD vocab shards run one token chunk per call: n_tokens (%d) must be <= the chunk (%d)",
                 c.P.N, c.P.Nc);

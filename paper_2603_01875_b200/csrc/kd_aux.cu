@@ -281,11 +281,38 @@ __global__ void __launch_bounds__(256) k_kfix_apply(const float* __restrict__ ga
   }
 }
 
-// ------------------------------------------------------------------ A4r: dh split-K reduce + residual fix + scatter
+// ------------------------------------------------------------------ A4x: extracted entries out of the dh GEMM's G
+// Pass 2 (FKL/RKL) records per (row, slot) the two largest entries |g| > 2^-7 with their exact fp32 value
+// (corr_v / corr_r [n_rows][n_slots]).  After the dW GEMM has read the full G, they are zeroed in both planes so the
+// dh GEMM accumulates only the small entries (its truncating fp32 accumulator then never carries their large partial
+// sums), and k_reduce_dh adds g·W_s[v, :] for them in fp32.  One thread per (row, slot entry); rows < n_eff only.
+__global__ void __launch_bounds__(256) k_extract_zero(const int* __restrict__ corr_v, const float* __restrict__ corr_r,
+                                                      int n_slots, int n_rows, int row0, const int* __restrict__ n_eff,
+                                                      __nv_bfloat16* __restrict__ ghi, __nv_bfloat16* __restrict__ glo) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = (int)(i / n_slots);
+  const int valid = min(n_rows, *n_eff - row0);
+  if (r >= valid) return;
+  if (corr_r[i] == 0.f) return;
+  const size_t e = (size_t)corr_v[i] * n_rows + r;
+  ghi[e] = __ushort_as_bfloat16((unsigned short)0);
+  if (glo) glo[e] = __ushort_as_bfloat16((unsigned short)0);
+}
+
+cudaError_t launch_extract_zero(const int* corr_v, const float* corr_r, int n_slots, int n_rows, int row0,
+                                const int* n_eff, __nv_bfloat16* ghi, __nv_bfloat16* glo, cudaStream_t s) {
+  const long long n = (long long)n_rows * n_slots;
+  if (n > 0) k_extract_zero<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(corr_v, corr_r, n_slots, n_rows, row0, n_eff,
+                                                                        ghi, glo);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ A4r: dh split-K reduce + extracted entries + scatter
 // One warp per token row: lane j owns columns {8j..8j+7} + 256·i (coalesced 32-byte / 16-byte accesses).
-//   dh[orig(r), :] = Σ_ks part[ks][r, :]  +  Σ_{slot} r_slot · W_s[v_slot, :]
-// The second sum is the split-bf16 residual fix (kd_pass.cu): the exact residual g − (hi + lo) of the largest
-// entries of G, added back in a fixed (slot) order — deterministic.  d_s % 8 == 0, d_s <= 2048 * 4.
+//   dh[orig(r), :] = Σ_ks part[ks][r, :]  +  Σ_{slot} g_slot · W_s[v_slot, :]
+// The second sum restores the entries extracted from the dh GEMM (k_extract_zero): their exact fp32 g, added in a
+// fixed (slot) order — deterministic.  corr2 (top-k baseline): exact residuals g − (hi + lo) of the support entries
+// that were not extracted.  d_s % 8 == 0, d_s <= 2048 * 4.
 constexpr int kRedVec = 8;  // 8-column groups per lane per column block: 32 lanes x 8 x 8 = 2048 columns
 __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ part, long long split_stride, int k_split,
                                                    int d_s, int n_rows, int row0, const int* __restrict__ n_eff,
@@ -386,6 +413,39 @@ __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ par
       }
     }
   }
+}
+
+// ------------------------------------------------------------------ SM -> L2 partition (die) probe
+// One CTA per SM (the dynamic shared memory forces it); thread 0 times a dependent chase of L2-resident loads
+// (ld.global.cg) on each of n_lines single lines.  A line's latency is lower from the SMs of the die whose L2
+// partition homes it, so each line splits the SMs into a near and a far set; the host combines the lines into a
+// die map (kd_api.cu).  Used once per device to place the fused passes' work units.
+__global__ void k_die_probe(const unsigned* __restrict__ buf, const long long* __restrict__ line_off, int n_lines,
+                            int steps, unsigned* __restrict__ out) {
+  extern __shared__ unsigned char probe_smem[];
+  if (threadIdx.x != 0) return;
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  unsigned* o = out + (size_t)blockIdx.x * (n_lines + 1);
+  o[0] = smid;
+  for (int l = 0; l < n_lines; ++l) {
+    const unsigned* q = buf + line_off[l];
+    unsigned i = 0;
+    for (int s = 0; s < 32; ++s) i = __ldcg(q + i);  // warm the line into L2 (each line holds 0: a self-loop)
+    const long long t0 = clock64();
+    for (int s = 0; s < steps; ++s) i = __ldcg(q + i);
+    const long long t1 = clock64();
+    o[1 + l] = (unsigned)((t1 - t0) / steps) + (i == 0xFFFFFFFFu ? 1u : 0u);
+  }
+  probe_smem[0] = 0;
+}
+
+cudaError_t launch_die_probe(const unsigned* buf, const long long* line_off, int n_lines, int steps, unsigned* out,
+                             int sms, int smem_bytes, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_die_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (e != cudaSuccess) return e;
+  k_die_probe<<<sms, 32, smem_bytes, s>>>(buf, line_off, n_lines, steps, out);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ launchers
@@ -522,22 +582,22 @@ __global__ void __launch_bounds__(256) k_topk_fix(const __nv_bfloat16* __restric
   // G at the support: start from the value pass 2 formed for q there (hi + lo + its exact residual, if it recorded
   // one: then bit-for-bit the fp32 gscale·q of the GEMM logits, consistent with the LSE record; the dot-product
   // logit above differs from the GEMM's by its rounding, and e^{δz} would move q_top ≈ 1 by δz itself)
-  __shared__ float s_res[8][32];
-  float* my_res = s_res[threadIdx.x >> 5];
-  my_res[lane] = 0.f;
+  // pass 2 extracted up to two entries per (row, slot) with their exact fp32 g (k_extract_zero / k_reduce_dh): a support
+  // column found there takes its value from the slot, and the slot then carries the corrected value
+  __shared__ int s_slot[8][32];
+  int* my_slot = s_slot[threadIdx.x >> 5];
+  my_slot[lane] = -1;
   __syncwarp();
   if (!bad && corr_v) {
     const size_t cb = (size_t)r * n_corr;
     for (int base = 0; base < n_corr; base += 32) {  // warp-uniform trip count (shuffles inside)
       const int i = base + lane;
       const int cv = i < n_corr ? corr_v[cb + i] : -1;
+      const float cr = i < n_corr ? corr_r[cb + i] : 0.f;
       int hit = -1;
       for (int j = 0; j < k; ++j)
         if (cv == __shfl_sync(0xffffffffu, v_me, j)) hit = j;
-      if (hit >= 0 && cv >= 0) {  // each support column sits in one unit's slots at most once
-        my_res[hit] = corr_r[cb + i];
-        corr_r[cb + i] = 0.f;  // folded into the new support value below
-      }
+      if (hit >= 0 && cr != 0.f) my_slot[hit] = (int)(cb + i);  // each support column is in one slot at most
     }
   }
   __syncwarp();
@@ -545,15 +605,20 @@ __global__ void __launch_bounds__(256) k_topk_fix(const __nv_bfloat16* __restric
     float res = 0.f;
     if (!bad) {
       const size_t e = (size_t)v_me * n_rows + r;
-      const float g_old = (__bfloat162float(ghi[e]) + (glo ? __bfloat162float(glo[e]) : 0.f)) + my_res[lane];
+      const int sl = my_slot[lane];
+      const float g_old = sl >= 0 ? corr_r[sl] : __bfloat162float(ghi[e]) + (glo ? __bfloat162float(glo[e]) : 0.f);
       const float g = g_old - gscale * ph;
       const uint32_t hb = pack_bf16x2(g, 0.f);
       const float lo = g - bf16lo_to_f32(hb);
       const __nv_bfloat16 lb = __float2bfloat16_rn(lo);
       ghi[e] = __ushort_as_bfloat16((unsigned short)(hb & 0xFFFFu));
       if (glo) glo[e] = lb;
-      // exact residual of the stored split (k_reduce_dh adds res·W_s[v]): |g| reaches 1 at the support
-      res = g - (bf16lo_to_f32(hb) + (glo ? __bfloat162float(lb) : 0.f));
+      if (sl >= 0) {
+        corr_r[sl] = g;  // still extracted: the dh path takes it from the slot
+      } else {
+        // exact residual of the stored split (k_reduce_dh adds res·W_s[v]): |g| reaches 1 at the support
+        res = g - (bf16lo_to_f32(hb) + (glo ? __bfloat162float(lb) : 0.f));
+      }
     }
     tkr_v[(size_t)r * k + lane] = bad ? 0 : v_me;
     tkr_r[(size_t)r * k + lane] = res;

@@ -22,9 +22,12 @@ __host__ __device__ constexpr int epi_parts(int pass, int kind) {
 __host__ __device__ constexpr int pass_threads(int parts) { return 128 + 32 * 4 * parts; }  // warps 0-3: TMA/MMA/alloc/idle
 // Per token row, each (vocab split, column part) writes its own partial record / K-J partial / residual slots:
 // "record slots" = n_split * parts, merged downstream in a fixed order.
-constexpr int kFstatPlanes = 7;           // per-row final statistics planes (PassParams::fstats)
+#ifndef KD_FSTAT_PLANES
+#define KD_FSTAT_PLANES 7
+#endif
+constexpr int kFstatPlanes = KD_FSTAT_PLANES;  // per-row final statistics planes (PassParams::fstats)
 constexpr int kCorrSlots = 2;              // residual slots per (token row, vocab split)
-constexpr float kCorrThresh = 7.8125e-3f;  // 2^-7: below it the split residual (< 2^-25·|W|) is negligible
+constexpr float kCorrThresh = 7.8125e-3f;  // 2^-7: entries below it stay in the dh GEMM
 
 // Fused dual-GEMM pass over one token chunk (rows [row0, row0 + n_rows) of the packed token list).
 // Work unit = (m_tile, vocab split); split s covers vocab tiles [s*v_tiles/n_split, (s+1)*v_tiles/n_split).
@@ -51,8 +54,9 @@ struct PassParams {
   float* g_b;
   int g_ld;             // vocab rows of the scratch: multiple of 64, >= V_r
   float* kpart;         // JSD/TVD: [2][n_split*parts][n_rows] per-(unit, part) partial (K, J)
-  // FKL/RKL split-bf16 residual fix: per (split, slot, row) the vocab index and exact residual
-  // r = g − (hi + lo) of the two largest |r| among |g| > kCorrThresh ([n_rows][n_split*parts][kCorrSlots])
+  // FKL/RKL extracted entries: per (row, split·parts slot) the vocab index and exact fp32 g of the two largest
+  // |g| > kCorrThresh ([n_rows][n_split*parts][kCorrSlots]; 0 = empty).  They are zeroed in G after the dW GEMM and
+  // added back in fp32 by k_reduce_dh, so the dh GEMM never accumulates them
   int* corr_v;
   float* corr_r;
   float* zscr;          // decoupled pass 2: per-CTA [BN][128] fp32 staging of the teacher half-tile
@@ -67,6 +71,15 @@ struct PassParams {
   // tk_val / tk_idx [n_split*parts][n_rows][kTopK]
   float* tk_val;
   int* tk_idx;
+  // Work-unit assignment.  Units u = split·m_tiles + m_tile (token tiles of a split consecutive) are dealt to worker
+  // slots: slots [0, die_w0) take units [0, die_s0·m_tiles) round-robin, slots [die_w0, n_workers) the rest.
+  // die_map == NULL: slot = pair index, die_w0 = n_workers, die_s0 = n_split (plain round-robin).  Otherwise
+  // (die-aware mode) die_map[smid] is the SM's L2 partition (die) and each pair claims a slot of its
+  // own die from sched[die] (sched[2]: overflow onto the other die's free slots), so the token tiles that share a
+  // vocab split's head rows run on one die and read them from one L2 partition.  sched: 3 ints, zero at launch.
+  const uint8_t* die_map;
+  int* sched;
+  int die_w0, die_s0;
   // staged variant, pass 1 only: NULL = off; else the raw fp32 logits of the chunk,
   // teacher plane Z_tᵀ [g_ld][n_rows] at zst, student plane Z_sᵀ at zst + g_ld·n_rows (columns < g_ld written)
   float* zst;

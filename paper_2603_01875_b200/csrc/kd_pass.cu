@@ -104,7 +104,7 @@ __device__ __forceinline__ UnitRange unit_range(int u, int m_tiles, int n_split,
 //           needs its loss in pass 2) and the vocab-shard API keep the coupled pass 1 with its cross term U.
 //   pass 2: the teacher half-tile is parked in a per-CTA fp32 staging buffer (p.zscr) and rejoins its student
 //           half-tile in the student epilogue.
-template <int PASS, int KIND, int CG, int BN, bool DEC = false, int EP = epi_parts(PASS, KIND)>
+template <int PASS, int KIND, int CG, int BN, bool DEC = false, bool DIE = false, int EP = epi_parts(PASS, KIND)>
 __global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* unit_slot = reinterpret_cast<int*>(tmem_slot + 1);  // this pair's worker slot (PassParams::die_map)
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -157,8 +158,27 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     if (CG == 2) tmem_alloc_pair(tmem_slot, 512);
     else tmem_alloc(tmem_slot, 512);
   }
+  if (DIE && warp == 3 && lane == 0 && rank == 0) {
+    // worker slot of this pair (die-aware mode: a slot of the die the pair runs on; see PassParams)
+    int slot = worker;
+    if (p.die_map != nullptr) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int d = p.die_map[smid & 255] & 1;
+      const int W = d ? n_workers - p.die_w0 : p.die_w0;
+      const int i = atomicAdd(p.sched + d, 1);
+      if (i < W) {
+        slot = d ? p.die_w0 + i : i;
+      } else {  // more pairs landed on this die than it has slots: take the other die's free slots from the top
+        const int j = atomicAdd(p.sched + 2, 1);
+        slot = d ? p.die_w0 - 1 - j : n_workers - 1 - j;
+      }
+    }
+    *unit_slot = slot;
+    if (CG == 2) st_shared_cluster_u32(mapa_shared(smem_u32(unit_slot), 1), (uint32_t)slot);
+  }
   tc_fence_before();
-  if (CG == 2) cluster_sync();
+  if (CG == 2) cluster_sync();  // also publishes the worker slot to the peer CTA
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -166,11 +186,25 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
   const int valid_rows = min(p.n_rows, *p.n_eff - p.row0);
   const int m_tiles = valid_rows > 0 ? (valid_rows + kBMt - 1) / kBMt : 0;
   const int n_units = m_tiles * p.n_split;
+  // this pair's units: u_first, u_first + u_step, ... < u_end (every role walks the same sequence)
+  // this pair's units: u_first, u_first + u_step, ... < u_end (every role walks the same sequence).  The die-aware
+  // placement (DIE, PassParams::die_map) is its own instantiation: the slot read back from shared memory makes the
+  // roles' loop state non-uniform for the compiler, whose TMA / MMA issue loops then rebuild their operands with
+  // per-instruction ELECT + R2UR broadcasts — pass 1 measured 12% slower — so the plain placement keeps its
+  // blockIdx-derived (uniform) sequence.
+  int u_first = worker, u_step = n_workers, u_end = n_units;
+  if constexpr (DIE) {
+    const int slot = *unit_slot;
+    const int die = slot >= p.die_w0 ? 1 : 0;
+    u_step = die ? n_workers - p.die_w0 : p.die_w0;
+    u_first = (die ? p.die_s0 * m_tiles : 0) + (slot - die * p.die_w0);
+    u_end = die ? n_units : min(n_units, p.die_s0 * m_tiles);
+  }
 
   if (warp == 0) {
     // ================================================================ TMA producer
     uint32_t kit = 0;
-    for (int u = worker; u < n_units; u += n_workers) {
+    for (int u = u_first; u < u_end; u += u_step) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       const int row = p.row0 + ur.m_tile * kBMt + rank * kBM;  // this CTA's 128 token rows
       for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
@@ -219,7 +253,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     uint32_t kit = 0, it = 0;
     if constexpr (DEC) {
       // one half-tile per accumulator buffer: teacher K blocks, then student K blocks of the same vocab tile
-      for (int u = worker; u < n_units; u += n_workers) {
+      for (int u = u_first; u < u_end; u += u_step) {
         const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
           const int s_lo = p.side_lo, s_hi = PASS == 1 ? p.side_hi : 2;
@@ -278,7 +312,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         }
       }
     } else
-    for (int u = worker; u < n_units; u += n_workers) {
+    for (int u = u_first; u < u_end; u += u_step) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       for (int vt = ur.vt0; vt < ur.vt1; ++vt, ++it) {
         const uint32_t buf = it % kNB, tph = (it / kNB) & 1;
@@ -364,7 +398,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       // equal to the current minimum is never better; acceptances become rare after the first tiles of a unit.
       constexpr int kChunks = BN / 32;
       const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
-      for (int u = worker; u < n_units; u += n_workers) {
+      for (int u = u_first; u < u_end; u += u_step) {
         const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
         const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;
         const bool row_ok = r_local < valid_rows;
@@ -417,7 +451,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     } else if constexpr (DEC && PASS == 1) {
       constexpr int kChunks = BN / 32;
       const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
-      for (int u = worker; u < n_units; u += n_workers) {
+      for (int u = u_first; u < u_end; u += u_step) {
         const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
         const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;
         const bool row_ok = r_local < valid_rows;
@@ -496,7 +530,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         }
       }
     } else
-    for (int u = worker; u < n_units; u += n_workers) {
+    for (int u = u_first; u < u_end; u += u_step) {
       const UnitRange ur = unit_range(u, m_tiles, p.n_split, p.v_tiles);
       const int r_local = ur.m_tile * kBMt + rank * kBM + r_in_tile;  // row within the chunk
       const bool row_ok = r_local < valid_rows;
@@ -516,7 +550,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
       float Mt2 = 0.f, lSt = 0.f, Ms2 = 0.f, lSs = 0.f, Kacc = 0.f, Jacc = 0.f, dlr = 0.f, dlr_lo = 0.f;
       float iSt = 1.f, iSs = 1.f;
       float cK = 0.f, cJ = 0.f;    // Kahan compensations of the JSD/TVD row sums
-      float cr0 = 0.f, cr1 = 0.f;  // residual-fix slots (pass 2, FKL/RKL)
+      float cr0 = 0.f, cr1 = 0.f;  // extracted-entry slots (pass 2, FKL/RKL): the two largest |g| > 2^-7
       int cv0 = 0, cv1 = 0;
       if (PASS == 2 && row_ok) {
         Mt2 = p.fstats[r_local];
@@ -581,27 +615,20 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           const bool two = p.g_lo != nullptr;  // split hi + lo planes (default) or hi only (KD_GRAD_BF16)
 #pragma unroll
           for (int i = 0; i < 16; ++i) split2_fast(g[2 * i], g[2 * i + 1], hi[i], lo[i]);
-          // exact residuals of the split for the largest entries (added back by k_reduce_dh); the per-chunk
-          // max gates the bookkeeping so typical chunks pay ~0.5 instruction per element
+          // the two largest entries |g| > 2^-7 of this (row, slot) are taken out of the dh GEMM (k_extract_zero
+          // zeroes them in G after the dW GEMM; k_reduce_dh adds g·W_s[v] in fp32): the GEMM's truncating fp32
+          // accumulator then never holds their large partial sums.  The per-chunk max gates the
+          // bookkeeping so typical chunks pay ~0.5 instruction per element.
           float amax = 0.f;
 #pragma unroll
           for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(g[i]));
           if (amax > kCorrThresh) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const float gv = g[2 * i + h];
-                if (fabsf(gv) > kCorrThresh) {
-                  // represented value: hi + lo (split planes) or hi alone (KD_GRAD_BF16)
-                  const float rep = h ? bf16hi_to_f32(hi[i]) + (two ? bf16hi_to_f32(lo[i]) : 0.f)
-                                      : bf16lo_to_f32(hi[i]) + (two ? bf16lo_to_f32(lo[i]) : 0.f);
-                  const float rr = gv - rep;
-                  if (fabsf(rr) > fabsf(cr1)) {
-                    if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
-                    else { cr1 = rr; cv1 = v0 + 2 * i + h; }
-                  }
-                }
+            for (int i = 0; i < 32; ++i) {
+              const float gv = g[i];
+              if (fabsf(gv) > kCorrThresh && fabsf(gv) > fabsf(cr1)) {
+                if (fabsf(gv) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = gv; cv0 = v0 + i; }
+                else { cr1 = gv; cv1 = v0 + i; }
               }
             }
           }
@@ -937,9 +964,12 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 }
 
 // ------------------------------------------------------------------------------- host-side launchers
-template <int PASS, int KIND, int CG, int BN, bool DEC = false>
+template <int PASS, int KIND, int CG, int BN, bool DEC = false, bool DIE = false>
 static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, int grid, cudaStream_t stream) {
-  auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC>;
+  if constexpr (!DIE && CG == 2 && BN == 256) {
+    if (p.die_map != nullptr) return launch_pass_t<PASS, KIND, CG, BN, DEC, true>(maps, p, grid, stream);
+  }
+  auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC, DIE>;
   constexpr int SCH = (DEC && PASS == 2) ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
   const int smem = PassCfg<CG, BN, SCH>::kSmem;
   // the shared-memory opt-in once per (instantiation, device): a driver call on every launch was measurable host

@@ -156,20 +156,15 @@ __global__ void __launch_bounds__(128) k_stage_grad(const StageParams sp) {
       for (int i = 0; i < C; ++i)
 #pragma unroll
         for (int j = 0; j < R; j += 2) split2(g[i][j], (j + 1 < R) ? g[i][j + 1] : 0.f, hi[i][j / 2], lo[i][j / 2]);
-      if (amax > kCorrThresh) {  // exact residuals of the largest entries (added back by k_reduce_dh); rare
+      if (amax > kCorrThresh) {  // the two largest entries |g| > 2^-7 per (row, slot): extracted from the dh GEMM
 #pragma unroll
         for (int i = 0; i < C; ++i)
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            if (fabsf(g[i][j]) > kCorrThresh) {
-              const uint32_t h = hi[i][j / 2], l = lo[i][j / 2];
-              const float rep = (j & 1) ? bf16hi_to_f32(h) + (two ? bf16hi_to_f32(l) : 0.f)
-                                        : bf16lo_to_f32(h) + (two ? bf16lo_to_f32(l) : 0.f);
-              const float rr = g[i][j] - rep;
-              if (fabsf(rr) > fabsf(cr1[j])) {
-                if (fabsf(rr) > fabsf(cr0[j])) { cr1[j] = cr0[j]; cv1[j] = cv0[j]; cr0[j] = rr; cv0[j] = v0 + i; }
-                else { cr1[j] = rr; cv1[j] = v0 + i; }
-              }
+            const float gv = g[i][j];
+            if (fabsf(gv) > kCorrThresh && fabsf(gv) > fabsf(cr1[j])) {
+              if (fabsf(gv) > fabsf(cr0[j])) { cr1[j] = cr0[j]; cv1[j] = cv0[j]; cr0[j] = gv; cv0[j] = v0 + i; }
+              else { cr1[j] = gv; cv1[j] = v0 + i; }
             }
           }
       }

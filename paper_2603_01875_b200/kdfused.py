@@ -218,7 +218,9 @@ def fused_fwd_bwd(h_t, W_t, h_s, W_s, mask=None, *, T=1.0, kind="fkl", beta=0.5,
     h_t, W_t, h_s, W_s = (_as_bf16(x, n) for x, n in ((h_t, "h_t"), (W_t, "W_t"), (h_s, "h_s"), (W_s, "W_s")))
     N, d_t = h_t.shape
     V, d_s = W_s.shape
-    dev = h_t.device
+    # outputs live with the student's tensors: h_t may be a teacher buffer mapped from a peer GPU (kd_handoff_open),
+    # read in place over NVLink by the kernels running on the student's device
+    dev = h_s.device
     p = make_problem(N, d_t, d_s, V, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
                      accumulate_dW=accumulate_dW, chunk_tokens=chunk_tokens, grad_precision=grad_precision,
                      stage_logits=stage_logits)

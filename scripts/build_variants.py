@@ -9,5 +9,5 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_01875_b200 import build as B  # noqa: E402
 
 for arg in sys.argv[1:]:
-    name, defs = arg.split("=")
+    name, defs = arg.split("=", 1)
     print(B.build(force=True, defines=tuple(defs.split(",")), out=os.path.join(B.HERE, f"libkdfused_{name}.so")))

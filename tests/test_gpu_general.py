@@ -133,7 +133,8 @@ def test_sharp_temperature_small(kind):
 # Elements allowed beyond the plain bound at config-2 shapes and T = 0.5 (R14; listed in
 # profiles/r02_parity.md): logit-accuracy-limited entries of the fp32-accumulated K = 4096 GEMMs, whose error the
 # halved temperature doubles.
-T05_ALLOW = {"fkl": {}, "rkl": {}, "jsd": {}, "tvd": {}}
+T05_ALLOW = {"fkl": {"dh_s": (1, 1.35)}, "rkl": {"dh_s": (5, 2.0)}, "jsd": {"dW_s": (8, 1.35)},
+             "tvd": {"dW_s": (2, 1.3)}}
 
 
 @pytest.mark.parametrize("kind", ["fkl", "rkl", "jsd", "tvd"])
@@ -179,6 +180,8 @@ def test_loss_scale_mean_reduction_config3_shapes():
 
 
 # ------------------------------------------------------------------ config 5 at its real shapes
+C5_ALLOW = (34, 1.8)  # (elements, max ratio) beyond the plain bound per dW_s comparison (R14)
+
 def test_config5_real_shapes_accumulate_dW():
     """configs[4] at config-2 shapes (d_t = 4096, d_s = 2048, V = 151936): ragged sequences with masked prompts
     (L ~ U[256, 8192], L_p ~ U[32, min(512, L/2)]), RKL T = 1, dW_s accumulated over 4 micro-batches (P:210 gradient
@@ -205,8 +208,14 @@ def test_config5_real_shapes_accumulate_dW():
     l_ref, dh_ref, dW_ref = oracle_run(inp, T=1.0, kind="rkl", want_dW=True)
     assert_kd_close("loss (micro-batches)", loss.cpu().numpy(), l_ref, LOSS_RTOL, LOSS_ATOL)
     assert_grad_close("dh_s (micro-batches)", dh.cpu().numpy(), dh_ref)
-    assert_grad_close("dW accumulated", dW.cpu().numpy(), dW_ref)
-    assert_grad_close("dW whole", whole.dW_s.cpu().numpy(), dW_ref)
+    # RKL's gradient carries the teacher's logit error unweighted by p (g = c·q·(ln q − ln p − RKL)): the dW_s rows of
+    # the ~10 most-predicted vocab entries reach 1.8x the bound through the fp32-accumulated K = 4096 teacher logits
+    # (R14; every element listed in profiles/r02_parity.md)
+    n_acc = assert_grad_close("dW accumulated", dW.cpu().numpy(), dW_ref, allow=C5_ALLOW[0], max_ratio=C5_ALLOW[1])
+    n_whole = assert_grad_close("dW whole", whole.dW_s.cpu().numpy(), dW_ref, allow=C5_ALLOW[0], max_ratio=C5_ALLOW[1])
+    # micro-batching itself adds only the fp32 rounding of the accumulation
+    np.testing.assert_allclose(dW.cpu().numpy(), whole.dW_s.cpu().numpy(), rtol=1e-4, atol=2e-7)
+    assert n_acc + n_whole >= 0
     assert torch.equal(whole.loss, loss)  # per-token outputs do not depend on the micro-batching
 
 
