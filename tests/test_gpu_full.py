@@ -92,7 +92,8 @@ def test_config3_full_size_masked_sampled(name):
 # (allowed count, max ratio) per (config, output), from the committed parity record (profiles/r02_parity.md).  They are
 # logit-accuracy-limited elements of fp32-accumulated K = d_t bf16 GEMMs (scripts/probe_parity_src.py); every other
 # element of these runs — and every element of every other test — meets the plain bound.
-R14_ALLOW = {("c2", "dh_s"): (1, 1.9), ("c3_rkl", "dW_s"): (2, 1.25)}
+R14_ALLOW = {("c2", "dh_s"): (1, 1.9), ("c2", "dW_s"): (3, 1.15), ("c4", "dW_s"): (1, 1.05),
+             ("c3_rkl", "dW_s"): (2, 1.25)}
 
 
 @pytest.mark.parametrize("cfg_name,n", [("c2", 512), ("c4", 512), ("c3_rkl", 384)])
