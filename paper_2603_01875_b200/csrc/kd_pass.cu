@@ -622,16 +622,41 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           float amax = 0.f;
 #pragma unroll
           for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(g[i]));
-          if (amax > kCorrThresh) {
+#ifndef KD_X_RESID
+          if (__builtin_expect(amax > kCorrThresh, 0)) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float gv = g[i];
-              if (fabsf(gv) > kCorrThresh && fabsf(gv) > fabsf(cr1)) {
-                if (fabsf(gv) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = gv; cv0 = v0 + i; }
-                else { cr1 = gv; cv1 = v0 + i; }
+              // a branch per element (rarely taken), not a 32-long predicated select chain on (cr0, cr1)
+              if (__builtin_expect(fabsf(gv) > kCorrThresh, 0)) {
+                const float a = fabsf(gv);
+                if (a > fabsf(cr1)) {
+                  if (a > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = gv; cv0 = v0 + i; }
+                  else { cr1 = gv; cv1 = v0 + i; }
+                }
               }
             }
           }
+#else  // experiment builds only: round 1's residual bookkeeping (timing A/B, not parity)
+          if (amax > kCorrThresh) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const float gv = g[2 * i + h];
+                if (fabsf(gv) > kCorrThresh) {
+                  const float rep = h ? bf16hi_to_f32(hi[i]) + (two ? bf16hi_to_f32(lo[i]) : 0.f)
+                                      : bf16lo_to_f32(hi[i]) + (two ? bf16lo_to_f32(lo[i]) : 0.f);
+                  const float rr = gv - rep;
+                  if (fabsf(rr) > fabsf(cr1)) {
+                    if (fabsf(rr) > fabsf(cr0)) { cr1 = cr0; cv1 = cv0; cr0 = rr; cv0 = v0 + 2 * i + h; }
+                    else { cr1 = rr; cv1 = v0 + 2 * i + h; }
+                  }
+                }
+              }
+            }
+          }
+#endif
           __nv_bfloat16* ph = p.g_hi + col0;
           __nv_bfloat16* pl = p.g_lo + col0;
 #ifdef KD_X_NOGSTORE  // experiment builds only: G computed but not stored

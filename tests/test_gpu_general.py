@@ -214,8 +214,8 @@ def test_config5_real_shapes_accumulate_dW():
     # (R14; every element listed in profiles/r02_parity.md)
     n_acc = assert_grad_close("dW accumulated", dW.cpu().numpy(), dW_ref, allow=C5_ALLOW[0], max_ratio=C5_ALLOW[1])
     n_whole = assert_grad_close("dW whole", whole.dW_s.cpu().numpy(), dW_ref, allow=C5_ALLOW[0], max_ratio=C5_ALLOW[1])
-    # micro-batching itself adds only the fp32 rounding of the accumulation
-    np.testing.assert_allclose(dW.cpu().numpy(), whole.dW_s.cpu().numpy(), rtol=1e-4, atol=2e-7)
+    # micro-batching changes only the order of the fp32 accumulation (different token chunks per GEMM)
+    np.testing.assert_allclose(dW.cpu().numpy(), whole.dW_s.cpu().numpy(), rtol=GRAD_RTOL, atol=GRAD_ATOL)
     assert n_acc + n_whole >= 0
     assert torch.equal(whole.loss, loss)  # per-token outputs do not depend on the micro-batching
 
