@@ -217,7 +217,9 @@ def test_config5_real_shapes_accumulate_dW():
     # micro-batching changes only the order of the fp32 accumulation (different token chunks per GEMM)
     np.testing.assert_allclose(dW.cpu().numpy(), whole.dW_s.cpu().numpy(), rtol=GRAD_RTOL, atol=GRAD_ATOL)
     assert n_acc + n_whole >= 0
-    assert torch.equal(whole.loss, loss)  # per-token outputs do not depend on the micro-batching
+    # per-token outputs depend on the micro-batching only through the vocab split the planner picks for the batch size
+    # (the order the per-split records merge in): fp32-rounding close
+    np.testing.assert_allclose(whole.loss.cpu().numpy(), loss.cpu().numpy(), rtol=1e-5, atol=1e-7)
 
 
 # ------------------------------------------------------------------ vocab shards with beta != 1/2
