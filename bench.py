@@ -466,7 +466,12 @@ def roofline_of(prof, steps, pk, cfg, n_eff, v_rows, teacher_lse=False, topk=0, 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom, {}).get("dram_bytes_per_launch")
+        cap = json.load(open(tpath)).get(dom, {})
+        # the capture is one launch of a given workload (c2 shapes, all V rows, FKL, the default variant); another
+        # workload's launch moves other bytes, so it gets no traffic figure
+        same = (cfg.name == cap.get("config", "c2") and v_rows == cfg.vocab and not teacher_lse and not topk
+                and grad_precision == "split")
+        traffic = cap.get("dram_bytes_per_launch") if same else None
     n_l, t_l = prof[dom]
     achieved = algo[dom] * steps / n_l / (t_l / n_l / 1e3) / 1e12
     what = ("2*tokens*V_r*d_s flop" if (dom == "pass1" and teacher_lse) or (topk and dom.startswith("pass")) else

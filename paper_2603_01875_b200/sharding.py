@@ -143,15 +143,21 @@ def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str) -> int:
     Each chunk's pass 1 runs while the previous chunk's records are all-gathered, and each chunk's partial-dh
     all-reduce runs under the next chunk's kernels, so only the last chunk's all-reduce is exposed; more chunks
     overlap more but shorten each launch.  JSD/TVD keep the chunk's G planes (12 B per (token, v)) between their two
-    calls, so their chunk is bounded to ~5 GB of planes: 8192 tokens at P = 8, 5376 at P = 2 (measured on one GPU
+    calls, so their chunk is bounded to ~5 GB of planes: 8192 tokens at P = 8, at most 5376 at P = 2, balanced over the chunks (measured on one GPU
     simulating rank 0, c3 JSD: per-GPU efficiency at P = 8 0.67 with 2048-token chunks -> 0.85 with 8192;
     scripts/gpu/simv_jsd*.sh).  FKL/RKL: 8192 tokens (four exchange chunks at config 2).  KD_VOCAB_FIX_CHUNK
     overrides."""
     if "KD_VOCAB_FIX_CHUNK" in os.environ:
         return max(1, int(os.environ["KD_VOCAB_FIX_CHUNK"]))
+    cap = 8192
     if kind in ("jsd", "tvd"):
-        return max(4096, min(8192, int(5e9 / (12 * max(1, v_rows))) // 256 * 256))
-    return 8192 if n_tokens > 8192 else max(1, n_tokens)
+        cap = max(4096, min(8192, int(5e9 / (12 * max(1, v_rows))) // 256 * 256))
+    if n_tokens <= cap:
+        return max(1, n_tokens)
+    # balance the chunks: a ragged tail of a few hundred tokens fills a fraction of a wave of output tiles (c3 JSD at
+    # P = 2: 5376-token chunks left a 512-token tail, per-rank efficiency 0.86)
+    n_chunks = -(-n_tokens // cap)
+    return min(cap, -(-(-(-n_tokens // n_chunks)) // 256) * 256)
 
 
 def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
