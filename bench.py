@@ -70,6 +70,14 @@ def parse():
     ap.add_argument("--sim-vocab-shards", type=int, default=0,
                     help="1 GPU: time rank 0's share of a P-way vocab-sharded strong-scaling step (all tokens, its "
                          "V/P head rows; compute only, identity exchanges) and report the projected efficiency")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 vocab-sharded FKL/RKL step: the partial-dh exchange over NCCL (default) or the library's "
+                         "peer-memory exchange (kd_vocab_backward_p2p: dh rows stored from the dh reduction straight "
+                         "into the owners' slots over NVLink, owners' rank-order sums stored into every rank; CUDA IPC "
+                         "arenas mapped once before the timing)")
+    ap.add_argument("--sim-p2p", type=int, default=0,
+                    help="1 GPU: run the P-rank peer-exchange step emulated on this GPU (every rank's kernels in one "
+                         "stream, local arenas as the peers) and report its time and kernel split alongside")
     ap.add_argument("--topk", type=int, default=0,
                     help="SURVEY §8(f) NEXT-3 negative control: the prior-art top-k teacher transfer (k <= 32).  The "
                          "teacher's (idx, logit) top-k is produced once by kd_teacher_topk outside the timed region; "
@@ -324,6 +332,10 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     dW = torch.empty(v1 - v0, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
     kw = dict(vocab=cfg.vocab, v_begin=v0, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0,
               want_dW=want_dW, accumulate_dW=False, group=group, dh_reduce="scatter" if own_tokens else "all")
+    p2p = (args.exchange == "p2p" and world > 1 and not sim and not own_tokens and cfg.kind in ("fkl", "rkl"))
+    if p2p:  # arenas allocated and peer-mapped once (CUDA IPC), outside the timing
+        chunk_p2p = sharding.default_exchange_chunk(n_all, v1 - v0, cfg.kind)
+        kw["exchange"] = sharding.P2PExchange.create(group, cfg.d_s, max_rows=chunk_p2p, max_tokens=n_all, device=dev)
     res = {}
 
     def step():
@@ -347,8 +359,13 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
            "exchange_bytes_per_step_per_rank": {
                "records_allgather": rec_bytes, "kj_allgather": kj_bytes,
                ("dh_reduce_scatter" if own_tokens else "dh_allreduce_payload"): dh_bytes},
-           "pipeline": "per exchange chunk: pass 1 of chunk c+1 under the records all-gather of chunk c; the partial-dh "
-                       "all-reduce of chunk c under chunk c+1's kernels (NCCL stream); only the last chunk's is exposed",
+           "pipeline": ("per exchange chunk: pass 1 of chunk c+1 under the records all-gather of chunk c; the partial "
+                        "dh rows stored by the dh reduction into their owners' slots (NVLink peer memory), the owners' "
+                        "rank-order sums of chunk c stored into every rank after chunk c+1's kernels (kd_p2p)"
+                        if p2p else
+                        "per exchange chunk: pass 1 of chunk c+1 under the records all-gather of chunk c; the partial-dh "
+                        "all-reduce of chunk c under chunk c+1's kernels (NCCL stream); only the last chunk's is exposed"),
+           "dh_exchange": "p2p (library kernels over peer memory)" if p2p else "nccl",
            "loss_finite": bool(torch.isfinite(r.loss).all().item()),
            "kernels_ms_per_step": {k: v / args.steps for k, (n, v) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
            "gpu_launches_per_step": sum(n for n, _ in prof.values()) / args.steps, "_prof": prof,
@@ -359,6 +376,34 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
                             f"communication.  value = the job's tokens / this time, i.e. the P-GPU strong-scaling "
                             f"throughput excluding the exchanges")
     return out
+
+
+def p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW):
+    """--sim-p2p P: the P-rank peer-exchange step emulated on one GPU (sharding.vocab_sharded_p2p_one_gpu): every
+    rank's kernels in one stream, the peers' arenas local.  The time is the whole job's compute serialised on one GPU
+    (so tokens/s ~ the single-GPU headline) plus the exchange kernels; their cost per rank is in the kernel split
+    ("p2p": owner sums + counters; the peer stores ride inside reduce_dh).  Local HBM stands in for NVLink."""
+    from paper_2603_01875_b200 import sharding
+    P = args.sim_p2p
+    n = Ht.shape[0]
+    chunk = sharding.default_exchange_chunk(n, -(-cfg.vocab // P), cfg.kind)
+    exs = sharding.P2PExchange.local_group(P, cfg.d_s, max_rows=chunk, max_tokens=n, device=Ht.device)
+    res = {}
+
+    def step():
+        res["r"] = sharding.vocab_sharded_p2p_one_gpu(Ht, Wt, Hs, Ws, mask, exchanges=exs, T=cfg.temperature,
+                                                     kind=cfg.kind, want_dW=want_dW, exchange_chunk=chunk)
+
+    t = timer.run(step, args.steps, args.warmup)
+    prof = timer.profiled(kd, step, args.steps)
+    n_eff = int(mask.sum().item()) if mask is not None else n
+    import torch
+    same = all(torch.equal(res["r"][0][1], o[1]) for o in res["r"][1:])
+    return {"ranks_emulated": P, "value": n_eff / (t["median_ms"] / 1e3), "unit": UNIT, "ms_per_step": t["median_ms"],
+            "exchange_chunk_tokens": chunk, "all_ranks_same_dh": bool(same),
+            "kernels_ms_per_step": {k: v / args.steps for k, (c, v) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            "note": "one GPU runs all P ranks' kernels (no concurrency needed: every counter a kernel waits on was "
+                    "raised by an earlier launch); the 'peer' stores go to local HBM, not NVLink"}
 
 
 # ------------------------------------------------------------------------------------------- hand-off leg
@@ -790,6 +835,9 @@ def main():
                 "bound": "hbm", "achieved": b / (t_l / n_l / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": b / (t_l / n_l / 1e3) / 1e9 / pk["hbm_gbs"],
                 "algorithmic_per_launch": f"tokens*V*(8 + {wb}) B = {b:.4g}"}
+
+    if args.sim_p2p > 1 and world == 1 and cfg.kind in ("fkl", "rkl"):
+        alongside["p2p_one_gpu"] = p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW)
 
     if args.handoff and world == 1:
         alongside["handoff"] = handoff_leg(args, cfg, kd, H_t, Ht, Wt, Hs, Ws, mask, kw, out, dW, n_eff, stream, local)

@@ -183,6 +183,64 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
                             float* loss, float* dh_s_partial, float* dW_s, int64_t* n_nonfinite,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- peer-memory exchange of the FKL/RKL vocab-sharded step (the north star's "NCCL
+ * all-reduce over NVLink" of the partial dh_s done by the library's own kernels over NVSwitch peer memory).
+ * The partial dh_s / FKL loss rows of a shard leave the dh split-K reduction (k_reduce_dh) and the loss
+ * reduction straight into the OWNING rank's receive slot — a reduce-scatter fused into the kernel that
+ * produces the rows — and the owner sums the P partials in rank order (deterministic) and stores the sum
+ * into every rank's output: a two-shot all-reduce, 2(P-1)/P x the chunk's bytes per rank on the wire.
+ *
+ * Arena (one per rank, kd_p2p_arena_bytes, device memory, 256-byte aligned, ZEROED by its owner before
+ * first use; every rank maps every other rank's arena, e.g. kd_handoff_export/open = CUDA IPC over NVLink):
+ *   [0, 256)   counters: u32 arrivals at byte 0 (+1 per rank per exchange chunk, raised by each pushing
+ *              rank), u32 done at byte 4 (+1 per owner per exchange chunk, raised by each owner).
+ *              Counters only grow (modulo 2^32, compared wrap-safe); the caller tracks the targets:
+ *              after k exchange chunks every counter of every rank is k*world.
+ *   then       kP2P sets (3) of receive slots [world][R][d_s] f32 and of loss slots [world][R] f32,
+ *              R = ceil(max_rows / world); dh_out [max_tokens][d_s] f32; loss_out [max_tokens] f32.
+ * Protocol per exchange chunk c (n_c <= max_rows tokens, rows [row0, row0 + n_c) of the step), every rank:
+ *   kd_vocab_backward_p2p(set = c % 3)        pushes its partials; then arrivals of every owner += 1
+ *   kd_p2p_combine(set = c % 3, target = (c+1)*world + base)   owner of rows [me*R_c, (me+1)*R_c) of the
+ *                                              chunk (R_c = ceil(n_c / world)): waits for the arrivals,
+ *                                              sums, stores into every rank's dh_out/loss_out rows
+ *                                              row0 + ..., masked rows 0; then done of every rank += 1
+ *   kd_p2p_wait(done target)                  before a slot set is reused (chunk c+3 waits for
+ *                                              done >= (c+1)*world + base) and before dh_out/loss_out
+ *                                              are read (done >= n_chunks*world + base)
+ * A rank may defer kd_p2p_combine(c) behind its next chunk's kernels (sharding.py does), hiding the wait.
+ * Waits are bounded: a counter that does not arrive within ~60 s traps the kernel (the launch fails with
+ * a CUDA error) instead of hanging the device.  world <= 8; all ranks pass identical problem shapes. */
+#define KD_P2P_MAX_RANKS 8
+typedef struct {
+  int32_t world;       /* ranks of the vocab group, 1..8 */
+  int32_t rank;        /* this rank's index */
+  int32_t d_s;         /* student width (multiple of 4) */
+  int32_t reserved;
+  int64_t max_rows;    /* capacity: tokens per exchange chunk */
+  int64_t max_tokens;  /* capacity of dh_out / loss_out: tokens per step */
+  void* arena[KD_P2P_MAX_RANKS]; /* every rank's arena as mapped in THIS process (arena[rank]: own) */
+} kd_p2p;
+/* Bytes of one rank's arena; 0 for invalid arguments. */
+size_t kd_p2p_arena_bytes(int32_t world, int64_t max_rows, int64_t max_tokens, int32_t d_s);
+/* Device pointers of this rank's dh_out [max_tokens][d_s] and loss_out [max_tokens] inside its arena. */
+kd_status kd_p2p_outputs(const kd_p2p* x, float** dh_out, float** loss_out);
+/* kd_vocab_backward with the exchange: no dh_s_partial argument (the rows go to the owners' slots);
+ * `loss`: RKL -> the full per-token loss (as kd_vocab_backward, local), FKL -> unused (NULL allowed; the
+ * partial loss goes to the owners and the sum lands in loss_out).  n_ranks must equal x->world.
+ * Errors: as kd_vocab_backward; KD_ERR_INVALID_ARG for a bad set / rank / world; KD_ERR_SHAPE if
+ * n_tokens > max_rows or d_s != x->d_s; KD_ERR_ALIGNMENT for an arena not 256-byte aligned. */
+kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
+                                float* loss, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                                size_t workspace_bytes, const kd_p2p* x, int32_t set, void* stream);
+/* Owner side of exchange chunk `set`: n_rows = the chunk's tokens, row0 = its first row in dh_out,
+ * mask = the chunk's mask [n_rows] or NULL, with_loss = 1 for FKL (sum the partial losses).
+ * Errors: KD_ERR_SHAPE if n_rows > max_rows or row0 + n_rows > max_tokens. */
+kd_status kd_p2p_combine(const kd_p2p* x, int32_t set, int64_t n_rows, int64_t row0, const uint8_t* mask,
+                         int32_t with_loss, uint32_t arrivals_target, void* stream);
+/* Holds `stream` until this rank's done counter reaches done_target (wrap-safe). */
+kd_status kd_p2p_wait(const kd_p2p* x, uint32_t done_target, void* stream);
+
 /* ---- JSD / TVD vocab shards: one more exchange.  The JSD gradient needs the per-token
  * K = KL(q||m) = sum over the FULL vocabulary (the TVD one sum_v q*sign(q - p)), known only after every
  * shard's pass 2 (R4, R5).  Per token chunk (n_tokens <= the chunk, KD_ERR_SHAPE otherwise; the

@@ -35,7 +35,7 @@ cudaError_t launch_merge(const float* part, long long plane, long long split_str
                          int row0, const int* n_eff, int kind, int mode, float* fstats, float* loss, float* rec,
                          long long rec_plane, const int* idx, int orig_rows, long long* nonfinite, int write_loss,
                          cudaStream_t s, const float* tstats_in = nullptr);
-cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, float* loss,
+cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, const RowDst& loss,
                              const int* idx, long long* nonfinite, cudaStream_t s);
 cudaError_t launch_kfix(const float* kpart, int n_split, int n_rows, int row0, const int* n_eff, int kind, float beta,
                         float* kfin, float* loss, const int* idx, long long* nonfinite, const float* ga,
@@ -49,9 +49,12 @@ cudaError_t launch_die_probe(const unsigned* buf, const long long* line_off, int
 int stage_rows();
 int stage_cols();
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
-                             const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
-                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v = nullptr,
-                             const float* corr2_r = nullptr, int n_slots2 = 0);
+                             const int* n_eff, const int* idx, const RowDst& dh, const int* corr_v,
+                             const float* corr_r, int n_slots, const __nv_bfloat16* Ws, cudaStream_t s,
+                             const int* corr2_v = nullptr, const float* corr2_r = nullptr, int n_slots2 = 0);
+cudaError_t launch_p2p_signal(const P2PFlags& f, cudaStream_t s);
+cudaError_t launch_p2p_wait(const unsigned* flag, unsigned target, cudaStream_t s);
+cudaError_t launch_p2p_combine(const P2PCombine& c, int num_sms, cudaStream_t s);
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
 cudaError_t launch_extract_zero(const int* corr_v, const float* corr_r, int n_slots, int n_rows, int row0,
                                 const int* n_eff, __nv_bfloat16* ghi, __nv_bfloat16* glo, cudaStream_t s);
@@ -91,10 +94,10 @@ static kd_status fail(kd_status st, const char* fmt, ...) {
 // When enabled, every launch is bracketed by two CUDA events on the launch stream; kd_profile_read()
 // resolves them into per-kernel totals (bench.py uses this for the live roofline figure).
 enum KernelId : int { K_COMPACT, K_GATHER, K_ZERO, K_PASS1, K_MERGE, K_PASS2, K_KFIX, K_GEMM_DH, K_REDUCE_DH,
-                      K_GEMM_DW, K_GEMM, K_TOPK, K_STAGE_GRAD, K_NUM };
+                      K_GEMM_DW, K_GEMM, K_TOPK, K_STAGE_GRAD, K_P2P, K_NUM };
 static const char* kKernelNames[K_NUM] = {"compact", "gather", "zero_masked", "pass1", "merge", "pass2",
                                           "kfix", "gemm_dh", "reduce_dh", "gemm_dW", "gemm", "topk",
-                                          "stage_grad"};
+                                          "stage_grad", "p2p"};
 struct ProfRec { int id; cudaEvent_t a, b; };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -766,7 +769,7 @@ static kd_status grad_chunk(Ctx& c, int row0, int side_lo = 0) {
 
 // After pass 2: [JSD/TVD fix-up with the local K partials, or with the P ranks' per-token totals kj_ranks]
 // + dh GEMM (+ split-K reduce) + dW GEMM for one chunk.
-static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW, const float* kj_ranks,
+static kd_status finish_chunk(Ctx& c, int row0, float* loss, const RowDst& dh, float* dW, const float* kj_ranks,
                               int n_ranks, int topk = 0) {
   const Plan& P = c.P;
   const kd_problem* p = c.p;
@@ -838,7 +841,7 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, float* dh, float* d
   return KD_OK;
 }
 
-static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float* dW) {
+static kd_status backward_chunk(Ctx& c, int row0, float* loss, const RowDst& dh, float* dW) {
   kd_status st = grad_chunk(c, row0);
   if (st != KD_OK) return st;
   return finish_chunk(c, row0, loss, dh, dW, nullptr, 0);
@@ -846,8 +849,10 @@ static kd_status backward_chunk(Ctx& c, int row0, float* loss, float* dh, float*
 
 static kd_status check_common(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
                               const void* W_s, float* loss, float* dh, float* dW, void* ws, size_t ws_bytes,
-                              const Plan& P) {
-  if (P.N > 0 && (!h_t || !h_s || !loss || !dh)) return fail(KD_ERR_INVALID_ARG, "NULL input/output pointer");
+                              const Plan& P, bool local_out = true) {
+  // local_out = false: the peer exchange (kd_vocab_backward_p2p) sends dh / the FKL loss to the owners' slots
+  if (P.N > 0 && (!h_t || !h_s || (local_out && (!loss || !dh))))
+    return fail(KD_ERR_INVALID_ARG, "NULL input/output pointer");
   if (!W_t || !W_s) return fail(KD_ERR_INVALID_ARG, "NULL LM-head pointer");
   if (p->want_dW && !dW) return fail(KD_ERR_INVALID_ARG, "want_dW set but dW_s is NULL");
   const void* ptrs[] = {h_t, W_t, h_s, W_s, loss, dh, dW};
@@ -933,12 +938,12 @@ static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_
       sp.corr_v = pp.corr_v;
       sp.corr_r = pp.corr_r;
       KD_LAUNCH(K_STAGE_GRAD, launch_stage_grad(P.kind, sp, P.n_gslots, c.s));
-      if ((st = finish_chunk(c, row0, loss, dh_s, dW, nullptr, 0)) != KD_OK) return st;
-    } else if ((st = backward_chunk(c, row0, loss, dh_s, dW)) != KD_OK) {
+      if ((st = finish_chunk(c, row0, loss, local_rows(dh_s, P.d_s), dW, nullptr, 0)) != KD_OK) return st;
+    } else if ((st = backward_chunk(c, row0, loss, local_rows(dh_s, P.d_s), dW)) != KD_OK) {
       return st;
     }
     if (P.kind == KD_FKL)
-      KD_LAUNCH(K_MERGE, launch_loss_rows(pp.kpart, P.n_gslots, P.Nc, row0, c.n_eff, loss, c.idx,
+      KD_LAUNCH(K_MERGE, launch_loss_rows(pp.kpart, P.n_gslots, P.Nc, row0, c.n_eff, local_rows(loss, 1), c.idx,
                                           c.nonfinite, c.s));
   }
   return KD_OK;
@@ -1070,7 +1075,7 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
                                       pp.alpha, pp.fstats, pp.gscale, pp.g_hi, pp.g_lo, pp.corr_v, pp.corr_r,
                                       P.n_split * epi_parts(2, P.kind) * kCorrSlots, ws_at<int>(c.ws, P.off_tkr_v),
                                       ws_at<float>(c.ws, P.off_tkr_r), loss, c.nonfinite, c.s));
-    if ((st = finish_chunk(c, row0, loss, dh_s, dW, nullptr, 0, k)) != KD_OK) return st;
+    if ((st = finish_chunk(c, row0, loss, local_rows(dh_s, P.d_s), dW, nullptr, 0, k)) != KD_OK) return st;
   }
   return KD_OK;
 }
@@ -1110,12 +1115,13 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   return KD_OK;
 }
 
-kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
-                            const uint8_t* mask, const float* recs, int32_t n_ranks, float* loss,
-                            float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
-                            size_t workspace_bytes, void* stream) {
-  g_launches = 0;
-  g_cur_stream = static_cast<cudaStream_t>(stream);
+// The FKL/RKL shard backward behind kd_vocab_backward (dh / FKL loss rows into local buffers) and
+// kd_vocab_backward_p2p (the same rows stored straight into the owning ranks' receive slots, RowDst).
+static kd_status vocab_backward_impl(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                     const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
+                                     float* loss, float* dh_local, const RowDst& dh_dst, const RowDst& floss_dst,
+                                     float* dW_s, int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
+                                     void* stream, bool p2p) {
   kd_status st = validate_unstaged(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL && p->kind != KD_RKL)
@@ -1128,7 +1134,8 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
   c.ws = workspace;
   attach_die(c);
   float* dW = p->want_dW ? dW_s : nullptr;
-  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s_partial, dW, workspace, workspace_bytes, c.P)) != KD_OK)
+  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_local, dW, workspace, workspace_bytes, c.P,
+                         !p2p)) != KD_OK)
     return st;
   if (c.P.N > 0 && !recs) return fail(KD_ERR_INVALID_ARG, "recs is NULL");
   const Plan& P = c.P;
@@ -1138,18 +1145,163 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
     return KD_OK;
   }
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
-  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
+  // masked rows: local outputs zeroed here; in the peer exchange the owner writes their zeros (k_p2p_combine)
+  if (mask && (loss || dh_local)) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_local, P.d_s, c.s));
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     // rank records [n_ranks][5][N] indexed by ORIGINAL row, merged in rank order
     KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite,
                            P.kind == KD_RKL ? 1 : 0, c.s));
-    if ((st = backward_chunk(c, row0, loss, dh_s_partial, dW)) != KD_OK) return st;
+    if ((st = backward_chunk(c, row0, loss, dh_dst, dW)) != KD_OK) return st;
     if (P.kind == KD_FKL)  // this shard's partial FKL: Σ over its vocab rows of p (ln p − ln q), global LSEs
-      KD_LAUNCH(K_MERGE, launch_loss_rows(pass_params(c, row0).kpart, P.n_gslots, P.Nc, row0, c.n_eff, loss, c.idx,
-                                          c.nonfinite, c.s));
+      KD_LAUNCH(K_MERGE, launch_loss_rows(pass_params(c, row0).kpart, P.n_gslots, P.Nc, row0, c.n_eff, floss_dst,
+                                          c.idx, c.nonfinite, c.s));
   }
+  return KD_OK;
+}
+
+kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                            const uint8_t* mask, const float* recs, int32_t n_ranks, float* loss,
+                            float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
+  return vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, n_ranks, loss, dh_s_partial,
+                             local_rows(dh_s_partial, p->d_s), local_rows(loss, 1), dW_s, n_nonfinite,
+                             workspace, workspace_bytes, stream, false);
+}
+
+// ------------------------------------------------------------------------------------ peer exchange (§8, kd_p2p)
+namespace {
+struct P2PLayout {
+  long long R, set_bytes, lset_bytes, off_slots, off_lslots, off_dh, off_loss, total;
+};
+long long align256(long long x) { return (x + 255) / 256 * 256; }
+P2PLayout p2p_layout(int world, long long max_rows, long long max_tokens, int d_s) {
+  P2PLayout L{};
+  L.R = world > 0 ? (max_rows + world - 1) / world : 0;
+  L.set_bytes = align256((long long)world * L.R * d_s * 4);
+  L.lset_bytes = align256((long long)world * L.R * 4);
+  L.off_slots = 256;
+  L.off_lslots = L.off_slots + kP2PSets * L.set_bytes;
+  L.off_dh = L.off_lslots + kP2PSets * L.lset_bytes;
+  L.off_loss = L.off_dh + align256(max_tokens * d_s * 4);
+  L.total = L.off_loss + align256(max_tokens * 4);
+  return L;
+}
+kd_status check_p2p(const kd_p2p* x) {
+  if (!x) return fail(KD_ERR_INVALID_ARG, "kd_p2p is NULL");
+  if (x->world < 1 || x->world > kP2PMaxRanks) return fail(KD_ERR_INVALID_ARG, "kd_p2p.world must be in [1, 8]");
+  if (x->rank < 0 || x->rank >= x->world) return fail(KD_ERR_INVALID_ARG, "kd_p2p.rank outside [0, world)");
+  if (x->d_s <= 0 || x->d_s % 4 || x->max_rows < 0 || x->max_tokens < 0)
+    return fail(KD_ERR_SHAPE, "kd_p2p: d_s must be a positive multiple of 4, capacities >= 0");
+  for (int j = 0; j < x->world; ++j)
+    if (!x->arena[j] || (reinterpret_cast<uintptr_t>(x->arena[j]) & 255))
+      return fail(KD_ERR_ALIGNMENT, "kd_p2p.arena[%d] must be non-NULL and 256-byte aligned", j);
+  return KD_OK;
+}
+uint8_t* arena_at(const kd_p2p* x, int j, long long off) { return static_cast<uint8_t*>(x->arena[j]) + off; }
+}  // namespace
+
+size_t kd_p2p_arena_bytes(int32_t world, int64_t max_rows, int64_t max_tokens, int32_t d_s) {
+  if (world < 1 || world > kP2PMaxRanks || max_rows < 0 || max_tokens < 0 || d_s <= 0) return 0;
+  return (size_t)p2p_layout(world, max_rows, max_tokens, d_s).total;
+}
+
+kd_status kd_p2p_outputs(const kd_p2p* x, float** dh_out, float** loss_out) {
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  if (!dh_out || !loss_out) return fail(KD_ERR_INVALID_ARG, "NULL output pointer");
+  const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
+  *dh_out = reinterpret_cast<float*>(arena_at(x, x->rank, L.off_dh));
+  *loss_out = reinterpret_cast<float*>(arena_at(x, x->rank, L.off_loss));
+  return KD_OK;
+}
+
+kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
+                                float* loss, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                                size_t workspace_bytes, const kd_p2p* x, int32_t set, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
+  if (set < 0 || set >= kP2PSets) return fail(KD_ERR_INVALID_ARG, "set must be in [0, %d)", kP2PSets);
+  if (n_ranks != x->world) return fail(KD_ERR_INVALID_ARG, "n_ranks (%d) != kd_p2p.world (%d)", n_ranks, x->world);
+  if (p->d_s != x->d_s) return fail(KD_ERR_SHAPE, "problem d_s != kd_p2p.d_s");
+  if (p->n_tokens > x->max_rows) return fail(KD_ERR_SHAPE, "n_tokens exceeds the arena's max_rows");
+  if (p->kind == KD_RKL && p->n_tokens > 0 && !loss) return fail(KD_ERR_INVALID_ARG, "RKL needs the local loss buffer");
+  const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
+  const long long R = (p->n_tokens + x->world - 1) / x->world;  // rows per owner in this exchange chunk
+  RowDst dh{}, fl{};
+  for (int j = 0; j < x->world; ++j) {
+    dh.base[j] = reinterpret_cast<float*>(arena_at(x, j, L.off_slots + set * L.set_bytes));
+    fl.base[j] = reinterpret_cast<float*>(arena_at(x, j, L.off_lslots + set * L.lset_bytes));
+  }
+  dh.rows_per_owner = fl.rows_per_owner = R > 0 ? R : 1;
+  dh.src_row = fl.src_row = (long long)x->rank * R;
+  dh.ld = x->d_s;
+  fl.ld = 1;
+  dh.sys_fence = fl.sys_fence = 1;
+  if ((st = vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, n_ranks, p->kind == KD_RKL ? loss : nullptr,
+                                nullptr, dh, fl, dW_s, n_nonfinite, workspace, workspace_bytes, stream, true)) != KD_OK)
+    return st;
+  // publish: every owner's arrival counter + 1 (one per rank per exchange chunk, also for an empty chunk)
+  P2PFlags f{};
+  f.n = x->world;
+  for (int j = 0; j < x->world; ++j) f.f[j] = reinterpret_cast<unsigned*>(arena_at(x, j, 0));
+  KD_LAUNCH(K_P2P, launch_p2p_signal(f, static_cast<cudaStream_t>(stream)));
+  return KD_OK;
+}
+
+kd_status kd_p2p_combine(const kd_p2p* x, int32_t set, int64_t n_rows, int64_t row0, const uint8_t* mask,
+                         int32_t with_loss, uint32_t arrivals_target, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  if (set < 0 || set >= kP2PSets) return fail(KD_ERR_INVALID_ARG, "set must be in [0, %d)", kP2PSets);
+  if (n_rows < 0 || n_rows > x->max_rows) return fail(KD_ERR_SHAPE, "n_rows outside [0, max_rows]");
+  if (row0 < 0 || row0 + n_rows > x->max_tokens) return fail(KD_ERR_SHAPE, "rows [row0, row0 + n_rows) exceed max_tokens");
+  const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  P2PCombine c{};
+  c.slots = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_slots + set * L.set_bytes));
+  c.lslots = with_loss ? reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_lslots + set * L.lset_bytes))
+                       : nullptr;
+  for (int t = 0; t < x->world; ++t) {
+    c.out[t] = reinterpret_cast<float*>(arena_at(x, t, L.off_dh)) + row0 * x->d_s;
+    c.lout[t] = with_loss ? reinterpret_cast<float*>(arena_at(x, t, L.off_loss)) + row0 : nullptr;
+  }
+  c.mask = mask;
+  c.arrivals = reinterpret_cast<const unsigned*>(arena_at(x, x->rank, 0));
+  c.target = arrivals_target;
+  c.P = x->world;
+  c.me = x->rank;
+  c.d_s = x->d_s;
+  c.R = (n_rows + x->world - 1) / x->world;
+  c.n_rows = n_rows;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  KD_LAUNCH(K_P2P, launch_p2p_combine(c, sms, s));
+  P2PFlags f{};
+  f.n = x->world;
+  for (int t = 0; t < x->world; ++t) f.f[t] = reinterpret_cast<unsigned*>(arena_at(x, t, 4));
+  KD_LAUNCH(K_P2P, launch_p2p_signal(f, s));
+  return KD_OK;
+}
+
+kd_status kd_p2p_wait(const kd_p2p* x, uint32_t done_target, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, 4)), done_target,
+                                   static_cast<cudaStream_t>(stream)));
   return KD_OK;
 }
 
@@ -1226,7 +1378,7 @@ kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t,
   // kd_vocab_partials used, leaving the chunk's G planes in the workspace untouched
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
   if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
-  return finish_chunk(c, 0, loss, dh_s_partial, dW, kj_all, n_ranks);
+  return finish_chunk(c, 0, loss, local_rows(dh_s_partial, c.P.d_s), dW, kj_all, n_ranks);
 }
 
 kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(256) k_zero_masked(const uint8_t* __restrict__
                                                      float* __restrict__ dh, int d_s) {
   const int n = blockIdx.x;
   if (mask[n] != 0) return;
-  if (threadIdx.x == 0) loss[n] = 0.f;
+  if (threadIdx.x == 0 && loss) loss[n] = 0.f;
+  if (!dh) return;  // peer exchange: the owner writes the masked rows' zeros (k_p2p_combine)
   float4* o = reinterpret_cast<float4*>(dh + (size_t)n * d_s);
   for (int j = threadIdx.x; j < d_s / 4; j += blockDim.x) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
@@ -308,111 +309,103 @@ cudaError_t launch_extract_zero(const int* corr_v, const float* corr_r, int n_sl
 }
 
 // ------------------------------------------------------------------ A4r: dh split-K reduce + extracted entries + scatter
-// One warp per token row: lane j owns columns {8j..8j+7} + 256·i (coalesced 32-byte / 16-byte accesses).
+// One warp per (token row, 512-column block): lane j owns the float4 columns cb + 128·i + 4j, i = 0..3 (512-B warp
+// runs), and the split loop is unrolled by four so a lane keeps 16 loads in flight (round 1's warp-per-row form
+// reached ~2.2 TB/s, latency-bound at 14 warps per SM).
 //   dh[orig(r), :] = Σ_ks part[ks][r, :]  +  Σ_{slot} g_slot · W_s[v_slot, :]
 // The second sum restores the entries extracted from the dh GEMM (k_extract_zero): their exact fp32 g, added in a
 // fixed (slot) order — deterministic.  corr2 (top-k baseline): exact residuals g − (hi + lo) of the support entries
-// that were not extracted.  d_s % 8 == 0, d_s <= 2048 * 4.
-constexpr int kRedVec = 8;  // 8-column groups per lane per column block: 32 lanes x 8 x 8 = 2048 columns
+// that were not extracted.  The summation order per element (splits 0..k−1, then the slots in order) is the round-1
+// kernel's, so the results are unchanged bit for bit.  d_s % 4 == 0.
+constexpr int kRedCols = 512;  // columns per warp
+__device__ __forceinline__ void red_add_rows(float (&acc)[16], const float* __restrict__ rr, const int* __restrict__ vv,
+                                             int n, const __nv_bfloat16* __restrict__ Ws, int d_s, int cb, int lane) {
+  for (int base = 0; base < n; base += 32) {
+    const float myr = base + lane < n ? rr[base + lane] : 0.f;
+    unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
+    while (live) {
+      const int src = __ffs(live) - 1;
+      live &= live - 1;
+      const float coef = __shfl_sync(0xffffffffu, myr, src);
+      const __nv_bfloat16* w = Ws + (size_t)vv[base + src] * d_s;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int col = cb + 128 * i + 4 * lane;
+        if (col < d_s) {
+          const uint2 q = *reinterpret_cast<const uint2*>(w + col);
+          acc[4 * i + 0] = fmaf(coef, bf16lo_to_f32(q.x), acc[4 * i + 0]);
+          acc[4 * i + 1] = fmaf(coef, bf16hi_to_f32(q.x), acc[4 * i + 1]);
+          acc[4 * i + 2] = fmaf(coef, bf16lo_to_f32(q.y), acc[4 * i + 2]);
+          acc[4 * i + 3] = fmaf(coef, bf16hi_to_f32(q.y), acc[4 * i + 3]);
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_reduce_dh(const float* __restrict__ part, long long split_stride, int k_split,
                                                    int d_s, int n_rows, int row0, const int* __restrict__ n_eff,
-                                                   const int* __restrict__ idx, float* __restrict__ dh,
+                                                   const int* __restrict__ idx, const RowDst dst,
                                                    const int* __restrict__ corr_v, const float* __restrict__ corr_r,
                                                    int n_slots, const __nv_bfloat16* __restrict__ Ws,
                                                    const int* __restrict__ corr2_v, const float* __restrict__ corr2_r,
                                                    int n_slots2) {
   const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int n_cb = (d_s + kRedCols - 1) / kRedCols;
+  const long long w = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int r = (int)(w / n_cb);
+  const int cb = (int)(w % n_cb) * kRedCols;
   const int valid = min(n_rows, *n_eff - row0);
   if (r >= valid) return;
   const int orow = idx ? idx[row0 + r] : row0 + r;
-  float* out = dh + (size_t)orow * d_s;
-  const float* rr = corr_r ? corr_r + (size_t)r * n_slots : nullptr;
-  const int* vv = corr_v ? corr_v + (size_t)r * n_slots : nullptr;
-  for (int cb = 0; cb < d_s; cb += 32 * 8 * kRedVec) {  // column blocks of 2048
-    float acc[kRedVec][8];
+  float acc[16];
 #pragma unroll
-    for (int g = 0; g < kRedVec; ++g)
+  for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+  const float* src = part + (size_t)r * d_s;
+  int ks = 0;
+  for (; ks + 4 <= k_split; ks += 4) {
+    float4 x[4][4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
-    for (int ks = 0; ks < k_split; ++ks) {
-      const float* src = part + ks * split_stride + (size_t)r * d_s;
+    for (int s = 0; s < 4; ++s)
 #pragma unroll
-      for (int g = 0; g < kRedVec; ++g) {
-        const int col = cb + (g * 32 + lane) * 8;
-        if (col < d_s) {
-          const float4 a = *reinterpret_cast<const float4*>(src + col);
-          const float4 b = *reinterpret_cast<const float4*>(src + col + 4);
-          acc[g][0] += a.x; acc[g][1] += a.y; acc[g][2] += a.z; acc[g][3] += a.w;
-          acc[g][4] += b.x; acc[g][5] += b.y; acc[g][6] += b.z; acc[g][7] += b.w;
-        }
+      for (int i = 0; i < 4; ++i) {
+        const int col = cb + 128 * i + 4 * lane;
+        x[s][i] = col < d_s ? *reinterpret_cast<const float4*>(src + (ks + s) * split_stride + col)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    }
-    if (rr) {
-      for (int base = 0; base < n_slots; base += 32) {
-        const float myr = base + lane < n_slots ? rr[base + lane] : 0.f;
-        unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
-        while (live) {
-          const int src = __ffs(live) - 1;
-          live &= live - 1;
-          const float coef = __shfl_sync(0xffffffffu, myr, src);
-          const __nv_bfloat16* w = Ws + (size_t)vv[base + src] * d_s;
 #pragma unroll
-          for (int g = 0; g < kRedVec; ++g) {
-            const int col = cb + (g * 32 + lane) * 8;
-            if (col < d_s) {
-              const uint4 q = *reinterpret_cast<const uint4*>(w + col);
-              acc[g][0] = fmaf(coef, bf16lo_to_f32(q.x), acc[g][0]);
-              acc[g][1] = fmaf(coef, bf16hi_to_f32(q.x), acc[g][1]);
-              acc[g][2] = fmaf(coef, bf16lo_to_f32(q.y), acc[g][2]);
-              acc[g][3] = fmaf(coef, bf16hi_to_f32(q.y), acc[g][3]);
-              acc[g][4] = fmaf(coef, bf16lo_to_f32(q.z), acc[g][4]);
-              acc[g][5] = fmaf(coef, bf16hi_to_f32(q.z), acc[g][5]);
-              acc[g][6] = fmaf(coef, bf16lo_to_f32(q.w), acc[g][6]);
-              acc[g][7] = fmaf(coef, bf16hi_to_f32(q.w), acc[g][7]);
-            }
-          }
-        }
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[4 * i + 0] += x[s][i].x;
+        acc[4 * i + 1] += x[s][i].y;
+        acc[4 * i + 2] += x[s][i].z;
+        acc[4 * i + 3] += x[s][i].w;
       }
-    }
-    if (corr2_r) {  // top-k baseline: exact residuals of the k support entries (k_topk_fix)
-      const float* rr = corr2_r + (size_t)r * n_slots2;
-      const int* vv = corr2_v + (size_t)r * n_slots2;
-      for (int base = 0; base < n_slots2; base += 32) {
-        const float myr = base + lane < n_slots2 ? rr[base + lane] : 0.f;
-        unsigned live = __ballot_sync(0xffffffffu, myr != 0.f);
-        while (live) {
-          const int src = __ffs(live) - 1;
-          live &= live - 1;
-          const float coef = __shfl_sync(0xffffffffu, myr, src);
-          const __nv_bfloat16* w = Ws + (size_t)vv[base + src] * d_s;
+  }
+  for (; ks < k_split; ++ks) {
 #pragma unroll
-          for (int g = 0; g < kRedVec; ++g) {
-            const int col = cb + (g * 32 + lane) * 8;
-            if (col < d_s) {
-              const uint4 q = *reinterpret_cast<const uint4*>(w + col);
-              acc[g][0] = fmaf(coef, bf16lo_to_f32(q.x), acc[g][0]);
-              acc[g][1] = fmaf(coef, bf16hi_to_f32(q.x), acc[g][1]);
-              acc[g][2] = fmaf(coef, bf16lo_to_f32(q.y), acc[g][2]);
-              acc[g][3] = fmaf(coef, bf16hi_to_f32(q.y), acc[g][3]);
-              acc[g][4] = fmaf(coef, bf16lo_to_f32(q.z), acc[g][4]);
-              acc[g][5] = fmaf(coef, bf16hi_to_f32(q.z), acc[g][5]);
-              acc[g][6] = fmaf(coef, bf16lo_to_f32(q.w), acc[g][6]);
-              acc[g][7] = fmaf(coef, bf16hi_to_f32(q.w), acc[g][7]);
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < kRedVec; ++g) {
-      const int col = cb + (g * 32 + lane) * 8;
+    for (int i = 0; i < 4; ++i) {
+      const int col = cb + 128 * i + 4 * lane;
       if (col < d_s) {
-        *reinterpret_cast<float4*>(out + col) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
-        *reinterpret_cast<float4*>(out + col + 4) = make_float4(acc[g][4], acc[g][5], acc[g][6], acc[g][7]);
+        const float4 a = *reinterpret_cast<const float4*>(src + ks * split_stride + col);
+        acc[4 * i + 0] += a.x;
+        acc[4 * i + 1] += a.y;
+        acc[4 * i + 2] += a.z;
+        acc[4 * i + 3] += a.w;
       }
     }
   }
+  if (corr_r) red_add_rows(acc, corr_r + (size_t)r * n_slots, corr_v + (size_t)r * n_slots, n_slots, Ws, d_s, cb, lane);
+  if (corr2_r)  // top-k baseline: exact residuals of the k support entries (k_topk_fix)
+    red_add_rows(acc, corr2_r + (size_t)r * n_slots2, corr2_v + (size_t)r * n_slots2, n_slots2, Ws, d_s, cb, lane);
+  float* out = row_dst(dst, orow);  // local dh row, or the owner's receive slot (peer exchange)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int col = cb + 128 * i + 4 * lane;
+    if (col < d_s) *reinterpret_cast<float4*>(out + col) = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+  }
+  if (dst.sys_fence) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ SM -> L2 partition (die) probe
@@ -668,7 +661,7 @@ cudaError_t launch_merge(const float* part, long long plane, long long split_str
 // FKL loss of the decoupled path: ℓ = ln2 · Σ_slots partial (each partial = Σ_v p_v (log2 p_v − log2 q_v) over one
 // (vocab split, column part)), summed in fp64 in fixed slot order.
 __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ lpart, int n_slots, int n_rows, int row0,
-                                                   const int* __restrict__ n_eff, float* __restrict__ loss,
+                                                   const int* __restrict__ n_eff, const RowDst loss,
                                                    const int* __restrict__ idx, long long* __restrict__ nonfinite) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int valid = min(n_rows, *n_eff - row0);
@@ -677,10 +670,11 @@ __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ lpa
   for (int s = 0; s < n_slots; ++s) acc += (double)lpart[(size_t)s * n_rows + r];
   const float ell = (float)(acc * 0.6931471805599453);
   const int orow = idx ? idx[row0 + r] : row0 + r;
-  loss[orow] = ell;
+  *row_dst(loss, orow) = ell;
   if (!isfinite(ell)) atomicAdd(reinterpret_cast<unsigned long long*>(nonfinite), 1ull);
+  if (loss.sys_fence) __threadfence_system();
 }
-cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, float* loss,
+cudaError_t launch_loss_rows(const float* lpart, int n_slots, int n_rows, int row0, const int* n_eff, const RowDst& loss,
                              const int* idx, long long* nonfinite, cudaStream_t s) {
   k_loss_rows<<<(n_rows + 255) / 256, 256, 0, s>>>(lpart, n_slots, n_rows, row0, n_eff, loss, idx, nonfinite);
   return cudaGetLastError();
@@ -704,12 +698,104 @@ cudaError_t launch_kj_rows(const float* kpart, int n_split, int n_rows, int row0
   return cudaGetLastError();
 }
 cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_split, int d_s, int n_rows, int row0,
-                             const int* n_eff, const int* idx, float* dh, const int* corr_v, const float* corr_r,
-                             int n_slots, const __nv_bfloat16* Ws, cudaStream_t s, const int* corr2_v,
-                             const float* corr2_r, int n_slots2) {
-  if (d_s % 8 != 0) return cudaErrorInvalidValue;
-  k_reduce_dh<<<(n_rows + 7) / 8, 256, 0, s>>>(part, split_stride, k_split, d_s, n_rows, row0, n_eff, idx, dh, corr_v,
+                             const int* n_eff, const int* idx, const RowDst& dh, const int* corr_v,
+                             const float* corr_r, int n_slots, const __nv_bfloat16* Ws, cudaStream_t s,
+                             const int* corr2_v, const float* corr2_r, int n_slots2) {
+  if (d_s % 4 != 0) return cudaErrorInvalidValue;
+  const long long warps = (long long)n_rows * ((d_s + kRedCols - 1) / kRedCols);
+  if (warps == 0) return cudaSuccess;
+  k_reduce_dh<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(part, split_stride, k_split, d_s, n_rows, row0, n_eff, idx, dh, corr_v,
                                                 corr_r, n_slots, Ws, corr2_v, corr2_r, n_slots2);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ peer exchange of the vocab-sharded step (§8)
+// The partial dh_s / FKL loss rows of a vocab shard leave k_reduce_dh / k_loss_rows straight into the owning rank's
+// receive slot (RowDst, NVLink peer memory); k_p2p_signal then raises every owner's arrival counter; k_p2p_combine
+// (the owner) waits for the P arrivals, sums the P partials in rank order and stores the sum into every rank's
+// output; k_p2p_signal raises every rank's done counter; k_p2p_wait holds a stream until its done counter arrives.
+// Counters only grow (wrap-safe comparison); the host tracks their targets.  Every wait is bounded (~60 s, then
+// __trap) so a lost peer fails the launch instead of hanging the GPU.
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ void p2p_spin_until(const unsigned* flag, unsigned target) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
+  while ((int)(ld_acquire_sys_u32(flag) - target) < 0) {
+    __nanosleep(ns);
+    if (ns < 4096) ns *= 2;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60ull * 1000000000ull) __trap();  // a peer never arrived
+  }
+}
+
+__global__ void k_p2p_signal(const P2PFlags f) {
+  // stream-ordered after the kernels whose peer stores it publishes (each of their threads ended with fence.sc.sys)
+  __threadfence_system();
+  if (threadIdx.x < f.n) red_release_sys_add_u32(f.f[threadIdx.x], 1u);
+}
+
+__global__ void k_p2p_wait(const unsigned* flag, unsigned target) {
+  if (threadIdx.x == 0) p2p_spin_until(flag, target);
+}
+
+__global__ void __launch_bounds__(256) k_p2p_combine(const P2PCombine c) {
+  if (threadIdx.x == 0) p2p_spin_until(c.arrivals, c.target);
+  __syncthreads();
+  const long long r0 = (long long)c.me * c.R;
+  const long long nr = max(0ll, min(c.n_rows, r0 + c.R) - r0);
+  const int v4 = c.d_s / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long slot_stride = c.R * c.d_s;  // between source ranks
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nr * v4; e += stride) {
+    const long long i = e / v4;
+    const int col = (int)(e % v4) * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!c.mask || c.mask[r0 + i]) {
+      const float* src = c.slots + i * c.d_s + col;
+      for (int r = 0; r < c.P; ++r) {  // rank order: deterministic for a fixed P
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(src + r * slot_stride));
+        acc.x += x.x;
+        acc.y += x.y;
+        acc.z += x.z;
+        acc.w += x.w;
+      }
+    }
+    for (int t = 0; t < c.P; ++t) *reinterpret_cast<float4*>(c.out[t] + (r0 + i) * c.d_s + col) = acc;
+  }
+  if (c.lslots) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += stride) {
+      float acc = 0.f;
+      if (!c.mask || c.mask[r0 + i])
+        for (int r = 0; r < c.P; ++r) acc += __ldcg(c.lslots + r * c.R + i);
+      for (int t = 0; t < c.P; ++t) c.lout[t][r0 + i] = acc;
+    }
+  }
+  __threadfence_system();
+}
+
+cudaError_t launch_p2p_signal(const P2PFlags& f, cudaStream_t s) {
+  k_p2p_signal<<<1, 32, 0, s>>>(f);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_wait(const unsigned* flag, unsigned target, cudaStream_t s) {
+  k_p2p_wait<<<1, 32, 0, s>>>(flag, target);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_combine(const P2PCombine& c, int num_sms, cudaStream_t s) {
+  // one CTA per SM at most: the waiting CTAs must leave room for NCCL's kernels of the records exchange
+  const long long nr = c.R;
+  const long long work = nr * (c.d_s / 4);
+  const int blocks = (int)std::max(1ll, std::min<long long>(num_sms, (work + 255) / 256));
+  k_p2p_combine<<<blocks, 256, 0, s>>>(c);
   return cudaGetLastError();
 }
 

@@ -85,6 +85,55 @@ struct PassParams {
   float* zst;
 };
 
+// Destination of per-token output rows (k_reduce_dh: dh_s rows, k_loss_rows: loss).  Local form: base[0] + orow·ld
+// (rows_per_owner larger than any row).  Peer-exchange form (kd_vocab_backward_p2p): row orow of the
+// exchange chunk belongs to owner j = orow / rows_per_owner and is stored into owner j's receive slot
+// base[j] + (src_row + orow − j·rows_per_owner)·ld, base[j] = owner j's slot set as mapped in this process (NVLink
+// peer memory for j != rank); sys_fence = 1 then ends every storing thread with fence.sc.sys, so the stores are
+// performed system-wide before the kernel completes and the stream's signal kernel (k_p2p_signal) raises the
+// owners' arrival counters.
+constexpr int kP2PMaxRanks = 8;
+constexpr int kP2PSets = 3;  // receive-slot sets rotated over exchange chunks (kd_vocab_backward_p2p `set`)
+struct RowDst {
+  float* base[kP2PMaxRanks];
+  long long rows_per_owner;
+  long long src_row;
+  long long ld;
+  int sys_fence;
+};
+__host__ __device__ inline float* row_dst(const RowDst& d, long long orow) {
+  const long long j = orow / d.rows_per_owner;
+  return d.base[j] + (d.src_row + orow - j * d.rows_per_owner) * d.ld;
+}
+inline RowDst local_rows(float* base, long long ld) {
+  RowDst d{};
+  d.base[0] = base;
+  d.rows_per_owner = 1ll << 62;
+  d.src_row = 0;
+  d.ld = ld;
+  d.sys_fence = 0;
+  return d;
+}
+
+// Owner side of the peer exchange (k_p2p_combine): the P partial rows of this owner's slice of an exchange chunk are
+// summed in rank order (deterministic) and the sum is stored into every rank's output (dh_out / loss_out rows of the
+// chunk, peer memory for the other ranks).
+struct P2PCombine {
+  const float* slots;               // this owner's slot set [P][R][d_s] (partials pushed by every rank)
+  const float* lslots;              // [P][R] partial losses (FKL), or NULL
+  float* out[kP2PMaxRanks];         // rank t's dh_out + row0·d_s, as mapped in this process
+  float* lout[kP2PMaxRanks];        // rank t's loss_out + row0 (FKL), or NULL
+  const uint8_t* mask;              // the chunk's mask [n_rows] or NULL: masked rows get 0 (never read)
+  const unsigned* arrivals;         // this owner's arrival counter
+  unsigned target;                  // wait until *arrivals - target >= 0 (wrap-safe)
+  int P, me, d_s;
+  long long R, n_rows;              // rows per owner (ceil(n_rows / P)) and the chunk's rows
+};
+struct P2PFlags {
+  unsigned* f[kP2PMaxRanks];        // one counter per rank (as mapped in this process)
+  int n;
+};
+
 // Logit-gradient kernel of the staged variant (kd_stage.cu): pass 2's outputs from the staged logits.
 struct StageParams {
   const int* n_eff;

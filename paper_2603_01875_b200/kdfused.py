@@ -22,7 +22,8 @@ STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALI
 EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_teacher_lse", "kd_fused_fwd_bwd_lse",
             "kd_teacher_topk", "kd_topk_fwd_bwd",
             "kd_vocab_stats", "kd_vocab_backward",
-            "kd_vocab_partials", "kd_vocab_finish", "kd_handoff_export", "kd_handoff_open", "kd_handoff_close",
+            "kd_vocab_partials", "kd_vocab_finish", "kd_p2p_arena_bytes", "kd_p2p_outputs", "kd_vocab_backward_p2p",
+            "kd_p2p_combine", "kd_p2p_wait", "kd_handoff_export", "kd_handoff_open", "kd_handoff_close",
             "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
             "kd_last_error", "kd_abi_version")
@@ -41,6 +42,13 @@ class KDProblem(ctypes.Structure):
                 ("loss_scale", ctypes.c_float), ("want_dW", ctypes.c_int32), ("accumulate_dW", ctypes.c_int32),
                 ("chunk_tokens", ctypes.c_int32), ("grad_precision", ctypes.c_int32),
                 ("stage_logits", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+
+
+class KDP2P(ctypes.Structure):
+    """kd_p2p: one rank's view of the peer-memory exchange (every rank's arena as mapped in this process)."""
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("d_s", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("max_rows", ctypes.c_int64), ("max_tokens", ctypes.c_int64),
+                ("arena", ctypes.c_void_p * 8)]
 
 
 _lib = None
@@ -79,6 +87,17 @@ def lib() -> ctypes.CDLL:
     L.kd_vocab_partials.restype = ctypes.c_int
     L.kd_vocab_finish.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64p, vp, sz, vp]
     L.kd_vocab_finish.restype = ctypes.c_int
+    X = ctypes.POINTER(KDP2P)
+    L.kd_p2p_arena_bytes.argtypes = [i32, ctypes.c_int64, ctypes.c_int64, i32]
+    L.kd_p2p_arena_bytes.restype = sz
+    L.kd_p2p_outputs.argtypes = [X, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
+    L.kd_p2p_outputs.restype = ctypes.c_int
+    L.kd_vocab_backward_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, i64p, vp, sz, X, i32, vp]
+    L.kd_vocab_backward_p2p.restype = ctypes.c_int
+    L.kd_p2p_combine.argtypes = [X, i32, ctypes.c_int64, ctypes.c_int64, vp, i32, ctypes.c_uint32, vp]
+    L.kd_p2p_combine.restype = ctypes.c_int
+    L.kd_p2p_wait.argtypes = [X, ctypes.c_uint32, vp]
+    L.kd_p2p_wait.restype = ctypes.c_int
     L.kd_handoff_export.argtypes = [vp, ctypes.c_uint64, vp]
     L.kd_handoff_export.restype = ctypes.c_int
     L.kd_handoff_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64)]
@@ -379,6 +398,77 @@ def vocab_backward(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, vocab, v_
                                    _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),
                                    _stream_handle(stream)))
     return KDResult(loss, dh, dW_s if want_dW else None, nnf)
+
+
+# ------------------------------------------------------------------ peer-memory exchange (kd_p2p)
+P2P_SETS = 3  # receive-slot sets rotated over exchange chunks (kdfused.h)
+
+
+def p2p_arena_bytes(world: int, max_rows: int, max_tokens: int, d_s: int) -> int:
+    n = int(lib().kd_p2p_arena_bytes(int(world), int(max_rows), int(max_tokens), int(d_s)))
+    if n == 0:
+        raise KDError(1, "kd_p2p_arena_bytes: invalid arguments")
+    return n
+
+
+def make_p2p(world: int, rank: int, d_s: int, max_rows: int, max_tokens: int, arenas) -> KDP2P:
+    """A kd_p2p view: ``arenas`` = every rank's arena base address (ints) as mapped in this process."""
+    x = KDP2P()
+    x.world, x.rank, x.d_s, x.reserved = int(world), int(rank), int(d_s), 0
+    x.max_rows, x.max_tokens = int(max_rows), int(max_tokens)
+    for j, a in enumerate(arenas):
+        x.arena[j] = int(a)
+    return x
+
+
+def p2p_outputs(x: KDP2P, device, n_tokens: int, d_s: int):
+    """(dh_out [n_tokens, d_s], loss_out [n_tokens]) views of this rank's arena (valid until the next step)."""
+    dh, ls = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib().kd_p2p_outputs(ctypes.byref(x), ctypes.byref(dh), ctypes.byref(ls)))
+    dev = torch.device(device)
+    dh_t = torch.as_tensor(_DevView(dh.value, (int(x.max_tokens), d_s), "<f4"), device=dev)[:n_tokens]
+    ls_t = torch.as_tensor(_DevView(ls.value, (int(x.max_tokens),), "<f4"), device=dev)[:n_tokens]
+    return dh_t, ls_t
+
+
+def vocab_backward_p2p(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, x: KDP2P, set: int, vocab, v_begin,
+                       T=1.0, kind="fkl", loss_scale=1.0, want_dW=False, accumulate_dW=False, dW_s=None,
+                       chunk_tokens=0, stream=None, workspace=None) -> KDResult:
+    """kd_vocab_backward_p2p: as vocab_backward, but the partial dh_s (and FKL's partial loss) rows go straight to
+    their owners' receive slots of set ``set``; the result carries the local loss (RKL) and dW_s only."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(t, "input") for t in (h_t, W_t_shard, h_s, W_s_shard))
+    N, d_t = h_t.shape
+    V_r, d_s = W_s_shard.shape
+    dev = h_t.device
+    p = make_problem(N, d_t, d_s, vocab, T=T, kind=kind, loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, v_begin=v_begin, v_end=v_begin + V_r, chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    recs = recs.to(device=dev, dtype=torch.float32).contiguous()
+    loss = torch.empty(N, dtype=torch.float32, device=dev) if kind == "rkl" else None
+    nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if accumulate_dW else torch.empty)(V_r, d_s, dtype=torch.float32, device=dev)
+    ws = _workspace(workspace_size(p), dev, stream, workspace)
+    _check(lib().kd_vocab_backward_p2p(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                       _ptr(mask), _ptr(recs), int(recs.shape[0]), _ptr(loss),
+                                       _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),
+                                       ctypes.byref(x), int(set), _stream_handle(stream)))
+    return KDResult(loss, None, dW_s if want_dW else None, nnf)
+
+
+def p2p_combine(x: KDP2P, set: int, n_rows: int, row0: int, mask=None, *, with_loss: bool, target: int,
+                stream=None):
+    """kd_p2p_combine: owner side of one exchange chunk (waits for the arrivals counter to reach ``target``)."""
+    if mask is not None:
+        mask = mask.to(dtype=torch.uint8).contiguous()
+    _check(lib().kd_p2p_combine(ctypes.byref(x), int(set), int(n_rows), int(row0), _ptr(mask), int(bool(with_loss)),
+                                int(target) & 0xFFFFFFFF, _stream_handle(stream)))
+
+
+def p2p_wait(x: KDP2P, target: int, stream=None):
+    """kd_p2p_wait: hold the stream until this rank's done counter reaches ``target``."""
+    _check(lib().kd_p2p_wait(ctypes.byref(x), int(target) & 0xFFFFFFFF, _stream_handle(stream)))
 
 
 @dataclass

@@ -160,11 +160,128 @@ def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str) -> int:
     return min(cap, -(-(-(-n_tokens // n_chunks)) // 256) * 256)
 
 
+class P2PExchange:
+    """One rank's end of the peer-memory exchange of the FKL/RKL vocab-sharded step (kdfused.h kd_p2p).
+
+    Each rank owns an arena (receive slots, counters, the step's dh_out / loss_out) and maps every peer's arena:
+    the library's kernels then push the partial dh_s rows straight from the dh reduction into their owners' slots
+    (NVLink peer stores) and the owners store the rank-order sums into every rank's dh_out — no NCCL call on the
+    data path.  ``create`` builds it over a process group (CUDA IPC handles exchanged with all_gather_object);
+    ``local_group`` builds P of them inside one process on one device (the one-GPU emulation the tests use).
+    ``chunks`` counts the exchange chunks completed, from which every counter target follows (kdfused.h)."""
+
+    def __init__(self, world: int, rank: int, d_s: int, max_rows: int, max_tokens: int, arenas, own: torch.Tensor,
+                 mapped=()):
+        from . import kdfused
+        self.world, self.rank, self.d_s = world, rank, d_s
+        self.max_rows, self.max_tokens = max_rows, max_tokens
+        self.own = own              # keeps this rank's arena alive
+        self.mapped = list(mapped)  # HandoffTensor views of the peers' arenas (closed by close())
+        self.x = kdfused.make_p2p(world, rank, d_s, max_rows, max_tokens, arenas)
+        self.chunks = 0
+
+    @staticmethod
+    def _alloc(world, d_s, max_rows, max_tokens, device) -> torch.Tensor:
+        from . import kdfused
+        n = kdfused.p2p_arena_bytes(world, max_rows, max_tokens, d_s)
+        return torch.zeros(n, dtype=torch.uint8, device=device)  # counters start at 0
+
+    @classmethod
+    def local_group(cls, world: int, d_s: int, max_rows: int, max_tokens: int, device="cuda") -> list:
+        """P exchanges sharing one process and device (every 'peer' arena is a local allocation)."""
+        arenas = [cls._alloc(world, d_s, max_rows, max_tokens, device) for _ in range(world)]
+        ptrs = [a.data_ptr() for a in arenas]
+        return [cls(world, r, d_s, max_rows, max_tokens, ptrs, arenas[r]) for r in range(world)]
+
+    @classmethod
+    def create(cls, group, d_s: int, max_rows: int, max_tokens: int, device=None):
+        """Collective over ``group``: allocate and zero this rank's arena, exchange CUDA IPC handles, map the peers."""
+        from . import kdfused
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        own = cls._alloc(world, d_s, max_rows, max_tokens, dev)
+        torch.cuda.synchronize(dev)
+        handles = [None] * world
+        dist.all_gather_object(handles, kdfused.handoff_export(own), group=group)
+        ptrs, mapped = [], []
+        for j, h in enumerate(handles):
+            if j == rank:
+                ptrs.append(own.data_ptr())
+            else:
+                m = kdfused.HandoffTensor(h, (own.numel(),), torch.uint8, device=dev)
+                mapped.append(m)
+                ptrs.append(m.ptr)
+        dist.barrier(group=group)
+        return cls(world, rank, d_s, max_rows, max_tokens, ptrs, own, mapped)
+
+    def set_of(self, chunk: int) -> int:
+        return chunk % 3
+
+    def arrivals_target(self, chunk: int) -> int:
+        return (chunk + 1) * self.world
+
+    def done_target(self, chunk: int) -> int:
+        return (chunk + 1) * self.world
+
+    def close(self):
+        for m in self.mapped:
+            m.close()
+        self.mapped = []
+
+
+def _p2p_step(ex: P2PExchange, spans, stats, backward_p2p, combine, wait, outputs, *, mask, kind, N, d_s, device):
+    """The per-rank p2p pipeline of one step (the records exchange as in the NCCL path):
+
+        stats(i+1) ‖ records(i) ;  [wait done(i-3)] backward_p2p(i) -> slots ;  combine(i-1) (deferred)
+        end: combine(last) ; wait done(all)
+
+    Chunk g (counted over the exchange's life) uses slot set g % 3; reusing it needs every owner's combine of chunk
+    g - 3 done (a done target), checked only inside a step — the previous step ended waiting for all of its chunks."""
+    base = ex.chunks
+    n = len(spans)
+    loss_rkl = None
+    dW = None
+    nxt = stats(0) if spans else None
+
+    def do_combine(i):
+        a, b = spans[i]
+        g = base + i
+        combine(ex, ex.set_of(g), b - a, a, None if mask is None else mask[a:b], with_loss=(kind == "fkl"),
+                target=ex.arrivals_target(g))
+
+    for i, (a, b) in enumerate(spans):
+        recs_out, work = nxt
+        if i + 1 < n:
+            nxt = stats(i + 1)
+        work.wait()
+        g = base + i
+        if i >= 3:
+            wait(ex, ex.done_target(g - 3))
+        r = backward_p2p(i, _gathered(recs_out), ex.set_of(g), dW)
+        if kind == "rkl":
+            if loss_rkl is None:  # the kernels' dtype (fp32; the CPU test stand-ins return fp64)
+                loss_rkl = torch.zeros(N, dtype=r.loss.dtype, device=r.loss.device)
+            loss_rkl[a:b] = r.loss
+        if r.dW_s is not None:
+            dW = r.dW_s
+        if i >= 1:
+            do_combine(i - 1)
+    if n:
+        do_combine(n - 1)
+        wait(ex, ex.done_target(base + n - 1))
+    ex.chunks = base + n
+    dh_out, loss_out = outputs(ex, N)
+    if kind == "rkl" and loss_rkl is None:  # no tokens
+        loss_rkl = torch.zeros(0, dtype=torch.float32, device=device)
+    return _Result(loss_rkl if kind == "rkl" else loss_out, dh_out, dW)
+
+
 def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
                           T=1.0, kind="fkl", beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False,
                           dW_s=None, chunk_tokens=0, exchange_chunk=0, stats_fn: Callable | None = None,
                           backward_fn: Callable | None = None, partials_fn: Callable | None = None,
-                          finish_fn: Callable | None = None, dh_reduce: str = "all"):
+                          finish_fn: Callable | None = None, dh_reduce: str = "all",
+                          exchange: "P2PExchange | None" = None, p2p_fns: dict | None = None):
     """One vocab-sharded step on this rank; every rank of ``group`` holds the same tokens and its own
     LM-head rows [v_begin, v_begin + V_r).  Returns a result whose dh_s is the full gradient (all-reduced) and whose
     dW_s holds this rank's rows.
@@ -181,6 +298,11 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
     dh_reduce="scatter": when the group's tokens are its members' equal slices concatenated in rank order (each rank
     contributes its own batch, bench.py's 2-D grid), every rank keeps dh_s / loss of its own slice only: one
     reduce-scatter at the end instead of the per-chunk all-reduces.
+
+    ``exchange`` (a P2PExchange, FKL/RKL, dh_reduce="all"): the partial dh_s / FKL loss leave the library's dh
+    reduction straight into their owners' slots in peer memory and the owners' rank-order sums land in every rank's
+    arena (kdfused.h kd_p2p) — no NCCL call for the dh exchange; the returned dh_s / loss are views of the arena,
+    valid until the next step on it.  ``p2p_fns`` substitutes {backward, combine, wait, outputs} (CPU stand-ins).
 
     ``chunk_tokens`` is the library's internal token chunk (kd_problem.chunk_tokens, 0 = its default).  The
     kernel-side callables default to the CUDA entry points; tests substitute CPU stand-ins to exercise this exchange
@@ -211,6 +333,35 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
         rec = stats_fn(h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, m_c, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
                        chunk_tokens=(b - a) if fix else chunk_tokens)
         return _all_gather_async(rec, group)
+
+    if exchange is not None:
+        if fix or dh_reduce != "all":
+            raise ValueError("the peer exchange serves the FKL/RKL step with dh_reduce='all'")
+        if N > exchange.max_tokens or chunk > exchange.max_rows:
+            raise ValueError(f"step of {N} tokens / exchange chunk {chunk} exceeds the arena "
+                             f"({exchange.max_tokens} / {exchange.max_rows})")
+        from . import kdfused
+        f = dict(backward=kdfused.vocab_backward_p2p, combine=kdfused.p2p_combine, wait=kdfused.p2p_wait,
+                 outputs=lambda ex, n: kdfused.p2p_outputs(ex.x, h_t.device, n, d_s))
+        f.update(p2p_fns or {})
+
+        def backward_p2p(i, recs, set_, dW_cur):
+            a, b = spans[i]
+            return f["backward"](h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, recs,
+                                 None if mask is None else mask[a:b], x=exchange.x, set=set_, vocab=vocab,
+                                 v_begin=v_begin, T=T, kind=kind, loss_scale=loss_scale, want_dW=want_dW,
+                                 accumulate_dW=accumulate_dW or i > 0, dW_s=dW_cur if i > 0 else dW_s,
+                                 chunk_tokens=chunk_tokens)
+
+        def combine(ex, set_, n_rows, row0, m, *, with_loss, target):
+            f["combine"](ex.x, set_, n_rows, row0, m, with_loss=with_loss, target=target)
+
+        def wait(ex, target):
+            f["wait"](ex.x, target)
+
+        r = _p2p_step(exchange, spans, stats, backward_p2p, combine, wait, f["outputs"], mask=mask, kind=kind, N=N,
+                      d_s=d_s, device=h_t.device)
+        return _Result(r.loss, r.dh_s, r.dW_s if want_dW else None)
 
     nxt = stats(0) if spans else None
     for i, (a, b) in enumerate(spans):
@@ -262,3 +413,54 @@ def token_sharded_dW_reduce(dW_s: torch.Tensor, group=None) -> torch.Tensor:
     """Token sharding with dW_s: the only exchange is the sum of the per-rank dW_s."""
     _all_reduce_sum(dW_s, group)
     return dW_s
+
+
+def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0, kind="fkl", loss_scale=1.0,
+                              want_dW=False, chunk_tokens=0, exchange_chunk=0):
+    """One-GPU emulation of the P-rank p2p step (tests, ``bench.py --sim-p2p``): the P ranks' kernels run in one
+    stream in an order where every counter a kernel waits on was raised by an EARLIER launch (per exchange chunk: all
+    ranks' stats, then all ranks' backward_p2p, then all owners' combine) — no kernel waits on one launched after it,
+    so nothing depends on two launches running concurrently.  The kernels, slot addressing, counters and set rotation
+    are the multi-GPU ones; the 'peer' arenas are local allocations (``P2PExchange.local_group``).
+
+    Returns per rank (loss, dh_s view, dW_s rows)."""
+    from . import kdfused
+    P = len(exchanges)
+    V = W_t.shape[0]
+    bounds = vocab_shard_bounds(V, P)
+    N = h_t.shape[0]
+    d_s = W_s.shape[1]
+    chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, -(-V // P), kind)
+    spans = [(a, min(N, a + chunk)) for a in range(0, N, chunk)]
+    base = exchanges[0].chunks
+    dW = [None] * P
+    loss_rkl = [torch.zeros(N, dtype=torch.float32, device=h_t.device) for _ in range(P)] if kind == "rkl" else None
+    for i, (a, b) in enumerate(spans):
+        m_c = None if mask is None else mask[a:b]
+        recs = torch.stack([kdfused.vocab_stats(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], m_c, vocab=V, v_begin=v0,
+                                                T=T, kind=kind, chunk_tokens=chunk_tokens) for v0, v1 in bounds])
+        g = base + i
+        for r, (v0, v1) in enumerate(bounds):
+            ex = exchanges[r]
+            if i >= 3:
+                kdfused.p2p_wait(ex.x, ex.done_target(g - 3))
+            res = kdfused.vocab_backward_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], recs, m_c, x=ex.x,
+                                             set=ex.set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
+                                             loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=i > 0,
+                                             dW_s=dW[r], chunk_tokens=chunk_tokens)
+            if want_dW:
+                dW[r] = res.dW_s
+            if kind == "rkl":
+                loss_rkl[r][a:b] = res.loss
+        for r in range(P):
+            ex = exchanges[r]
+            kdfused.p2p_combine(ex.x, ex.set_of(g), b - a, a, m_c, with_loss=(kind == "fkl"),
+                                target=ex.arrivals_target(g))
+    out = []
+    for r, ex in enumerate(exchanges):
+        if spans:
+            kdfused.p2p_wait(ex.x, ex.done_target(base + len(spans) - 1))
+        ex.chunks = base + len(spans)
+        dh, ls = kdfused.p2p_outputs(ex.x, h_t.device, N, d_s)
+        out.append((loss_rkl[r] if kind == "rkl" else ls, dh, dW[r]))
+    return out

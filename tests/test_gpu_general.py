@@ -218,8 +218,10 @@ def test_config5_real_shapes_accumulate_dW():
     np.testing.assert_allclose(dW.cpu().numpy(), whole.dW_s.cpu().numpy(), rtol=GRAD_RTOL, atol=GRAD_ATOL)
     assert n_acc + n_whole >= 0
     # per-token outputs depend on the micro-batching only through the vocab split the planner picks for the batch size
-    # (the order the per-split records merge in): fp32-rounding close
-    np.testing.assert_allclose(whole.loss.cpu().numpy(), loss.cpu().numpy(), rtol=1e-5, atol=1e-7)
+    # (the order the per-split records merge in): fp32-rounding close.  The RKL loss is a difference of O(10) terms
+    # (log-sum-exps and U/S), so its order-dependent rounding is absolute, ~ulp(16) = 2e-6 (a re-run measured 2.7e-7
+    # on a 1.2e-3 loss): the absolute floor is R13's 1e-5, the relative part 100x tighter than R13's
+    np.testing.assert_allclose(whole.loss.cpu().numpy(), loss.cpu().numpy(), rtol=1e-5, atol=LOSS_ATOL)
 
 
 # ------------------------------------------------------------------ vocab shards with beta != 1/2

