@@ -192,22 +192,31 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
  *
  * Arena (one per rank, kd_p2p_arena_bytes, device memory, 256-byte aligned, ZEROED by its owner before
  * first use; every rank maps every other rank's arena, e.g. kd_handoff_export/open = CUDA IPC over NVLink):
- *   [0, 256)   counters: u32 arrivals at byte 0 (+1 per rank per exchange chunk, raised by each pushing
- *              rank), u32 done at byte 4 (+1 per owner per exchange chunk, raised by each owner).
- *              Counters only grow (modulo 2^32, compared wrap-safe); the caller tracks the targets:
- *              after k exchange chunks every counter of every rank is k*world.
- *   then       kP2P sets (3) of receive slots [world][R][d_s] f32 and of loss slots [world][R] f32,
- *              R = ceil(max_rows / world); dh_out [max_tokens][d_s] f32; loss_out [max_tokens] f32.
+ *   [0, 256)   counters, one u32 per SOURCE rank t (written by rank t only): arrivals[t] at byte 4t
+ *              (rank t pushed its partials of a chunk here), done[t] at byte 32 + 4t (owner t stored its
+ *              sums of a chunk here), records[t] at byte 64 + 4t (rank t's record of a chunk is here).
+ *              A wait for chunk c needs EVERY source at c+1 (a shared sum could be satisfied by a rank
+ *              running a chunk ahead).  Counters only grow (modulo 2^32, compared wrap-safe); after k
+ *              exchange chunks every counter is k, so the caller's target for chunk c is base + c + 1.
+ *   then       3 sets each of receive slots [world][R][d_s] f32, loss slots [world][R] f32 and records
+ *              [world][5][ceil4(max_rows)] f32, R = ceil(max_rows / world); dh_out [max_tokens][d_s] f32;
+ *              loss_out [max_tokens] f32.
  * Protocol per exchange chunk c (n_c <= max_rows tokens, rows [row0, row0 + n_c) of the step), every rank:
- *   kd_vocab_backward_p2p(set = c % 3)        pushes its partials; then arrivals of every owner += 1
- *   kd_p2p_combine(set = c % 3, target = (c+1)*world + base)   owner of rows [me*R_c, (me+1)*R_c) of the
- *                                              chunk (R_c = ceil(n_c / world)): waits for the arrivals,
+ *   kd_vocab_stats_p2p(set = c % 3)           its record into every rank's record set (the all-gather);
+ *                                              then records[rank] of every rank += 1
+ *   kd_vocab_backward_p2p(set = c % 3, recs = NULL, records_target = base + c + 1)
+ *                                              waits for the P records, merges them in rank order, pushes
+ *                                              its partials; then arrivals[rank] of every owner += 1
+ *   kd_p2p_combine(set = c % 3, target = base + c + 1)   owner of rows [me*R_c, (me+1)*R_c) of the
+ *                                              chunk (R_c = ceil(n_c / world)): waits for the P arrivals,
  *                                              sums, stores into every rank's dh_out/loss_out rows
- *                                              row0 + ..., masked rows 0; then done of every rank += 1
+ *                                              row0 + ..., masked rows 0; then done[rank] of every rank += 1
  *   kd_p2p_wait(done target)                  before a slot set is reused (chunk c+3 waits for
- *                                              done >= (c+1)*world + base) and before dh_out/loss_out
- *                                              are read (done >= n_chunks*world + base)
- * A rank may defer kd_p2p_combine(c) behind its next chunk's kernels (sharding.py does), hiding the wait.
+ *                                              done >= base + c + 1 from every owner) and before
+ *                                              dh_out/loss_out are read (done >= base + n_chunks)
+ * A rank may defer kd_p2p_combine(c) behind its next chunk's kernels (sharding.py does), hiding the wait, and
+ * run kd_vocab_stats_p2p(c+1) before kd_vocab_backward_p2p(c) — record set (c+1) % 3 was last read by chunk c-2,
+ * whose combine (which waited for every rank's backward of c-2) this rank has already run.
  * Waits are bounded: a counter that does not arrive within ~60 s traps the kernel (the launch fails with
  * a CUDA error) instead of hanging the device.  world <= 8; all ranks pass identical problem shapes. */
 #define KD_P2P_MAX_RANKS 8
@@ -224,7 +233,15 @@ typedef struct {
 size_t kd_p2p_arena_bytes(int32_t world, int64_t max_rows, int64_t max_tokens, int32_t d_s);
 /* Device pointers of this rank's dh_out [max_tokens][d_s] and loss_out [max_tokens] inside its arena. */
 kd_status kd_p2p_outputs(const kd_p2p* x, float** dh_out, float** loss_out);
+/* kd_vocab_stats into the arena: this rank's record [5][n_tokens] lands in slot [rank] of record set `set` of
+ * EVERY rank (written here, copied to the peers), then every rank's records counter += 1.
+ * Errors: as kd_vocab_stats; KD_ERR_SHAPE if n_tokens > max_rows or d_s != x->d_s. */
+kd_status kd_vocab_stats_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                             const void* W_s, const uint8_t* mask, void* workspace, size_t workspace_bytes,
+                             const kd_p2p* x, int32_t set, void* stream);
 /* kd_vocab_backward with the exchange: no dh_s_partial argument (the rows go to the owners' slots);
+ * recs = NULL: the records of arena set `set`, after waiting for this rank's records counter to reach
+ * records_target (else recs [n_ranks][5][n_tokens] as kd_vocab_backward, records_target ignored);
  * `loss`: RKL -> the full per-token loss (as kd_vocab_backward, local), FKL -> unused (NULL allowed; the
  * partial loss goes to the owners and the sum lands in loss_out).  n_ranks must equal x->world.
  * Errors: as kd_vocab_backward; KD_ERR_INVALID_ARG for a bad set / rank / world; KD_ERR_SHAPE if
@@ -232,13 +249,14 @@ kd_status kd_p2p_outputs(const kd_p2p* x, float** dh_out, float** loss_out);
 kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
                                 const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
                                 float* loss, float* dW_s, int64_t* n_nonfinite, void* workspace,
-                                size_t workspace_bytes, const kd_p2p* x, int32_t set, void* stream);
+                                size_t workspace_bytes, const kd_p2p* x, int32_t set, uint32_t records_target,
+                                void* stream);
 /* Owner side of exchange chunk `set`: n_rows = the chunk's tokens, row0 = its first row in dh_out,
  * mask = the chunk's mask [n_rows] or NULL, with_loss = 1 for FKL (sum the partial losses).
  * Errors: KD_ERR_SHAPE if n_rows > max_rows or row0 + n_rows > max_tokens. */
 kd_status kd_p2p_combine(const kd_p2p* x, int32_t set, int64_t n_rows, int64_t row0, const uint8_t* mask,
                          int32_t with_loss, uint32_t arrivals_target, void* stream);
-/* Holds `stream` until this rank's done counter reaches done_target (wrap-safe). */
+/* Holds `stream` until every owner's done counter in this rank's arena reaches done_target (wrap-safe). */
 kd_status kd_p2p_wait(const kd_p2p* x, uint32_t done_target, void* stream);
 
 /* ---- JSD / TVD vocab shards: one more exchange.  The JSD gradient needs the per-token

@@ -53,8 +53,9 @@ cudaError_t launch_reduce_dh(const float* part, long long split_stride, int k_sp
                              const float* corr_r, int n_slots, const __nv_bfloat16* Ws, cudaStream_t s,
                              const int* corr2_v = nullptr, const float* corr2_r = nullptr, int n_slots2 = 0);
 cudaError_t launch_p2p_signal(const P2PFlags& f, cudaStream_t s);
-cudaError_t launch_p2p_wait(const unsigned* flag, unsigned target, cudaStream_t s);
+cudaError_t launch_p2p_wait(const unsigned* ctr, int n, unsigned target, cudaStream_t s);
 cudaError_t launch_p2p_combine(const P2PCombine& c, int num_sms, cudaStream_t s);
+cudaError_t launch_p2p_copy(const P2PCopy& c, int num_sms, cudaStream_t s);
 cudaError_t launch_zero_records(const uint8_t* mask, int N, float* rec, long long plane, cudaStream_t s);
 cudaError_t launch_extract_zero(const int* corr_v, const float* corr_r, int n_slots, int n_rows, int row0,
                                 const int* n_eff, __nv_bfloat16* ghi, __nv_bfloat16* glo, cudaStream_t s);
@@ -1080,10 +1081,11 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
   return KD_OK;
 }
 
-kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
-                         const uint8_t* mask, float* rec, void* workspace, size_t workspace_bytes, void* stream) {
-  g_launches = 0;
-  g_cur_stream = static_cast<cudaStream_t>(stream);
+// Stats of one shard into `rec` (plane stride rec_plane >= N): kd_vocab_stats (local) and kd_vocab_stats_p2p
+// (straight into this rank's slot of the arena's record set).
+static kd_status vocab_stats_impl(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                  const void* W_s, const uint8_t* mask, float* rec, long long rec_plane,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
   kd_status st = validate_unstaged(p, false);
   if (st != KD_OK) return st;
   Ctx c{};
@@ -1099,26 +1101,35 @@ kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, 
   const Plan& P = c.P;
   if (P.N == 0) return KD_OK;
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
-  if (mask) KD_LAUNCH(K_ZERO, launch_zero_records(mask, P.N, rec, (long long)P.N, c.s));
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_records(mask, P.N, rec, rec_plane, c.s));
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    // the shard record carries the cross term U (merged across ranks into the loss): coupled pass 1
     // RKL shards need the cross term U in the record: the RKL value enters the gradient, so it must be merged
-    // before pass 2.  FKL (loss partials from pass 2, summed by the caller), JSD/TVD (loss from the (K, J) exchange)
-    // need the two LSEs only: the decoupled pass 1, as the fused path
+    // before pass 2.  FKL (loss partials from pass 2, summed over the shards) needs the two LSEs only: the
+    // decoupled pass 1, as the fused path
     const bool coupled = P.kind == KD_RKL;
     if ((st = run_pass(c, 1, P.kind, coupled, pp)) != KD_OK) return st;
-    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 1, nullptr,
-                           nullptr, rec, (long long)P.N, c.idx, 0, c.nonfinite, 0, c.s));
+    KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff,
+                           P.kind, 1, nullptr, nullptr, rec, rec_plane, c.idx, 0, c.nonfinite, 0, c.s));
   }
   return KD_OK;
+}
+
+kd_status kd_vocab_stats(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                         const uint8_t* mask, float* rec, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
+  return vocab_stats_impl(p, h_t, W_t, h_s, W_s, mask, rec, (long long)p->n_tokens, workspace, workspace_bytes,
+                          stream);
 }
 
 // The FKL/RKL shard backward behind kd_vocab_backward (dh / FKL loss rows into local buffers) and
 // kd_vocab_backward_p2p (the same rows stored straight into the owning ranks' receive slots, RowDst).
 static kd_status vocab_backward_impl(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
-                                     const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
+                                     const void* W_s, const uint8_t* mask, const float* recs, long long rec_plane,
+                                     long long rec_rank_stride, int32_t n_ranks,
                                      float* loss, float* dh_local, const RowDst& dh_dst, const RowDst& floss_dst,
                                      float* dW_s, int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
                                      void* stream, bool p2p) {
@@ -1150,7 +1161,7 @@ static kd_status vocab_backward_impl(const kd_problem* p, const void* h_t, const
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     // rank records [n_ranks][5][N] indexed by ORIGINAL row, merged in rank order
-    KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
+    KD_LAUNCH(K_MERGE, launch_merge(recs, rec_plane, rec_rank_stride, n_ranks, P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, 0, c.idx, 1, c.nonfinite,
                            P.kind == KD_RKL ? 1 : 0, c.s));
     if ((st = backward_chunk(c, row0, loss, dh_dst, dW)) != KD_OK) return st;
@@ -1168,15 +1179,19 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
   if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
-  return vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, n_ranks, loss, dh_s_partial,
+  return vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, (long long)p->n_tokens, 5ll * p->n_tokens, n_ranks,
+                             loss, dh_s_partial,
                              local_rows(dh_s_partial, p->d_s), local_rows(loss, 1), dW_s, n_nonfinite,
                              workspace, workspace_bytes, stream, false);
 }
 
 // ------------------------------------------------------------------------------------ peer exchange (§8, kd_p2p)
 namespace {
+// counter block [0, 256) of an arena: one u32 per SOURCE rank and kind, each written by that rank only — a wait
+// needs every source to have reached the chunk (a shared sum could be satisfied by a rank running ahead)
+constexpr long long kCtrArrivals = 0, kCtrDone = 32, kCtrRecords = 64;
 struct P2PLayout {
-  long long R, set_bytes, lset_bytes, off_slots, off_lslots, off_dh, off_loss, total;
+  long long R, rplane, set_bytes, lset_bytes, rset_bytes, off_slots, off_lslots, off_recs, off_dh, off_loss, total;
 };
 long long align256(long long x) { return (x + 255) / 256 * 256; }
 P2PLayout p2p_layout(int world, long long max_rows, long long max_tokens, int d_s) {
@@ -1186,7 +1201,10 @@ P2PLayout p2p_layout(int world, long long max_rows, long long max_tokens, int d_
   L.lset_bytes = align256((long long)world * L.R * 4);
   L.off_slots = 256;
   L.off_lslots = L.off_slots + kP2PSets * L.set_bytes;
-  L.off_dh = L.off_lslots + kP2PSets * L.lset_bytes;
+  L.rplane = (max_rows + 3) / 4 * 4;                               // record plane stride (16-B aligned planes)
+  L.rset_bytes = align256((long long)world * 5 * L.rplane * 4);   // records [world][5][rplane]
+  L.off_recs = L.off_lslots + kP2PSets * L.lset_bytes;
+  L.off_dh = L.off_recs + kP2PSets * L.rset_bytes;
   L.off_loss = L.off_dh + align256(max_tokens * d_s * 4);
   L.total = L.off_loss + align256(max_tokens * 4);
   return L;
@@ -1220,10 +1238,49 @@ kd_status kd_p2p_outputs(const kd_p2p* x, float** dh_out, float** loss_out) {
   return KD_OK;
 }
 
+kd_status kd_vocab_stats_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                             const uint8_t* mask, void* workspace, size_t workspace_bytes, const kd_p2p* x,
+                             int32_t set, void* stream) {
+  g_launches = 0;
+  g_cur_stream = static_cast<cudaStream_t>(stream);
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  if (!p) return fail(KD_ERR_INVALID_ARG, "problem is NULL");
+  if (set < 0 || set >= kP2PSets) return fail(KD_ERR_INVALID_ARG, "set must be in [0, %d)", kP2PSets);
+  if (p->n_tokens > x->max_rows) return fail(KD_ERR_SHAPE, "n_tokens exceeds the arena's max_rows");
+  if (p->d_s != x->d_s) return fail(KD_ERR_SHAPE, "problem d_s != kd_p2p.d_s");
+  const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
+  const long long slot = L.off_recs + set * L.rset_bytes + (long long)x->rank * 5 * L.rplane * 4;
+  float* own = reinterpret_cast<float*>(arena_at(x, x->rank, slot));
+  if ((st = vocab_stats_impl(p, h_t, W_t, h_s, W_s, mask, own, L.rplane, workspace, workspace_bytes, stream)) !=
+      KD_OK)
+    return st;
+  // all-gather: this rank's record into every peer's slot [rank] of the set, then their record counters + 1
+  P2PCopy cp{};
+  cp.src = own;
+  cp.n_dst = 0;
+  for (int t = 0; t < x->world; ++t)
+    if (t != x->rank) cp.dst[cp.n_dst++] = reinterpret_cast<float*>(arena_at(x, t, slot));
+  cp.n = 5 * L.rplane;
+  cp.rows = p->n_tokens;  // rows >= n_tokens of the planes are never read
+  cp.plane = L.rplane;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cp.n_dst > 0 && p->n_tokens > 0) KD_LAUNCH(K_P2P, launch_p2p_copy(cp, sms, s));
+  P2PFlags f{};
+  f.n = x->world;
+  for (int t = 0; t < x->world; ++t) f.f[t] = reinterpret_cast<unsigned*>(arena_at(x, t, kCtrRecords + 4 * x->rank));
+  KD_LAUNCH(K_P2P, launch_p2p_signal(f, s));
+  return KD_OK;
+}
+
 kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
                                 const void* W_s, const uint8_t* mask, const float* recs, int32_t n_ranks,
                                 float* loss, float* dW_s, int64_t* n_nonfinite, void* workspace,
-                                size_t workspace_bytes, const kd_p2p* x, int32_t set, void* stream) {
+                                size_t workspace_bytes, const kd_p2p* x, int32_t set, uint32_t records_target,
+                                void* stream) {
   g_launches = 0;
   g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = check_p2p(x);
@@ -1246,13 +1303,23 @@ kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void
   dh.ld = x->d_s;
   fl.ld = 1;
   dh.sys_fence = fl.sys_fence = 1;
-  if ((st = vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, n_ranks, p->kind == KD_RKL ? loss : nullptr,
-                                nullptr, dh, fl, dW_s, n_nonfinite, workspace, workspace_bytes, stream, true)) != KD_OK)
+  long long rec_plane = p->n_tokens, rec_rank = 5ll * p->n_tokens;
+  if (!recs) {  // the records all-gathered into this rank's arena by kd_vocab_stats_p2p: wait for all of them
+    recs = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_recs + set * L.rset_bytes));
+    rec_plane = L.rplane;
+    rec_rank = 5ll * L.rplane;
+    KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrRecords)), x->world,
+                                     records_target,
+                                     static_cast<cudaStream_t>(stream)));
+  }
+  if ((st = vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, rec_plane, rec_rank, n_ranks,
+                                p->kind == KD_RKL ? loss : nullptr, nullptr, dh, fl, dW_s, n_nonfinite, workspace,
+                                workspace_bytes, stream, true)) != KD_OK)
     return st;
   // publish: every owner's arrival counter + 1 (one per rank per exchange chunk, also for an empty chunk)
   P2PFlags f{};
   f.n = x->world;
-  for (int j = 0; j < x->world; ++j) f.f[j] = reinterpret_cast<unsigned*>(arena_at(x, j, 0));
+  for (int j = 0; j < x->world; ++j) f.f[j] = reinterpret_cast<unsigned*>(arena_at(x, j, kCtrArrivals + 4 * x->rank));
   KD_LAUNCH(K_P2P, launch_p2p_signal(f, static_cast<cudaStream_t>(stream)));
   return KD_OK;
 }
@@ -1277,7 +1344,7 @@ kd_status kd_p2p_combine(const kd_p2p* x, int32_t set, int64_t n_rows, int64_t r
     c.lout[t] = with_loss ? reinterpret_cast<float*>(arena_at(x, t, L.off_loss)) + row0 : nullptr;
   }
   c.mask = mask;
-  c.arrivals = reinterpret_cast<const unsigned*>(arena_at(x, x->rank, 0));
+  c.arrivals = reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrArrivals));
   c.target = arrivals_target;
   c.P = x->world;
   c.me = x->rank;
@@ -1290,7 +1357,7 @@ kd_status kd_p2p_combine(const kd_p2p* x, int32_t set, int64_t n_rows, int64_t r
   KD_LAUNCH(K_P2P, launch_p2p_combine(c, sms, s));
   P2PFlags f{};
   f.n = x->world;
-  for (int t = 0; t < x->world; ++t) f.f[t] = reinterpret_cast<unsigned*>(arena_at(x, t, 4));
+  for (int t = 0; t < x->world; ++t) f.f[t] = reinterpret_cast<unsigned*>(arena_at(x, t, kCtrDone + 4 * x->rank));
   KD_LAUNCH(K_P2P, launch_p2p_signal(f, s));
   return KD_OK;
 }
@@ -1300,7 +1367,7 @@ kd_status kd_p2p_wait(const kd_p2p* x, uint32_t done_target, void* stream) {
   g_cur_stream = static_cast<cudaStream_t>(stream);
   kd_status st = check_p2p(x);
   if (st != KD_OK) return st;
-  KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, 4)), done_target,
+  KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrDone)), x->world, done_target,
                                    static_cast<cudaStream_t>(stream)));
   return KD_OK;
 }

@@ -743,12 +743,17 @@ __global__ void k_p2p_signal(const P2PFlags f) {
   if (threadIdx.x < f.n) red_release_sys_add_u32(f.f[threadIdx.x], 1u);
 }
 
-__global__ void k_p2p_wait(const unsigned* flag, unsigned target) {
-  if (threadIdx.x == 0) p2p_spin_until(flag, target);
+// ctr[0..n): one counter per source rank; returns when every source has reached `target`
+__device__ void p2p_wait_all(const unsigned* ctr, int n, unsigned target) {
+  for (int t = 0; t < n; ++t) p2p_spin_until(ctr + t, target);
+}
+
+__global__ void k_p2p_wait(const unsigned* ctr, int n, unsigned target) {
+  if (threadIdx.x == 0) p2p_wait_all(ctr, n, target);
 }
 
 __global__ void __launch_bounds__(256) k_p2p_combine(const P2PCombine c) {
-  if (threadIdx.x == 0) p2p_spin_until(c.arrivals, c.target);
+  if (threadIdx.x == 0) p2p_wait_all(c.arrivals, c.P, c.target);
   __syncthreads();
   const long long r0 = (long long)c.me * c.R;
   const long long nr = max(0ll, min(c.n_rows, r0 + c.R) - r0);
@@ -782,12 +787,39 @@ __global__ void __launch_bounds__(256) k_p2p_combine(const P2PCombine c) {
   __threadfence_system();
 }
 
+__global__ void __launch_bounds__(256) k_p2p_copy(const P2PCopy c) {
+  const long long per = (c.rows + 3) / 4;  // float4 groups per plane (plane and the slot are 16-B aligned)
+  const long long total = 5 * per;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long f = e / per, k = (e % per) * 4;
+    const float* src = c.src + f * c.plane + k;
+    const long long left = c.rows - k;
+    if (left >= 4 && (c.plane % 4) == 0) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+      for (int t = 0; t < c.n_dst; ++t) *reinterpret_cast<float4*>(c.dst[t] + f * c.plane + k) = v;
+    } else {
+      for (long long q = 0; q < min(4ll, left); ++q) {
+        const float v = __ldcg(src + q);
+        for (int t = 0; t < c.n_dst; ++t) c.dst[t][f * c.plane + k + q] = v;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+cudaError_t launch_p2p_copy(const P2PCopy& c, int num_sms, cudaStream_t s) {
+  const long long work = 5 * ((c.rows + 3) / 4);
+  const int blocks = (int)std::max(1ll, std::min<long long>(num_sms, (work + 255) / 256));
+  k_p2p_copy<<<blocks, 256, 0, s>>>(c);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_p2p_signal(const P2PFlags& f, cudaStream_t s) {
   k_p2p_signal<<<1, 32, 0, s>>>(f);
   return cudaGetLastError();
 }
-cudaError_t launch_p2p_wait(const unsigned* flag, unsigned target, cudaStream_t s) {
-  k_p2p_wait<<<1, 32, 0, s>>>(flag, target);
+cudaError_t launch_p2p_wait(const unsigned* ctr, int n, unsigned target, cudaStream_t s) {
+  k_p2p_wait<<<1, 32, 0, s>>>(ctr, n, target);
   return cudaGetLastError();
 }
 cudaError_t launch_p2p_combine(const P2PCombine& c, int num_sms, cudaStream_t s) {

@@ -124,13 +124,20 @@ struct P2PCombine {
   float* out[kP2PMaxRanks];         // rank t's dh_out + row0·d_s, as mapped in this process
   float* lout[kP2PMaxRanks];        // rank t's loss_out + row0 (FKL), or NULL
   const uint8_t* mask;              // the chunk's mask [n_rows] or NULL: masked rows get 0 (never read)
-  const unsigned* arrivals;         // this owner's arrival counter
-  unsigned target;                  // wait until *arrivals - target >= 0 (wrap-safe)
+  const unsigned* arrivals;         // this owner's arrival counters [P], one per source rank
+  unsigned target;                  // wait until arrivals[t] - target >= 0 for every t (wrap-safe)
   int P, me, d_s;
   long long R, n_rows;              // rows per owner (ceil(n_rows / P)) and the chunk's rows
 };
+// kd_vocab_stats_p2p: this rank's record planes [5][plane] (rows < `rows` valid) copied into n_dst peers' slots.
+struct P2PCopy {
+  const float* src;
+  float* dst[kP2PMaxRanks];
+  int n_dst;
+  long long n, rows, plane;
+};
 struct P2PFlags {
-  unsigned* f[kP2PMaxRanks];        // one counter per rank (as mapped in this process)
+  unsigned* f[kP2PMaxRanks];        // this rank's counter slot in each destination arena (as mapped here)
   int n;
 };
 

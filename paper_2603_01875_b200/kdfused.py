@@ -22,7 +22,7 @@ STATUS = {0: "KD_OK", 1: "KD_ERR_INVALID_ARG", 2: "KD_ERR_SHAPE", 3: "KD_ERR_ALI
 EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_teacher_lse", "kd_fused_fwd_bwd_lse",
             "kd_teacher_topk", "kd_topk_fwd_bwd",
             "kd_vocab_stats", "kd_vocab_backward",
-            "kd_vocab_partials", "kd_vocab_finish", "kd_p2p_arena_bytes", "kd_p2p_outputs", "kd_vocab_backward_p2p",
+            "kd_vocab_partials", "kd_vocab_finish", "kd_p2p_arena_bytes", "kd_p2p_outputs", "kd_vocab_stats_p2p", "kd_vocab_backward_p2p",
             "kd_p2p_combine", "kd_p2p_wait", "kd_handoff_export", "kd_handoff_open", "kd_handoff_close",
             "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
@@ -92,7 +92,10 @@ def lib() -> ctypes.CDLL:
     L.kd_p2p_arena_bytes.restype = sz
     L.kd_p2p_outputs.argtypes = [X, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
     L.kd_p2p_outputs.restype = ctypes.c_int
-    L.kd_vocab_backward_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, i64p, vp, sz, X, i32, vp]
+    L.kd_vocab_stats_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, sz, X, i32, vp]
+    L.kd_vocab_stats_p2p.restype = ctypes.c_int
+    L.kd_vocab_backward_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, i64p, vp, sz, X, i32, ctypes.c_uint32,
+                                        vp]
     L.kd_vocab_backward_p2p.restype = ctypes.c_int
     L.kd_p2p_combine.argtypes = [X, i32, ctypes.c_int64, ctypes.c_int64, vp, i32, ctypes.c_uint32, vp]
     L.kd_p2p_combine.restype = ctypes.c_int
@@ -431,11 +434,28 @@ def p2p_outputs(x: KDP2P, device, n_tokens: int, d_s: int):
     return dh_t, ls_t
 
 
+def vocab_stats_p2p(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, x: KDP2P, set: int, vocab, v_begin, T=1.0,
+                    kind="fkl", chunk_tokens=0, stream=None, workspace=None):
+    """kd_vocab_stats_p2p: this shard's record into record set ``set`` of every rank's arena (the all-gather)."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(t, "input") for t in (h_t, W_t_shard, h_s, W_s_shard))
+    N, d_t = h_t.shape
+    V_r, d_s = W_s_shard.shape
+    p = make_problem(N, d_t, d_s, vocab, T=T, kind=kind, v_begin=v_begin, v_end=v_begin + V_r,
+                     chunk_tokens=chunk_tokens)
+    if mask is not None:
+        mask = mask.to(device=h_t.device, dtype=torch.uint8).contiguous()
+    ws = _workspace(workspace_size(p), h_t.device, stream, workspace)
+    _check(lib().kd_vocab_stats_p2p(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                    _ptr(mask), _ptr(ws), ws.numel(), ctypes.byref(x), int(set),
+                                    _stream_handle(stream)))
+
+
 def vocab_backward_p2p(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, x: KDP2P, set: int, vocab, v_begin,
                        T=1.0, kind="fkl", loss_scale=1.0, want_dW=False, accumulate_dW=False, dW_s=None,
-                       chunk_tokens=0, stream=None, workspace=None) -> KDResult:
+                       chunk_tokens=0, records_target: int = 0, stream=None, workspace=None) -> KDResult:
     """kd_vocab_backward_p2p: as vocab_backward, but the partial dh_s (and FKL's partial loss) rows go straight to
-    their owners' receive slots of set ``set``; the result carries the local loss (RKL) and dW_s only."""
+    their owners' receive slots of set ``set``; the result carries the local loss (RKL) and dW_s only.
+    recs=None: the records kd_vocab_stats_p2p gathered into the arena (waiting for ``records_target``)."""
     h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(t, "input") for t in (h_t, W_t_shard, h_s, W_s_shard))
     N, d_t = h_t.shape
     V_r, d_s = W_s_shard.shape
@@ -444,16 +464,20 @@ def vocab_backward_p2p(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, x: KD
                      accumulate_dW=accumulate_dW, v_begin=v_begin, v_end=v_begin + V_r, chunk_tokens=chunk_tokens)
     if mask is not None:
         mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
-    recs = recs.to(device=dev, dtype=torch.float32).contiguous()
+    n_ranks = x.world
+    if recs is not None:
+        recs = recs.to(device=dev, dtype=torch.float32).contiguous()
+        n_ranks = int(recs.shape[0])
     loss = torch.empty(N, dtype=torch.float32, device=dev) if kind == "rkl" else None
     nnf = torch.zeros(1, dtype=torch.int64, device=dev)
     if want_dW and dW_s is None:
         dW_s = (torch.zeros if accumulate_dW else torch.empty)(V_r, d_s, dtype=torch.float32, device=dev)
     ws = _workspace(workspace_size(p), dev, stream, workspace)
     _check(lib().kd_vocab_backward_p2p(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
-                                       _ptr(mask), _ptr(recs), int(recs.shape[0]), _ptr(loss),
+                                       _ptr(mask), _ptr(recs), n_ranks, _ptr(loss),
                                        _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),
-                                       ctypes.byref(x), int(set), _stream_handle(stream)))
+                                       ctypes.byref(x), int(set), int(records_target) & 0xFFFFFFFF,
+                                       _stream_handle(stream)))
     return KDResult(loss, None, dW_s if want_dW else None, nnf)
 
 

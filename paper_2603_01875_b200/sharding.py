@@ -217,11 +217,15 @@ class P2PExchange:
     def set_of(self, chunk: int) -> int:
         return chunk % 3
 
+    # every counter is per source rank (kdfused.h): after chunk g, each source has raised its counter g + 1 times
     def arrivals_target(self, chunk: int) -> int:
-        return (chunk + 1) * self.world
+        return chunk + 1
 
     def done_target(self, chunk: int) -> int:
-        return (chunk + 1) * self.world
+        return chunk + 1
+
+    def records_target(self, chunk: int) -> int:
+        return chunk + 1
 
     def close(self):
         for m in self.mapped:
@@ -229,19 +233,23 @@ class P2PExchange:
         self.mapped = []
 
 
-def _p2p_step(ex: P2PExchange, spans, stats, backward_p2p, combine, wait, outputs, *, mask, kind, N, d_s, device):
-    """The per-rank p2p pipeline of one step (the records exchange as in the NCCL path):
+def _p2p_step(ex: P2PExchange, spans, stats_p2p, backward_p2p, combine, wait, outputs, *, mask, kind, N, device):
+    """The per-rank p2p pipeline of one step — no NCCL call on the data path:
 
-        stats(i+1) ‖ records(i) ;  [wait done(i-3)] backward_p2p(i) -> slots ;  combine(i-1) (deferred)
-        end: combine(last) ; wait done(all)
+        stats_p2p(0)
+        per chunk i:  stats_p2p(i+1)  [records into every rank's arena]
+                      [wait done(i-3)]  backward_p2p(i)  [waits for the P records of i; partial rows -> owners]
+                      combine(i-1)  (deferred behind chunk i's kernels: the P arrivals of i-1 are long there)
+        end:          combine(last) ; wait done(all)
 
-    Chunk g (counted over the exchange's life) uses slot set g % 3; reusing it needs every owner's combine of chunk
-    g - 3 done (a done target), checked only inside a step — the previous step ended waiting for all of its chunks."""
+    Chunk g (counted over the exchange's life) uses set g % 3 of the dh slots and of the records.  Reusing a dh slot
+    set needs every owner's combine of chunk g - 3 (a done target); a record set is rewritten by stats_p2p(g) only
+    after this rank ran combine(g - 3), which waited for every rank's backward of g - 3 (the set's last reader).
+    The previous step ended waiting for all of its chunks."""
     base = ex.chunks
     n = len(spans)
     loss_rkl = None
     dW = None
-    nxt = stats(0) if spans else None
 
     def do_combine(i):
         a, b = spans[i]
@@ -249,15 +257,15 @@ def _p2p_step(ex: P2PExchange, spans, stats, backward_p2p, combine, wait, output
         combine(ex, ex.set_of(g), b - a, a, None if mask is None else mask[a:b], with_loss=(kind == "fkl"),
                 target=ex.arrivals_target(g))
 
+    if n:
+        stats_p2p(0, ex.set_of(base))
     for i, (a, b) in enumerate(spans):
-        recs_out, work = nxt
-        if i + 1 < n:
-            nxt = stats(i + 1)
-        work.wait()
         g = base + i
+        if i + 1 < n:
+            stats_p2p(i + 1, ex.set_of(g + 1))
         if i >= 3:
             wait(ex, ex.done_target(g - 3))
-        r = backward_p2p(i, _gathered(recs_out), ex.set_of(g), dW)
+        r = backward_p2p(i, ex.set_of(g), dW, ex.records_target(g))
         if kind == "rkl":
             if loss_rkl is None:  # the kernels' dtype (fp32; the CPU test stand-ins return fp64)
                 loss_rkl = torch.zeros(N, dtype=r.loss.dtype, device=r.loss.device)
@@ -341,17 +349,22 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
             raise ValueError(f"step of {N} tokens / exchange chunk {chunk} exceeds the arena "
                              f"({exchange.max_tokens} / {exchange.max_rows})")
         from . import kdfused
-        f = dict(backward=kdfused.vocab_backward_p2p, combine=kdfused.p2p_combine, wait=kdfused.p2p_wait,
-                 outputs=lambda ex, n: kdfused.p2p_outputs(ex.x, h_t.device, n, d_s))
+        f = dict(stats=kdfused.vocab_stats_p2p, backward=kdfused.vocab_backward_p2p, combine=kdfused.p2p_combine,
+                 wait=kdfused.p2p_wait, outputs=lambda ex, n: kdfused.p2p_outputs(ex.x, h_t.device, n, d_s))
         f.update(p2p_fns or {})
 
-        def backward_p2p(i, recs, set_, dW_cur):
+        def stats_p2p(i, set_):
             a, b = spans[i]
-            return f["backward"](h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, recs,
+            f["stats"](h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, None if mask is None else mask[a:b], x=exchange.x,
+                       set=set_, vocab=vocab, v_begin=v_begin, T=T, kind=kind, chunk_tokens=chunk_tokens)
+
+        def backward_p2p(i, set_, dW_cur, rec_target):
+            a, b = spans[i]
+            return f["backward"](h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, None,
                                  None if mask is None else mask[a:b], x=exchange.x, set=set_, vocab=vocab,
                                  v_begin=v_begin, T=T, kind=kind, loss_scale=loss_scale, want_dW=want_dW,
                                  accumulate_dW=accumulate_dW or i > 0, dW_s=dW_cur if i > 0 else dW_s,
-                                 chunk_tokens=chunk_tokens)
+                                 chunk_tokens=chunk_tokens, records_target=rec_target)
 
         def combine(ex, set_, n_rows, row0, m, *, with_loss, target):
             f["combine"](ex.x, set_, n_rows, row0, m, with_loss=with_loss, target=target)
@@ -359,8 +372,8 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
         def wait(ex, target):
             f["wait"](ex.x, target)
 
-        r = _p2p_step(exchange, spans, stats, backward_p2p, combine, wait, f["outputs"], mask=mask, kind=kind, N=N,
-                      d_s=d_s, device=h_t.device)
+        r = _p2p_step(exchange, spans, stats_p2p, backward_p2p, combine, wait, f["outputs"], mask=mask, kind=kind,
+                      N=N, device=h_t.device)
         return _Result(r.loss, r.dh_s, r.dW_s if want_dW else None)
 
     nxt = stats(0) if spans else None
@@ -419,7 +432,7 @@ def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0
                               want_dW=False, chunk_tokens=0, exchange_chunk=0):
     """One-GPU emulation of the P-rank p2p step (tests, ``bench.py --sim-p2p``): the P ranks' kernels run in one
     stream in an order where every counter a kernel waits on was raised by an EARLIER launch (per exchange chunk: all
-    ranks' stats, then all ranks' backward_p2p, then all owners' combine) — no kernel waits on one launched after it,
+    ranks' stats_p2p, then all ranks' backward_p2p, then all owners' combine) — no kernel waits on one launched after it,
     so nothing depends on two launches running concurrently.  The kernels, slot addressing, counters and set rotation
     are the multi-GPU ones; the 'peer' arenas are local allocations (``P2PExchange.local_group``).
 
@@ -437,17 +450,20 @@ def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0
     loss_rkl = [torch.zeros(N, dtype=torch.float32, device=h_t.device) for _ in range(P)] if kind == "rkl" else None
     for i, (a, b) in enumerate(spans):
         m_c = None if mask is None else mask[a:b]
-        recs = torch.stack([kdfused.vocab_stats(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], m_c, vocab=V, v_begin=v0,
-                                                T=T, kind=kind, chunk_tokens=chunk_tokens) for v0, v1 in bounds])
         g = base + i
+        for r, (v0, v1) in enumerate(bounds):  # every rank's record into every rank's arena
+            kdfused.vocab_stats_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], m_c, x=exchanges[r].x,
+                                    set=exchanges[r].set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
+                                    chunk_tokens=chunk_tokens)
         for r, (v0, v1) in enumerate(bounds):
             ex = exchanges[r]
             if i >= 3:
                 kdfused.p2p_wait(ex.x, ex.done_target(g - 3))
-            res = kdfused.vocab_backward_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], recs, m_c, x=ex.x,
+            res = kdfused.vocab_backward_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], None, m_c, x=ex.x,
                                              set=ex.set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
                                              loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=i > 0,
-                                             dW_s=dW[r], chunk_tokens=chunk_tokens)
+                                             dW_s=dW[r], chunk_tokens=chunk_tokens,
+                                             records_target=ex.records_target(g))
             if want_dW:
                 dW[r] = res.dW_s
             if kind == "rkl":

@@ -1,12 +1,15 @@
 """Multi-process (world_size 2, gloo, CPU) test of the host protocol of the peer-memory exchange
 (sharding.vocab_sharded_fwd_bwd(exchange=P2PExchange), kdfused.h kd_p2p).
 
-The CUDA kernels and peer mappings cannot run here, so the four kernel-side callables are CPU stand-ins over
-shared-memory "arenas" created by the parent: the backward stand-in writes each partial dh_s / loss row into its
+The CUDA kernels and peer mappings cannot run here, so the five kernel-side callables are CPU stand-ins over
+shared-memory "arenas" created by the parent: the stats stand-in writes its record into every rank's record set and
+raises their record counters; the backward stand-in waits for the P records and writes each partial dh_s / loss row into its
 owner's receive slot (owner = row // R, R = ceil(n / P)) of the chunk's slot set and then raises its arrival
 counter; the combine stand-in polls the arrivals, sums the slots in rank order, stores the sum into every rank's
 dh_out / loss_out and raises the done counters; the wait stand-in polls the done counters.  Every counter entry
-is written by one process only (a per-source entry), so the stand-ins need no atomics.  What is under test is the
+is written by one process only (a per-source entry, as in the arena's counter block), so the stand-ins need no
+atomics, and a wait needs every source at the chunk (an early version summed the sources: a rank running a chunk
+ahead satisfied the sum — this test caught it).  What is under test is the
 product's protocol: slot-set rotation over five exchange chunks, the set-reuse waits, the deferred combine, the
 counter targets across two steps, and the result, against the fp64 oracle."""
 import os
@@ -36,6 +39,8 @@ def _arena(world, max_rows, max_tokens, d_s):
     R = -(-max_rows // world)
     return dict(arr=torch.zeros(world, dtype=torch.int64).share_memory_(),    # [src]: chunks src pushed here
                 done=torch.zeros(world, dtype=torch.int64).share_memory_(),   # [owner]: chunks owner combined
+                nrec=torch.zeros(world, dtype=torch.int64).share_memory_(),   # [src]: records src wrote here
+                recs=torch.zeros(3, world, 5, max_rows, dtype=torch.float64).share_memory_(),
                 slots=torch.zeros(3, world, R, d_s, dtype=torch.float64).share_memory_(),
                 lslots=torch.zeros(3, world, R, dtype=torch.float64).share_memory_(),
                 dh=torch.zeros(max_tokens, d_s, dtype=torch.float64).share_memory_(),
@@ -57,12 +62,28 @@ def _poll(fn, what):
         time.sleep(0.001)
 
 
+def _stats_p2p_standin(h_t, Wt, h_s, Ws, mask, *, x, set, vocab, v_begin, T, kind, chunk_tokens):
+    time.sleep(0.004 * (x.world - 1 - x.rank))  # skew: rank 0 lags in its stats, rank 1 in its backward
+    rec = _stats_standin(h_t, Wt, h_s, Ws, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
+                         chunk_tokens=chunk_tokens)
+    n = h_t.shape[0]
+    for a in x.arenas:  # the all-gather: this rank's record into slot [rank] of every rank's record set
+        a["recs"][set, x.rank, :, :n] = rec
+    for a in x.arenas:
+        a["nrec"][x.rank] += 1
+
+
 def _backward_p2p_standin(h_t, Wt, h_s, Ws, recs, mask, *, x, set, vocab, v_begin, T, kind, loss_scale, want_dW,
-                          accumulate_dW, dW_s, chunk_tokens):
+                          accumulate_dW, dW_s, chunk_tokens, records_target):
+    me = x.arenas[x.rank]
+    n = h_t.shape[0]
+    time.sleep(0.004 * x.rank)
+    assert recs is None  # the product path reads the records from the arena
+    _poll(lambda: int(me["nrec"].min()) >= records_target, f"records {records_target}")
+    recs = me["recs"][set, :, :, :n].clone()
     r = _backward_standin(h_t, Wt, h_s, Ws, recs, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
                           loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
                           chunk_tokens=chunk_tokens)
-    n = h_t.shape[0]
     R = -(-n // x.world)
     for row in range(n):  # masked rows are not pushed (the owner writes their zeros)
         if mask is not None and mask[row] == 0:
@@ -80,7 +101,7 @@ def _backward_p2p_standin(h_t, Wt, h_s, Ws, recs, mask, *, x, set, vocab, v_begi
 
 def _combine_standin(x, set, n_rows, row0, mask, *, with_loss, target):
     me = x.arenas[x.rank]
-    _poll(lambda: int(me["arr"].sum()) >= target, f"arrivals {target}")
+    _poll(lambda: int(me["arr"].min()) >= target, f"arrivals {target}")
     R = -(-n_rows // x.world)
     r0 = x.rank * R
     for i in range(max(0, min(n_rows, r0 + R) - r0)):
@@ -101,7 +122,7 @@ def _combine_standin(x, set, n_rows, row0, mask, *, with_loss, target):
 
 def _wait_standin(x, target):
     me = x.arenas[x.rank]
-    _poll(lambda: int(me["done"].sum()) >= target, f"done {target}")
+    _poll(lambda: int(me["done"].min()) >= target, f"done {target}")
 
 
 def _worker(rank, world, port, kind, arenas, q):
@@ -116,13 +137,13 @@ def _worker(rank, world, port, kind, arenas, q):
         a, b = vocab_shard_bounds(V, world, granule=16)[rank]
         ex = P2PExchange(world, rank, D_S, CHUNK, N, [0] * world, own=None)
         ex.x = _X(rank, arenas)
-        fns = dict(backward=_backward_p2p_standin, combine=_combine_standin, wait=_wait_standin,
+        fns = dict(stats=_stats_p2p_standin, backward=_backward_p2p_standin, combine=_combine_standin,
+                   wait=_wait_standin,
                    outputs=lambda e, n: (e.x.arenas[e.rank]["dh"][:n].clone(), e.x.arenas[e.rank]["loss"][:n].clone()))
         outs = []
         for step in range(2):  # counters and slot sets carry over into the second step
             r = vocab_sharded_fwd_bwd(ht, Wt[a:b], hs, Ws[a:b], torch.tensor(mask), vocab=V, v_begin=a, T=1.3,
-                                      kind=kind, want_dW=True, exchange_chunk=CHUNK, stats_fn=_stats_standin,
-                                      exchange=ex, p2p_fns=fns)
+                                      kind=kind, want_dW=True, exchange_chunk=CHUNK, exchange=ex, p2p_fns=fns)
             outs.append((r.loss.numpy().copy(), r.dh_s.numpy().copy(), r.dW_s.numpy().copy()))
             dist.barrier()  # the next step overwrites dh_out: both ranks have read this one
         q.put((rank, (a, b), ex.chunks, outs))
@@ -161,3 +182,4 @@ def test_p2p_exchange_protocol_world2(kind):
     np.testing.assert_allclose(dW_cat, dW, rtol=1e-11, atol=1e-13)
     for a in arenas:  # every owner combined every chunk of both steps for every rank
         assert int(a["done"].sum()) == WORLD * 2 * n_chunks and int(a["arr"].sum()) == WORLD * 2 * n_chunks
+        assert int(a["nrec"].sum()) == WORLD * 2 * n_chunks
