@@ -71,7 +71,7 @@ def parse():
                     help="1 GPU: time rank 0's share of a P-way vocab-sharded strong-scaling step (all tokens, its "
                          "V/P head rows; compute only, identity exchanges) and report the projected efficiency")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 vocab-sharded FKL/RKL step: the partial-dh exchange over NCCL (default) or the library's "
+                    help="N>1 vocab-sharded step: the partial-dh exchange over NCCL (default) or the library's "
                          "peer-memory exchange (kd_vocab_backward_p2p: dh rows stored from the dh reduction straight "
                          "into the owners' slots over NVLink, owners' rank-order sums stored into every rank; CUDA IPC "
                          "arenas mapped once before the timing)")
@@ -332,7 +332,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     dW = torch.empty(v1 - v0, cfg.d_s, dtype=torch.float32, device=dev) if want_dW else None
     kw = dict(vocab=cfg.vocab, v_begin=v0, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, loss_scale=1.0,
               want_dW=want_dW, accumulate_dW=False, group=group, dh_reduce="scatter" if own_tokens else "all")
-    p2p = (args.exchange == "p2p" and world > 1 and not sim and not own_tokens and cfg.kind in ("fkl", "rkl"))
+    p2p = args.exchange == "p2p" and world > 1 and not sim and not own_tokens
     if p2p:  # arenas allocated and peer-mapped once (CUDA IPC), outside the timing
         chunk_p2p = sharding.default_exchange_chunk(n_all, v1 - v0, cfg.kind)
         kw["exchange"] = sharding.P2PExchange.create(group, cfg.d_s, max_rows=chunk_p2p, max_tokens=n_all, device=dev)
@@ -392,7 +392,8 @@ def p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW):
 
     def step():
         res["r"] = sharding.vocab_sharded_p2p_one_gpu(Ht, Wt, Hs, Ws, mask, exchanges=exs, T=cfg.temperature,
-                                                     kind=cfg.kind, want_dW=want_dW, exchange_chunk=chunk)
+                                                     kind=cfg.kind, beta=cfg.jsd_beta, want_dW=want_dW,
+                                                     exchange_chunk=chunk)
 
     t = timer.run(step, args.steps, args.warmup)
     prof = timer.profiled(kd, step, args.steps)
@@ -836,7 +837,7 @@ def main():
                 "frac": b / (t_l / n_l / 1e3) / 1e9 / pk["hbm_gbs"],
                 "algorithmic_per_launch": f"tokens*V*(8 + {wb}) B = {b:.4g}"}
 
-    if args.sim_p2p > 1 and world == 1 and cfg.kind in ("fkl", "rkl"):
+    if args.sim_p2p > 1 and world == 1:
         alongside["p2p_one_gpu"] = p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW)
 
     if args.handoff and world == 1:

@@ -183,7 +183,7 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
                             float* loss, float* dh_s_partial, float* dW_s, int64_t* n_nonfinite,
                             void* workspace, size_t workspace_bytes, void* stream);
 
-/* ---- peer-memory exchange of the FKL/RKL vocab-sharded step (the north star's "NCCL
+/* ---- peer-memory exchange of the vocab-sharded step (the north star's "NCCL
  * all-reduce over NVLink" of the partial dh_s done by the library's own kernels over NVSwitch peer memory).
  * The partial dh_s / FKL loss rows of a shard leave the dh split-K reduction (k_reduce_dh) and the loss
  * reduction straight into the OWNING rank's receive slot — a reduce-scatter fused into the kernel that
@@ -194,13 +194,14 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
  * first use; every rank maps every other rank's arena, e.g. kd_handoff_export/open = CUDA IPC over NVLink):
  *   [0, 256)   counters, one u32 per SOURCE rank t (written by rank t only): arrivals[t] at byte 4t
  *              (rank t pushed its partials of a chunk here), done[t] at byte 32 + 4t (owner t stored its
- *              sums of a chunk here), records[t] at byte 64 + 4t (rank t's record of a chunk is here).
+ *              sums of a chunk here), records[t] at byte 64 + 4t (rank t's record of a chunk is here),
+ *              kj[t] at byte 96 + 4t (JSD/TVD: rank t's (K, J) partials of a chunk are here).
  *              A wait for chunk c needs EVERY source at c+1 (a shared sum could be satisfied by a rank
  *              running a chunk ahead).  Counters only grow (modulo 2^32, compared wrap-safe); after k
  *              exchange chunks every counter is k, so the caller's target for chunk c is base + c + 1.
- *   then       3 sets each of receive slots [world][R][d_s] f32, loss slots [world][R] f32 and records
- *              [world][5][ceil4(max_rows)] f32, R = ceil(max_rows / world); dh_out [max_tokens][d_s] f32;
- *              loss_out [max_tokens] f32.
+ *   then       3 sets each of receive slots [world][R][d_s] f32, loss slots [world][R] f32, records
+ *              [world][5][ceil4(max_rows)] f32 and (K, J) partials [world][2][ceil4(max_rows)] f32,
+ *              R = ceil(max_rows / world); dh_out [max_tokens][d_s] f32; loss_out [max_tokens] f32.
  * Protocol per exchange chunk c (n_c <= max_rows tokens, rows [row0, row0 + n_c) of the step), every rank:
  *   kd_vocab_stats_p2p(set = c % 3)           its record into every rank's record set (the all-gather);
  *                                              then records[rank] of every rank += 1
@@ -251,6 +252,21 @@ kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void
                                 float* loss, float* dW_s, int64_t* n_nonfinite, void* workspace,
                                 size_t workspace_bytes, const kd_p2p* x, int32_t set, uint32_t records_target,
                                 void* stream);
+/* JSD/TVD shards with the exchange (one token chunk per call pair, as kd_vocab_partials / kd_vocab_finish):
+ *   kd_vocab_partials_p2p waits for the P records of set `set` (records_target), merges them, runs pass 2 (G
+ *     planes kept in `workspace`) and all-gathers this shard's (K, J) partials into every rank's arena; then
+ *     kj[rank] of every rank += 1.
+ *   kd_vocab_finish_p2p (same problem, inputs, workspace) waits for the P (K, J) partials (kj_target), sums them
+ *     in rank order, writes the full per-token `loss` (local), the G fix-up, the local dW_s rows, and stores the
+ *     partial dh_s rows into their owners' slots; then arrivals[rank] of every owner += 1.  kd_p2p_combine
+ *     with with_loss = 0 follows as for FKL/RKL. */
+kd_status kd_vocab_partials_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                const void* W_s, const uint8_t* mask, void* workspace, size_t workspace_bytes,
+                                const kd_p2p* x, int32_t set, uint32_t records_target, void* stream);
+kd_status kd_vocab_finish_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                              const void* W_s, const uint8_t* mask, float* loss, float* dW_s,
+                              int64_t* n_nonfinite, void* workspace, size_t workspace_bytes, const kd_p2p* x,
+                              int32_t set, uint32_t kj_target, void* stream);
 /* Owner side of exchange chunk `set`: n_rows = the chunk's tokens, row0 = its first row in dh_out,
  * mask = the chunk's mask [n_rows] or NULL, with_loss = 1 for FKL (sum the partial losses).
  * Errors: KD_ERR_SHAPE if n_rows > max_rows or row0 + n_rows > max_tokens. */

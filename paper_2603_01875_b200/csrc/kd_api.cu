@@ -771,7 +771,7 @@ static kd_status grad_chunk(Ctx& c, int row0, int side_lo = 0) {
 // After pass 2: [JSD/TVD fix-up with the local K partials, or with the P ranks' per-token totals kj_ranks]
 // + dh GEMM (+ split-K reduce) + dW GEMM for one chunk.
 static kd_status finish_chunk(Ctx& c, int row0, float* loss, const RowDst& dh, float* dW, const float* kj_ranks,
-                              int n_ranks, int topk = 0) {
+                              int n_ranks, int topk = 0, long long kj_plane = -1) {
   const Plan& P = c.P;
   const kd_problem* p = c.p;
   PassParams pp = pass_params(c, row0);
@@ -781,7 +781,8 @@ static kd_status finish_chunk(Ctx& c, int row0, float* loss, const RowDst& dh, f
                                                  : 0.5 * cscale);
     KD_LAUNCH(K_KFIX, launch_kfix(pp.kpart, P.n_gslots, P.Nc, row0, c.n_eff, P.kind, p->jsd_beta,
                           ws_at<float>(c.ws, P.off_kfin), loss, c.idx, c.nonfinite, pp.g_a, pp.g_b, P.g_ld, scale,
-                          pp.g_hi, pp.g_lo, P.num_sms, kj_ranks, n_ranks, (long long)P.N, c.s));
+                          pp.g_hi, pp.g_lo, P.num_sms, kj_ranks, n_ranks, kj_plane >= 0 ? kj_plane : (long long)P.N,
+                          c.s));
   }
   kd_status st;
   if (dW) {
@@ -1189,9 +1190,10 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
 namespace {
 // counter block [0, 256) of an arena: one u32 per SOURCE rank and kind, each written by that rank only — a wait
 // needs every source to have reached the chunk (a shared sum could be satisfied by a rank running ahead)
-constexpr long long kCtrArrivals = 0, kCtrDone = 32, kCtrRecords = 64;
+constexpr long long kCtrArrivals = 0, kCtrDone = 32, kCtrRecords = 64, kCtrKJ = 96;
 struct P2PLayout {
-  long long R, rplane, set_bytes, lset_bytes, rset_bytes, off_slots, off_lslots, off_recs, off_dh, off_loss, total;
+  long long R, rplane, set_bytes, lset_bytes, rset_bytes, kjset_bytes, off_slots, off_lslots, off_recs, off_kj, off_dh,
+      off_loss, total;
 };
 long long align256(long long x) { return (x + 255) / 256 * 256; }
 P2PLayout p2p_layout(int world, long long max_rows, long long max_tokens, int d_s) {
@@ -1203,8 +1205,10 @@ P2PLayout p2p_layout(int world, long long max_rows, long long max_tokens, int d_
   L.off_lslots = L.off_slots + kP2PSets * L.set_bytes;
   L.rplane = (max_rows + 3) / 4 * 4;                               // record plane stride (16-B aligned planes)
   L.rset_bytes = align256((long long)world * 5 * L.rplane * 4);   // records [world][5][rplane]
+  L.kjset_bytes = align256((long long)world * 2 * L.rplane * 4);  // JSD/TVD (K, J) partials [world][2][rplane]
   L.off_recs = L.off_lslots + kP2PSets * L.lset_bytes;
-  L.off_dh = L.off_recs + kP2PSets * L.rset_bytes;
+  L.off_kj = L.off_recs + kP2PSets * L.rset_bytes;
+  L.off_dh = L.off_kj + kP2PSets * L.kjset_bytes;
   L.off_loss = L.off_dh + align256(max_tokens * d_s * 4);
   L.total = L.off_loss + align256(max_tokens * 4);
   return L;
@@ -1238,6 +1242,42 @@ kd_status kd_p2p_outputs(const kd_p2p* x, float** dh_out, float** loss_out) {
   return KD_OK;
 }
 
+// The all-gather of a per-rank block ([planes][rplane] f32 at byte offset `slot` of every arena): copy this rank's
+// block into every peer's, then raise counter `ctr` [rank] in every arena.
+static kd_status p2p_allgather(const kd_p2p* x, long long slot, int planes, long long rows, long long plane,
+                               long long ctr, cudaStream_t s) {
+  P2PCopy cp{};
+  cp.src = reinterpret_cast<const float*>(arena_at(x, x->rank, slot));
+  cp.n_dst = 0;
+  for (int t = 0; t < x->world; ++t)
+    if (t != x->rank) cp.dst[cp.n_dst++] = reinterpret_cast<float*>(arena_at(x, t, slot));
+  cp.planes = planes;
+  cp.rows = rows;
+  cp.plane = plane;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cp.n_dst > 0 && rows > 0) KD_LAUNCH(K_P2P, launch_p2p_copy(cp, sms, s));
+  P2PFlags f{};
+  f.n = x->world;
+  for (int t = 0; t < x->world; ++t) f.f[t] = reinterpret_cast<unsigned*>(arena_at(x, t, ctr + 4 * x->rank));
+  KD_LAUNCH(K_P2P, launch_p2p_signal(f, s));
+  return KD_OK;
+}
+
+static RowDst p2p_dh_dst(const kd_p2p* x, const P2PLayout& L, int set, long long n_tokens, bool loss) {
+  RowDst d{};
+  const long long R = (n_tokens + x->world - 1) / x->world;  // rows per owner in this exchange chunk
+  for (int j = 0; j < x->world; ++j)
+    d.base[j] = reinterpret_cast<float*>(
+        arena_at(x, j, loss ? L.off_lslots + set * L.lset_bytes : L.off_slots + set * L.set_bytes));
+  d.rows_per_owner = R > 0 ? R : 1;
+  d.src_row = (long long)x->rank * R;
+  d.ld = loss ? 1 : x->d_s;
+  d.sys_fence = 1;
+  return d;
+}
+
 kd_status kd_vocab_stats_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
                              const uint8_t* mask, void* workspace, size_t workspace_bytes, const kd_p2p* x,
                              int32_t set, void* stream) {
@@ -1256,24 +1296,7 @@ kd_status kd_vocab_stats_p2p(const kd_problem* p, const void* h_t, const void* W
       KD_OK)
     return st;
   // all-gather: this rank's record into every peer's slot [rank] of the set, then their record counters + 1
-  P2PCopy cp{};
-  cp.src = own;
-  cp.n_dst = 0;
-  for (int t = 0; t < x->world; ++t)
-    if (t != x->rank) cp.dst[cp.n_dst++] = reinterpret_cast<float*>(arena_at(x, t, slot));
-  cp.n = 5 * L.rplane;
-  cp.rows = p->n_tokens;  // rows >= n_tokens of the planes are never read
-  cp.plane = L.rplane;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (cp.n_dst > 0 && p->n_tokens > 0) KD_LAUNCH(K_P2P, launch_p2p_copy(cp, sms, s));
-  P2PFlags f{};
-  f.n = x->world;
-  for (int t = 0; t < x->world; ++t) f.f[t] = reinterpret_cast<unsigned*>(arena_at(x, t, kCtrRecords + 4 * x->rank));
-  KD_LAUNCH(K_P2P, launch_p2p_signal(f, s));
-  return KD_OK;
+  return p2p_allgather(x, slot, 5, p->n_tokens, L.rplane, kCtrRecords, static_cast<cudaStream_t>(stream));
 }
 
 kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
@@ -1292,17 +1315,7 @@ kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void
   if (p->n_tokens > x->max_rows) return fail(KD_ERR_SHAPE, "n_tokens exceeds the arena's max_rows");
   if (p->kind == KD_RKL && p->n_tokens > 0 && !loss) return fail(KD_ERR_INVALID_ARG, "RKL needs the local loss buffer");
   const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
-  const long long R = (p->n_tokens + x->world - 1) / x->world;  // rows per owner in this exchange chunk
-  RowDst dh{}, fl{};
-  for (int j = 0; j < x->world; ++j) {
-    dh.base[j] = reinterpret_cast<float*>(arena_at(x, j, L.off_slots + set * L.set_bytes));
-    fl.base[j] = reinterpret_cast<float*>(arena_at(x, j, L.off_lslots + set * L.lset_bytes));
-  }
-  dh.rows_per_owner = fl.rows_per_owner = R > 0 ? R : 1;
-  dh.src_row = fl.src_row = (long long)x->rank * R;
-  dh.ld = x->d_s;
-  fl.ld = 1;
-  dh.sys_fence = fl.sys_fence = 1;
+  const RowDst dh = p2p_dh_dst(x, L, set, p->n_tokens, false), fl = p2p_dh_dst(x, L, set, p->n_tokens, true);
   long long rec_plane = p->n_tokens, rec_rank = 5ll * p->n_tokens;
   if (!recs) {  // the records all-gathered into this rank's arena by kd_vocab_stats_p2p: wait for all of them
     recs = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_recs + set * L.rset_bytes));
@@ -1398,12 +1411,10 @@ static kd_status vocab_fix_setup(Ctx& c, const kd_problem* p, void* workspace, s
   return KD_OK;
 }
 
-kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
-                            const uint8_t* mask, const float* recs, int32_t n_ranks, float* kj, void* workspace,
-                            size_t workspace_bytes, void* stream) {
-  Ctx c{};
-  kd_status st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, n_ranks);
-  if (st != KD_OK) return st;
+static kd_status vocab_partials_impl(Ctx& c, const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                     const void* W_s, const uint8_t* mask, const float* recs, long long rec_plane,
+                                     long long rec_rank, int32_t n_ranks, float* kj, long long kj_plane,
+                                     void* workspace, size_t workspace_bytes) {
   const Plan& P = c.P;
   if (P.N == 0) return KD_OK;
   if (!recs || !kj) return fail(KD_ERR_INVALID_ARG, "recs / kj is NULL");
@@ -1412,29 +1423,40 @@ kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_
   // kd_vocab_finish's output, not this call's
   kd_problem q = *p;
   q.want_dW = 0;
+  kd_status st;
   if ((st = check_common(&q, h_t, W_t, h_s, W_s, kj, kj, nullptr, workspace, workspace_bytes, P)) != KD_OK) return st;
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
-  KD_CUDA(cudaMemsetAsync(kj, 0, (size_t)2 * P.N * sizeof(float), c.s));
-  KD_LAUNCH(K_MERGE, launch_merge(recs, (long long)P.N, 5ll * P.N, n_ranks, P.Nc, 0, c.n_eff, P.kind, 0,
+  KD_CUDA(cudaMemsetAsync(kj, 0, (size_t)2 * kj_plane * sizeof(float), c.s));
+  KD_LAUNCH(K_MERGE, launch_merge(recs, rec_plane, rec_rank, n_ranks, P.Nc, 0, c.n_eff, P.kind, 0,
                                   ws_at<float>(c.ws, P.off_fstats), nullptr, nullptr, 0, c.idx, 1, c.nonfinite, 0, c.s));
   if ((st = grad_chunk(c, 0)) != KD_OK) return st;
   PassParams pp = pass_params(c, 0);
-  KD_LAUNCH(K_KFIX, launch_kj_rows(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, 0, c.n_eff, c.idx, kj,
-                                   (long long)P.N, c.s));
+  KD_LAUNCH(K_KFIX, launch_kj_rows(pp.kpart, P.n_split * epi_parts(2, P.kind), P.Nc, 0, c.n_eff, c.idx, kj, kj_plane,
+                                   c.s));
   return KD_OK;
 }
 
-kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
-                          const uint8_t* mask, const float* kj_all, int32_t n_ranks, float* loss,
-                          float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
-                          size_t workspace_bytes, void* stream) {
+kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                            const uint8_t* mask, const float* recs, int32_t n_ranks, float* kj, void* workspace,
+                            size_t workspace_bytes, void* stream) {
   Ctx c{};
   kd_status st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, n_ranks);
   if (st != KD_OK) return st;
+  return vocab_partials_impl(c, p, h_t, W_t, h_s, W_s, mask, recs, c.P.N, 5ll * c.P.N, n_ranks, kj, c.P.N, workspace,
+                             workspace_bytes);
+}
+
+static kd_status vocab_finish_impl(Ctx& c, const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                   const void* W_s, const uint8_t* mask, const float* kj_all, long long kj_plane,
+                                   int32_t n_ranks, float* loss, float* dh_local, const RowDst& dh, float* dW_s,
+                                   int64_t* n_nonfinite, void* workspace, size_t workspace_bytes) {
   const Plan& P = c.P;
   float* dW = p->want_dW ? dW_s : nullptr;
-  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_s_partial, dW, workspace, workspace_bytes, P)) != KD_OK)
+  kd_status st;
+  if ((st = check_common(p, h_t, W_t, h_s, W_s, loss, dh_local, dW, workspace, workspace_bytes, P,
+                         dh_local != nullptr)) != KD_OK)
     return st;
+  if (P.N > 0 && !loss) return fail(KD_ERR_INVALID_ARG, "NULL loss pointer");
   if (dW && !p->accumulate_dW) KD_CUDA(cudaMemsetAsync(dW, 0, (size_t)P.V_r * P.d_s * 4, c.s));
   if (P.N == 0) {
     if (n_nonfinite) KD_CUDA(cudaMemsetAsync(n_nonfinite, 0, 8, c.s));
@@ -1444,8 +1466,74 @@ kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t,
   // the prologue is deterministic in the inputs: it rebuilds the same row compaction / packed rows that
   // kd_vocab_partials used, leaving the chunk's G planes in the workspace untouched
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
-  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_s_partial, P.d_s, c.s));
-  return finish_chunk(c, 0, loss, local_rows(dh_s_partial, c.P.d_s), dW, kj_all, n_ranks);
+  if (mask) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_local, P.d_s, c.s));
+  return finish_chunk(c, 0, loss, dh, dW, kj_all, n_ranks, 0, kj_plane);
+}
+
+kd_status kd_vocab_finish(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                          const uint8_t* mask, const float* kj_all, int32_t n_ranks, float* loss,
+                          float* dh_s_partial, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  Ctx c{};
+  kd_status st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, n_ranks);
+  if (st != KD_OK) return st;
+  if (c.P.N > 0 && !dh_s_partial) return fail(KD_ERR_INVALID_ARG, "NULL input/output pointer");
+  return vocab_finish_impl(c, p, h_t, W_t, h_s, W_s, mask, kj_all, c.P.N, n_ranks, loss, dh_s_partial,
+                           local_rows(dh_s_partial, c.P.d_s), dW_s, n_nonfinite, workspace, workspace_bytes);
+}
+
+// JSD/TVD shards with the peer exchange: records and (K, J) partials through the arena, dh to the owners.
+kd_status kd_vocab_partials_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
+                                const void* W_s, const uint8_t* mask, void* workspace, size_t workspace_bytes,
+                                const kd_p2p* x, int32_t set, uint32_t records_target, void* stream) {
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  Ctx c{};
+  if ((st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, x->world)) != KD_OK) return st;
+  if (set < 0 || set >= kP2PSets) return fail(KD_ERR_INVALID_ARG, "set must be in [0, %d)", kP2PSets);
+  if (p->n_tokens > x->max_rows) return fail(KD_ERR_SHAPE, "n_tokens exceeds the arena's max_rows");
+  if (p->d_s != x->d_s) return fail(KD_ERR_SHAPE, "problem d_s != kd_p2p.d_s");
+  const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->n_tokens > 0)
+    KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrRecords)), x->world,
+                                     records_target, s));
+  const float* recs = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_recs + set * L.rset_bytes));
+  const long long kslot = L.off_kj + set * L.kjset_bytes + (long long)x->rank * 2 * L.rplane * 4;
+  float* kj = reinterpret_cast<float*>(arena_at(x, x->rank, kslot));
+  if ((st = vocab_partials_impl(c, p, h_t, W_t, h_s, W_s, mask, recs, L.rplane, 5ll * L.rplane, x->world, kj,
+                                L.rplane, workspace, workspace_bytes)) != KD_OK)
+    return st;
+  return p2p_allgather(x, kslot, 2, p->n_tokens, L.rplane, kCtrKJ, s);
+}
+
+kd_status kd_vocab_finish_p2p(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s, const void* W_s,
+                              const uint8_t* mask, float* loss, float* dW_s, int64_t* n_nonfinite, void* workspace,
+                              size_t workspace_bytes, const kd_p2p* x, int32_t set, uint32_t kj_target,
+                              void* stream) {
+  kd_status st = check_p2p(x);
+  if (st != KD_OK) return st;
+  Ctx c{};
+  if ((st = vocab_fix_setup(c, p, workspace, workspace_bytes, stream, x->world)) != KD_OK) return st;
+  if (set < 0 || set >= kP2PSets) return fail(KD_ERR_INVALID_ARG, "set must be in [0, %d)", kP2PSets);
+  if (p->n_tokens > x->max_rows) return fail(KD_ERR_SHAPE, "n_tokens exceeds the arena's max_rows");
+  if (p->d_s != x->d_s) return fail(KD_ERR_SHAPE, "problem d_s != kd_p2p.d_s");
+  const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->n_tokens > 0)
+    KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrKJ)), x->world,
+                                     kj_target, s));
+  const float* kj_all = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_kj + set * L.kjset_bytes));
+  if ((st = vocab_finish_impl(c, p, h_t, W_t, h_s, W_s, mask, kj_all, L.rplane, x->world, loss, nullptr,
+                              p2p_dh_dst(x, L, set, p->n_tokens, false), dW_s, n_nonfinite, workspace,
+                              workspace_bytes)) != KD_OK)
+    return st;
+  // publish: every owner's arrival counter [rank] + 1 (also for an empty chunk)
+  P2PFlags f{};
+  f.n = x->world;
+  for (int j = 0; j < x->world; ++j) f.f[j] = reinterpret_cast<unsigned*>(arena_at(x, j, kCtrArrivals + 4 * x->rank));
+  KD_LAUNCH(K_P2P, launch_p2p_signal(f, s));
+  return KD_OK;
 }
 
 kd_status kd_gemm_bf16_f32(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,

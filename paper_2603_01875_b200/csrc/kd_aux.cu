@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(256) k_p2p_combine(const P2PCombine c) {
 
 __global__ void __launch_bounds__(256) k_p2p_copy(const P2PCopy c) {
   const long long per = (c.rows + 3) / 4;  // float4 groups per plane (plane and the slot are 16-B aligned)
-  const long long total = 5 * per;
+  const long long total = c.planes * per;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
     const long long f = e / per, k = (e % per) * 4;
     const float* src = c.src + f * c.plane + k;
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(256) k_p2p_copy(const P2PCopy c) {
 }
 
 cudaError_t launch_p2p_copy(const P2PCopy& c, int num_sms, cudaStream_t s) {
-  const long long work = 5 * ((c.rows + 3) / 4);
+  const long long work = c.planes * ((c.rows + 3) / 4);
   const int blocks = (int)std::max(1ll, std::min<long long>(num_sms, (work + 255) / 256));
   k_p2p_copy<<<blocks, 256, 0, s>>>(c);
   return cudaGetLastError();

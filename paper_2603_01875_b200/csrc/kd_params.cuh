@@ -130,11 +130,13 @@ struct P2PCombine {
   long long R, n_rows;              // rows per owner (ceil(n_rows / P)) and the chunk's rows
 };
 // kd_vocab_stats_p2p: this rank's record planes [5][plane] (rows < `rows` valid) copied into n_dst peers' slots.
+// The all-gather of a per-rank block: this rank's [planes][plane] f32 block (rows < `rows` valid) copied into the same
+// slot of n_dst peers' arenas (records: 5 planes, JSD/TVD (K, J): 2).
 struct P2PCopy {
   const float* src;
   float* dst[kP2PMaxRanks];
-  int n_dst;
-  long long n, rows, plane;
+  int n_dst, planes;
+  long long rows, plane;
 };
 struct P2PFlags {
   unsigned* f[kP2PMaxRanks];        // this rank's counter slot in each destination arena (as mapped here)

@@ -23,6 +23,7 @@ EXPORTED = ("kd_check_problem", "kd_workspace_size", "kd_fused_fwd_bwd", "kd_tea
             "kd_teacher_topk", "kd_topk_fwd_bwd",
             "kd_vocab_stats", "kd_vocab_backward",
             "kd_vocab_partials", "kd_vocab_finish", "kd_p2p_arena_bytes", "kd_p2p_outputs", "kd_vocab_stats_p2p", "kd_vocab_backward_p2p",
+            "kd_vocab_partials_p2p", "kd_vocab_finish_p2p",
             "kd_p2p_combine", "kd_p2p_wait", "kd_handoff_export", "kd_handoff_open", "kd_handoff_close",
             "kd_gemm_bf16_f32",
             "kd_last_launch_count", "kd_profile_enable", "kd_profile_read", "kd_profile_kernel_name",
@@ -97,6 +98,10 @@ def lib() -> ctypes.CDLL:
     L.kd_vocab_backward_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, i32, vp, vp, i64p, vp, sz, X, i32, ctypes.c_uint32,
                                         vp]
     L.kd_vocab_backward_p2p.restype = ctypes.c_int
+    L.kd_vocab_partials_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, sz, X, i32, ctypes.c_uint32, vp]
+    L.kd_vocab_partials_p2p.restype = ctypes.c_int
+    L.kd_vocab_finish_p2p.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, i64p, vp, sz, X, i32, ctypes.c_uint32, vp]
+    L.kd_vocab_finish_p2p.restype = ctypes.c_int
     L.kd_p2p_combine.argtypes = [X, i32, ctypes.c_int64, ctypes.c_int64, vp, i32, ctypes.c_uint32, vp]
     L.kd_p2p_combine.restype = ctypes.c_int
     L.kd_p2p_wait.argtypes = [X, ctypes.c_uint32, vp]
@@ -478,6 +483,49 @@ def vocab_backward_p2p(h_t, W_t_shard, h_s, W_s_shard, recs, mask=None, *, x: KD
                                        _ptr(dW_s) if want_dW else None, _ptr(nnf), _ptr(ws), ws.numel(),
                                        ctypes.byref(x), int(set), int(records_target) & 0xFFFFFFFF,
                                        _stream_handle(stream)))
+    return KDResult(loss, None, dW_s if want_dW else None, nnf)
+
+
+def vocab_partials_p2p(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, x: KDP2P, set: int, vocab, v_begin, T=1.0,
+                       kind="jsd", beta=0.5, loss_scale=1.0, want_dW=False, accumulate_dW=False,
+                       records_target: int, stream=None) -> VocabFixState:
+    """kd_vocab_partials_p2p: merge the arena's records of set ``set``, pass 2, (K, J) partials into every rank's
+    arena.  Returns the state kd_vocab_finish_p2p needs (the problem and the workspace holding the G planes)."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(t, "input") for t in (h_t, W_t_shard, h_s, W_s_shard))
+    N, d_t = h_t.shape
+    V_r, d_s = W_s_shard.shape
+    dev = h_t.device
+    p = make_problem(N, d_t, d_s, vocab, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                     accumulate_dW=accumulate_dW, v_begin=v_begin, v_end=v_begin + V_r, chunk_tokens=max(1, N))
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    ws = torch.empty(max(workspace_size(p), 256), dtype=torch.uint8, device=dev)  # carries the G planes to finish
+    _check(lib().kd_vocab_partials_p2p(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                       _ptr(mask), _ptr(ws), ws.numel(), ctypes.byref(x), int(set),
+                                       int(records_target) & 0xFFFFFFFF, _stream_handle(stream)))
+    return VocabFixState(p, ws)
+
+
+def vocab_finish_p2p(state, h_t, W_t_shard, h_s, W_s_shard, mask=None, *, x: KDP2P, set: int, kj_target: int,
+                     dW_s=None, stream=None) -> KDResult:
+    """kd_vocab_finish_p2p: (K, J) sums from the arena, loss (local), G fix-up, dW_s rows, partial dh rows to the
+    owners' slots."""
+    h_t, W_t_shard, h_s, W_s_shard = (_as_bf16(t, "input") for t in (h_t, W_t_shard, h_s, W_s_shard))
+    p = state.problem
+    N = int(p.n_tokens)
+    V_r, d_s = W_s_shard.shape
+    dev = h_t.device
+    if mask is not None:
+        mask = mask.to(device=dev, dtype=torch.uint8).contiguous()
+    loss = torch.empty(N, dtype=torch.float32, device=dev)
+    nnf = torch.zeros(1, dtype=torch.int64, device=dev)
+    want_dW = bool(p.want_dW)
+    if want_dW and dW_s is None:
+        dW_s = (torch.zeros if p.accumulate_dW else torch.empty)(V_r, d_s, dtype=torch.float32, device=dev)
+    _check(lib().kd_vocab_finish_p2p(ctypes.byref(p), _ptr(h_t), _ptr(W_t_shard), _ptr(h_s), _ptr(W_s_shard),
+                                     _ptr(mask), _ptr(loss), _ptr(dW_s) if want_dW else None, _ptr(nnf),
+                                     _ptr(state.workspace), state.workspace.numel(), ctypes.byref(x), int(set),
+                                     int(kj_target) & 0xFFFFFFFF, _stream_handle(stream)))
     return KDResult(loss, None, dW_s if want_dW else None, nnf)
 
 

@@ -161,7 +161,7 @@ def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str) -> int:
 
 
 class P2PExchange:
-    """One rank's end of the peer-memory exchange of the FKL/RKL vocab-sharded step (kdfused.h kd_p2p).
+    """One rank's end of the peer-memory exchange of the vocab-sharded step (kdfused.h kd_p2p).
 
     Each rank owns an arena (receive slots, counters, the step's dh_out / loss_out) and maps every peer's arena:
     the library's kernels then push the partial dh_s rows straight from the dh reduction into their owners' slots
@@ -266,7 +266,7 @@ def _p2p_step(ex: P2PExchange, spans, stats_p2p, backward_p2p, combine, wait, ou
         if i >= 3:
             wait(ex, ex.done_target(g - 3))
         r = backward_p2p(i, ex.set_of(g), dW, ex.records_target(g))
-        if kind == "rkl":
+        if kind != "fkl":  # RKL / JSD / TVD: every rank derives the full loss itself
             if loss_rkl is None:  # the kernels' dtype (fp32; the CPU test stand-ins return fp64)
                 loss_rkl = torch.zeros(N, dtype=r.loss.dtype, device=r.loss.device)
             loss_rkl[a:b] = r.loss
@@ -279,9 +279,9 @@ def _p2p_step(ex: P2PExchange, spans, stats_p2p, backward_p2p, combine, wait, ou
         wait(ex, ex.done_target(base + n - 1))
     ex.chunks = base + n
     dh_out, loss_out = outputs(ex, N)
-    if kind == "rkl" and loss_rkl is None:  # no tokens
+    if kind != "fkl" and loss_rkl is None:  # no tokens
         loss_rkl = torch.zeros(0, dtype=torch.float32, device=device)
-    return _Result(loss_rkl if kind == "rkl" else loss_out, dh_out, dW)
+    return _Result(loss_rkl if kind != "fkl" else loss_out, dh_out, dW)
 
 
 def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: int, v_begin: int, group=None,
@@ -307,10 +307,12 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
     contributes its own batch, bench.py's 2-D grid), every rank keeps dh_s / loss of its own slice only: one
     reduce-scatter at the end instead of the per-chunk all-reduces.
 
-    ``exchange`` (a P2PExchange, FKL/RKL, dh_reduce="all"): the partial dh_s / FKL loss leave the library's dh
+    ``exchange`` (a P2PExchange, dh_reduce="all"): records (and JSD/TVD's (K, J) partials) are all-gathered and the
+    partial dh_s / FKL loss leave the library's dh
     reduction straight into their owners' slots in peer memory and the owners' rank-order sums land in every rank's
     arena (kdfused.h kd_p2p) — no NCCL call for the dh exchange; the returned dh_s / loss are views of the arena,
-    valid until the next step on it.  ``p2p_fns`` substitutes {backward, combine, wait, outputs} (CPU stand-ins).
+    valid until the next step on it.  ``p2p_fns`` substitutes {stats, backward, partials, finish, combine, wait, outputs}
+    (CPU stand-ins).
 
     ``chunk_tokens`` is the library's internal token chunk (kd_problem.chunk_tokens, 0 = its default).  The
     kernel-side callables default to the CUDA entry points; tests substitute CPU stand-ins to exercise this exchange
@@ -343,13 +345,14 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
         return _all_gather_async(rec, group)
 
     if exchange is not None:
-        if fix or dh_reduce != "all":
-            raise ValueError("the peer exchange serves the FKL/RKL step with dh_reduce='all'")
+        if dh_reduce != "all":
+            raise ValueError("the peer exchange serves dh_reduce='all'")
         if N > exchange.max_tokens or chunk > exchange.max_rows:
             raise ValueError(f"step of {N} tokens / exchange chunk {chunk} exceeds the arena "
                              f"({exchange.max_tokens} / {exchange.max_rows})")
         from . import kdfused
-        f = dict(stats=kdfused.vocab_stats_p2p, backward=kdfused.vocab_backward_p2p, combine=kdfused.p2p_combine,
+        f = dict(stats=kdfused.vocab_stats_p2p, backward=kdfused.vocab_backward_p2p,
+                 partials=kdfused.vocab_partials_p2p, finish=kdfused.vocab_finish_p2p, combine=kdfused.p2p_combine,
                  wait=kdfused.p2p_wait, outputs=lambda ex, n: kdfused.p2p_outputs(ex.x, h_t.device, n, d_s))
         f.update(p2p_fns or {})
 
@@ -360,6 +363,14 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
 
         def backward_p2p(i, set_, dW_cur, rec_target):
             a, b = spans[i]
+            m_c = None if mask is None else mask[a:b]
+            acc = accumulate_dW or i > 0
+            if fix:  # JSD/TVD: (K, J) partials all-gathered through the arena between the two calls
+                st = f["partials"](h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, m_c, x=exchange.x, set=set_, vocab=vocab,
+                                   v_begin=v_begin, T=T, kind=kind, beta=beta, loss_scale=loss_scale,
+                                   want_dW=want_dW, accumulate_dW=acc, records_target=rec_target)
+                return f["finish"](st, h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, m_c, x=exchange.x, set=set_,
+                                   kj_target=rec_target, dW_s=dW_cur if i > 0 else dW_s)
             return f["backward"](h_t[a:b], W_t_shard, h_s[a:b], W_s_shard, None,
                                  None if mask is None else mask[a:b], x=exchange.x, set=set_, vocab=vocab,
                                  v_begin=v_begin, T=T, kind=kind, loss_scale=loss_scale, want_dW=want_dW,
@@ -428,13 +439,14 @@ def token_sharded_dW_reduce(dW_s: torch.Tensor, group=None) -> torch.Tensor:
     return dW_s
 
 
-def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0, kind="fkl", loss_scale=1.0,
-                              want_dW=False, chunk_tokens=0, exchange_chunk=0):
+def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0, kind="fkl", beta=0.5,
+                              loss_scale=1.0, want_dW=False, chunk_tokens=0, exchange_chunk=0):
     """One-GPU emulation of the P-rank p2p step (tests, ``bench.py --sim-p2p``): the P ranks' kernels run in one
     stream in an order where every counter a kernel waits on was raised by an EARLIER launch (per exchange chunk: all
-    ranks' stats_p2p, then all ranks' backward_p2p, then all owners' combine) — no kernel waits on one launched after it,
-    so nothing depends on two launches running concurrently.  The kernels, slot addressing, counters and set rotation
-    are the multi-GPU ones; the 'peer' arenas are local allocations (``P2PExchange.local_group``).
+    ranks' stats_p2p, then all ranks' backward_p2p — JSD/TVD: all partials_p2p, then all finish_p2p — then all owners'
+    combine) — no kernel waits on one launched after it, so nothing depends on two launches running concurrently.
+    The kernels, slot addressing, counters and set rotation are the multi-GPU ones; the 'peer' arenas are local
+    allocations (``P2PExchange.local_group``).
 
     Returns per rank (loss, dh_s view, dW_s rows)."""
     from . import kdfused
@@ -443,31 +455,45 @@ def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0
     bounds = vocab_shard_bounds(V, P)
     N = h_t.shape[0]
     d_s = W_s.shape[1]
+    fix = kind in ("jsd", "tvd")
     chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, -(-V // P), kind)
     spans = [(a, min(N, a + chunk)) for a in range(0, N, chunk)]
     base = exchanges[0].chunks
     dW = [None] * P
-    loss_rkl = [torch.zeros(N, dtype=torch.float32, device=h_t.device) for _ in range(P)] if kind == "rkl" else None
+    loss_loc = [torch.zeros(N, dtype=torch.float32, device=h_t.device) for _ in range(P)] if kind != "fkl" else None
     for i, (a, b) in enumerate(spans):
         m_c = None if mask is None else mask[a:b]
         g = base + i
         for r, (v0, v1) in enumerate(bounds):  # every rank's record into every rank's arena
             kdfused.vocab_stats_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], m_c, x=exchanges[r].x,
                                     set=exchanges[r].set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
-                                    chunk_tokens=chunk_tokens)
+                                    chunk_tokens=(b - a) if fix else chunk_tokens)
+        for r, (v0, v1) in enumerate(bounds):
+            if i >= 3:
+                kdfused.p2p_wait(exchanges[r].x, exchanges[r].done_target(g - 3))
+        states = []
+        if fix:
+            for r, (v0, v1) in enumerate(bounds):
+                ex = exchanges[r]
+                states.append(kdfused.vocab_partials_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], m_c, x=ex.x,
+                                                         set=ex.set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
+                                                         beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                                                         accumulate_dW=i > 0, records_target=ex.records_target(g)))
         for r, (v0, v1) in enumerate(bounds):
             ex = exchanges[r]
-            if i >= 3:
-                kdfused.p2p_wait(ex.x, ex.done_target(g - 3))
-            res = kdfused.vocab_backward_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], None, m_c, x=ex.x,
-                                             set=ex.set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
-                                             loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=i > 0,
-                                             dW_s=dW[r], chunk_tokens=chunk_tokens,
-                                             records_target=ex.records_target(g))
+            if fix:
+                res = kdfused.vocab_finish_p2p(states[r], h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], m_c, x=ex.x,
+                                               set=ex.set_of(g), kj_target=ex.records_target(g), dW_s=dW[r])
+            else:
+                res = kdfused.vocab_backward_p2p(h_t[a:b], W_t[v0:v1], h_s[a:b], W_s[v0:v1], None, m_c, x=ex.x,
+                                                 set=ex.set_of(g), vocab=V, v_begin=v0, T=T, kind=kind,
+                                                 loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=i > 0,
+                                                 dW_s=dW[r], chunk_tokens=chunk_tokens,
+                                                 records_target=ex.records_target(g))
             if want_dW:
                 dW[r] = res.dW_s
-            if kind == "rkl":
-                loss_rkl[r][a:b] = res.loss
+            if kind != "fkl":
+                loss_loc[r][a:b] = res.loss
         for r in range(P):
             ex = exchanges[r]
             kdfused.p2p_combine(ex.x, ex.set_of(g), b - a, a, m_c, with_loss=(kind == "fkl"),
@@ -478,5 +504,5 @@ def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0
             kdfused.p2p_wait(ex.x, ex.done_target(base + len(spans) - 1))
         ex.chunks = base + len(spans)
         dh, ls = kdfused.p2p_outputs(ex.x, h_t.device, N, d_s)
-        out.append((loss_rkl[r] if kind == "rkl" else ls, dh, dW[r]))
+        out.append((loss_loc[r] if kind != "fkl" else ls, dh, dW[r]))
     return out

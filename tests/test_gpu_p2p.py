@@ -1,4 +1,4 @@
-"""Peer-memory exchange of the vocab-sharded FKL/RKL step (kdfused.h kd_p2p) on one GPU.
+"""Peer-memory exchange of the vocab-sharded step (FKL / RKL / JSD / TVD) (kdfused.h kd_p2p) on one GPU.
 
 P ranks run in one process against P local arenas (sharding.vocab_sharded_p2p_one_gpu): the same kernels, slot
 addressing, counters and slot-set rotation as the multi-GPU path, launched in an order where no kernel waits on a
@@ -21,7 +21,7 @@ def kd():
     return m
 
 
-def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind):
+def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind, beta=0.5):
     """The NCCL path's arithmetic: per exchange chunk, each shard's partial dh_s / loss from kd_vocab_backward, summed
     over shards in rank order in fp32 (what the owner's combine does)."""
     N, d_s = Hs.shape[0], Ws.shape[1]
@@ -30,13 +30,22 @@ def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind):
     dW = [None] * len(bounds)
     for i, (a, b) in enumerate(spans):
         m_c = None if m is None else m[a:b]
+        fix = kind in ("jsd", "tvd")
         recs = torch.stack([kd().vocab_stats(Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], m_c, vocab=V, v_begin=v0, T=T,
-                                             kind=kind) for v0, v1 in bounds])
+                                             kind=kind, chunk_tokens=(b - a) if fix else 0) for v0, v1 in bounds])
         acc_dh = torch.zeros(b - a, d_s, device="cuda")
         acc_l = torch.zeros(b - a, device="cuda")
+        if fix:
+            parts = [kd().vocab_partials(Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], recs, m_c, vocab=V, v_begin=v0, T=T,
+                                         kind=kind, beta=beta, want_dW=True, accumulate_dW=i > 0)
+                     for v0, v1 in bounds]
+            kj_all = torch.stack([kj for kj, _ in parts])
         for r, (v0, v1) in enumerate(bounds):
-            res = kd().vocab_backward(Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], recs, m_c, vocab=V, v_begin=v0, T=T,
-                                      kind=kind, want_dW=True, accumulate_dW=i > 0, dW_s=dW[r])
+            if fix:
+                res = kd().vocab_finish(parts[r][1], Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], kj_all, m_c, dW_s=dW[r])
+            else:
+                res = kd().vocab_backward(Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], recs, m_c, vocab=V, v_begin=v0,
+                                          T=T, kind=kind, want_dW=True, accumulate_dW=i > 0, dW_s=dW[r])
             dW[r] = res.dW_s
             acc_dh = acc_dh + res.dh_s
             acc_l = acc_l + res.loss if kind == "fkl" else res.loss
@@ -46,7 +55,7 @@ def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind):
 
 
 @pytest.mark.parametrize("P,kind,N,chunk", [(2, "fkl", 520, 128), (3, "rkl", 520, 128), (8, "fkl", 517, 128),
-                                            (4, "rkl", 300, 0)])
+                                            (4, "rkl", 300, 0), (2, "jsd", 520, 128), (3, "tvd", 517, 256)])
 def test_p2p_exchange_equals_rank_order_sum(P, kind, N, chunk):
     from paper_2603_01875_b200.sharding import P2PExchange, vocab_shard_bounds, vocab_sharded_p2p_one_gpu
     d_t, d_s, V, T = 256, 128, 5000, 1.5
@@ -58,9 +67,10 @@ def test_p2p_exchange_equals_rank_order_sum(P, kind, N, chunk):
     c = chunk if chunk > 0 else N
     spans = [(a, min(N, a + c)) for a in range(0, N, c)]
     exs = P2PExchange.local_group(P, d_s, max_rows=c, max_tokens=N)
-    ref_loss, ref_dh, ref_dW = _reference(Ht, Wt, Hs, Ws, m, spans, bounds, V=V, T=T, kind=kind)
+    beta = 0.3
+    ref_loss, ref_dh, ref_dW = _reference(Ht, Wt, Hs, Ws, m, spans, bounds, V=V, T=T, kind=kind, beta=beta)
     for step in range(2):  # the second step reuses the arenas: counters continue, slot sets keep rotating
-        out = vocab_sharded_p2p_one_gpu(Ht, Wt, Hs, Ws, m, exchanges=exs, T=T, kind=kind, want_dW=True,
+        out = vocab_sharded_p2p_one_gpu(Ht, Wt, Hs, Ws, m, exchanges=exs, T=T, kind=kind, beta=beta, want_dW=True,
                                         exchange_chunk=c)
         torch.cuda.synchronize()
         assert all(ex.chunks == (step + 1) * len(spans) for ex in exs)
@@ -68,7 +78,7 @@ def test_p2p_exchange_equals_rank_order_sum(P, kind, N, chunk):
             assert torch.equal(dh, ref_dh), f"rank {r} step {step}: dh_s differs from the rank-order sum"
             assert torch.equal(loss, ref_loss), f"rank {r} step {step}: loss differs"
             assert torch.equal(dW, ref_dW[r]), f"rank {r} step {step}: dW_s rows differ"
-    loss, dh_ref, dW_ref = oracle_run(inp, T=T, kind=kind, want_dW=True)
+    loss, dh_ref, dW_ref = oracle_run(inp, T=T, kind=kind, beta=beta, want_dW=True)
     assert_kd_close("loss (p2p)", out[0][0].cpu().numpy(), loss, LOSS_RTOL, LOSS_ATOL)
     assert_grad_close("dh_s (p2p)", out[0][1].cpu().numpy(), dh_ref)
     dW = torch.cat([o[2] for o in out]).cpu().numpy()

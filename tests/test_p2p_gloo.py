@@ -1,7 +1,7 @@
 """Multi-process (world_size 2, gloo, CPU) test of the host protocol of the peer-memory exchange
 (sharding.vocab_sharded_fwd_bwd(exchange=P2PExchange), kdfused.h kd_p2p).
 
-The CUDA kernels and peer mappings cannot run here, so the five kernel-side callables are CPU stand-ins over
+The CUDA kernels and peer mappings cannot run here, so the kernel-side callables are CPU stand-ins over
 shared-memory "arenas" created by the parent: the stats stand-in writes its record into every rank's record set and
 raises their record counters; the backward stand-in waits for the P records and writes each partial dh_s / loss row into its
 owner's receive slot (owner = row // R, R = ceil(n / P)) of the chunk's slot set and then raises its arrival
@@ -22,7 +22,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from tests.test_sharding_gloo import _backward_standin, _stats_standin
+from tests.test_sharding_gloo import _backward_standin, _finish_standin, _partials_standin, _stats_standin
 
 N, D_T, D_S, V, CHUNK, WORLD = 40, 32, 24, 300, 8, 2
 
@@ -40,7 +40,9 @@ def _arena(world, max_rows, max_tokens, d_s):
     return dict(arr=torch.zeros(world, dtype=torch.int64).share_memory_(),    # [src]: chunks src pushed here
                 done=torch.zeros(world, dtype=torch.int64).share_memory_(),   # [owner]: chunks owner combined
                 nrec=torch.zeros(world, dtype=torch.int64).share_memory_(),   # [src]: records src wrote here
+                nkj=torch.zeros(world, dtype=torch.int64).share_memory_(),    # [src]: (K, J) src wrote here
                 recs=torch.zeros(3, world, 5, max_rows, dtype=torch.float64).share_memory_(),
+                kj=torch.zeros(3, world, 2, max_rows, dtype=torch.float64).share_memory_(),
                 slots=torch.zeros(3, world, R, d_s, dtype=torch.float64).share_memory_(),
                 lslots=torch.zeros(3, world, R, dtype=torch.float64).share_memory_(),
                 dh=torch.zeros(max_tokens, d_s, dtype=torch.float64).share_memory_(),
@@ -84,18 +86,49 @@ def _backward_p2p_standin(h_t, Wt, h_s, Ws, recs, mask, *, x, set, vocab, v_begi
     r = _backward_standin(h_t, Wt, h_s, Ws, recs, mask, vocab=vocab, v_begin=v_begin, T=T, kind=kind,
                           loss_scale=loss_scale, want_dW=want_dW, accumulate_dW=accumulate_dW, dW_s=dW_s,
                           chunk_tokens=chunk_tokens)
+    _push_rows(x, set, n, mask, r.dh_s, r.loss)
+    r.dh_s = None
+    if kind != "rkl":
+        r.loss = None
+    return r
+
+
+def _push_rows(x, set, n, mask, dh, loss):
     R = -(-n // x.world)
     for row in range(n):  # masked rows are not pushed (the owner writes their zeros)
         if mask is not None and mask[row] == 0:
             continue
         j = row // R
-        x.arenas[j]["slots"][set, x.rank, row - j * R] = r.dh_s[row]
-        x.arenas[j]["lslots"][set, x.rank, row - j * R] = r.loss[row]
+        x.arenas[j]["slots"][set, x.rank, row - j * R] = dh[row]
+        if loss is not None:
+            x.arenas[j]["lslots"][set, x.rank, row - j * R] = loss[row]
     for a in x.arenas:
         a["arr"][x.rank] += 1
+
+
+def _partials_p2p_standin(h_t, Wt, h_s, Ws, mask, *, x, set, vocab, v_begin, T, kind, beta, loss_scale, want_dW,
+                          accumulate_dW, records_target):
+    me = x.arenas[x.rank]
+    n = h_t.shape[0]
+    time.sleep(0.004 * x.rank)
+    _poll(lambda: int(me["nrec"].min()) >= records_target, f"records {records_target}")
+    kj, st = _partials_standin(h_t, Wt, h_s, Ws, me["recs"][set, :, :, :n].clone(), mask, vocab=vocab,
+                               v_begin=v_begin, T=T, kind=kind, beta=beta, loss_scale=loss_scale, want_dW=want_dW,
+                               accumulate_dW=accumulate_dW, chunk_tokens=n)
+    for a in x.arenas:  # the (K, J) all-gather through the arenas
+        a["kj"][set, x.rank, :, :n] = kj
+    for a in x.arenas:
+        a["nkj"][x.rank] += 1
+    return st
+
+
+def _finish_p2p_standin(st, h_t, Wt, h_s, Ws, mask, *, x, set, kj_target, dW_s=None):
+    me = x.arenas[x.rank]
+    n = h_t.shape[0]
+    _poll(lambda: int(me["nkj"].min()) >= kj_target, f"kj {kj_target}")
+    r = _finish_standin(st, h_t, Wt, h_s, Ws, me["kj"][set, :, :, :n].clone(), mask, dW_s=dW_s)
+    _push_rows(x, set, n, mask, r.dh_s, None)
     r.dh_s = None
-    if kind != "rkl":
-        r.loss = None
     return r
 
 
@@ -137,13 +170,14 @@ def _worker(rank, world, port, kind, arenas, q):
         a, b = vocab_shard_bounds(V, world, granule=16)[rank]
         ex = P2PExchange(world, rank, D_S, CHUNK, N, [0] * world, own=None)
         ex.x = _X(rank, arenas)
-        fns = dict(stats=_stats_p2p_standin, backward=_backward_p2p_standin, combine=_combine_standin,
-                   wait=_wait_standin,
+        fns = dict(stats=_stats_p2p_standin, backward=_backward_p2p_standin, partials=_partials_p2p_standin,
+                   finish=_finish_p2p_standin, combine=_combine_standin, wait=_wait_standin,
                    outputs=lambda e, n: (e.x.arenas[e.rank]["dh"][:n].clone(), e.x.arenas[e.rank]["loss"][:n].clone()))
         outs = []
         for step in range(2):  # counters and slot sets carry over into the second step
             r = vocab_sharded_fwd_bwd(ht, Wt[a:b], hs, Ws[a:b], torch.tensor(mask), vocab=V, v_begin=a, T=1.3,
-                                      kind=kind, want_dW=True, exchange_chunk=CHUNK, exchange=ex, p2p_fns=fns)
+                                      kind=kind, beta=0.3, want_dW=True, exchange_chunk=CHUNK, exchange=ex,
+                                      p2p_fns=fns)
             outs.append((r.loss.numpy().copy(), r.dh_s.numpy().copy(), r.dW_s.numpy().copy()))
             dist.barrier()  # the next step overwrites dh_out: both ranks have read this one
         q.put((rank, (a, b), ex.chunks, outs))
@@ -151,7 +185,7 @@ def _worker(rank, world, port, kind, arenas, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["fkl", "rkl"])
+@pytest.mark.parametrize("kind", ["fkl", "rkl", "jsd", "tvd"])
 def test_p2p_exchange_protocol_world2(kind):
     import kd_inputs as KI
     from oracle.kd_oracle import kd_fused_fwd_bwd
@@ -170,7 +204,7 @@ def test_p2p_exchange_protocol_world2(kind):
     inp = KI.make_inputs(N, D_T, D_S, V, seed=4, mask=mask)
     f = KI.bf16_to_f64
     loss, dh, dW = kd_fused_fwd_bwd(f(inp.H_t), f(inp.W_t), f(inp.H_s), f(inp.W_s), mask, T=1.3, kind=kind,
-                                    want_dW=True)
+                                    beta=0.3, want_dW=True)
     dW_cat = np.zeros_like(dW)
     n_chunks = -(-N // CHUNK)
     for rank, (a, b), chunks, outs in res:
@@ -183,3 +217,4 @@ def test_p2p_exchange_protocol_world2(kind):
     for a in arenas:  # every owner combined every chunk of both steps for every rank
         assert int(a["done"].sum()) == WORLD * 2 * n_chunks and int(a["arr"].sum()) == WORLD * 2 * n_chunks
         assert int(a["nrec"].sum()) == WORLD * 2 * n_chunks
+        assert int(a["nkj"].sum()) == (WORLD * 2 * n_chunks if kind in ("jsd", "tvd") else 0)
