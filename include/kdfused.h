@@ -15,7 +15,7 @@
  * The vocabulary is swept in 256-column tiles (SM-pair UMMA, 256 tokens x 256 vocab rows) with an online
  * log-sum-exp, so no [tokens × V] logit tensor exists in HBM (BASELINE.json north_star).  Definitions and the
  * readings of points the paper leaves open (no T² factor, β convention, reduction, masking) are in DESIGN.md
- * "Readings" R1-R20.
+ * "Readings" R1-R22.
  *
  * Conventions for every entry point
  *  - All tensor pointers are DEVICE pointers (cudaMalloc / PyTorch CUDA memory), row-major, owned by
@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define KDFUSED_ABI_VERSION 2
+#define KDFUSED_ABI_VERSION 3  /* 3: the peer-memory exchange (kd_p2p) */
 
 typedef enum {
   KD_FKL = 0, /* forward KL  Σ p ln(p/q) */

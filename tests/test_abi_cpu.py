@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(kdfused.EXPORTED)
-    assert L.kd_abi_version() == 2
+    assert L.kd_abi_version() == 3
 
 
 def test_struct_layout_matches_header():
