@@ -21,7 +21,7 @@ def kd():
     return m
 
 
-def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind, beta=0.5):
+def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind, beta=0.5, want_dW=True):
     """The NCCL path's arithmetic: per exchange chunk, each shard's partial dh_s / loss from kd_vocab_backward, summed
     over shards in rank order in fp32 (what the owner's combine does)."""
     N, d_s = Hs.shape[0], Ws.shape[1]
@@ -37,7 +37,7 @@ def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind, beta=0.5):
         acc_l = torch.zeros(b - a, device="cuda")
         if fix:
             parts = [kd().vocab_partials(Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], recs, m_c, vocab=V, v_begin=v0, T=T,
-                                         kind=kind, beta=beta, want_dW=True, accumulate_dW=i > 0)
+                                         kind=kind, beta=beta, want_dW=want_dW, accumulate_dW=i > 0)
                      for v0, v1 in bounds]
             kj_all = torch.stack([kj for kj, _ in parts])
         for r, (v0, v1) in enumerate(bounds):
@@ -45,7 +45,7 @@ def _reference(Ht, Wt, Hs, Ws, m, spans, bounds, *, V, T, kind, beta=0.5):
                 res = kd().vocab_finish(parts[r][1], Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], kj_all, m_c, dW_s=dW[r])
             else:
                 res = kd().vocab_backward(Ht[a:b], Wt[v0:v1], Hs[a:b], Ws[v0:v1], recs, m_c, vocab=V, v_begin=v0,
-                                          T=T, kind=kind, want_dW=True, accumulate_dW=i > 0, dW_s=dW[r])
+                                          T=T, kind=kind, want_dW=want_dW, accumulate_dW=i > 0, dW_s=dW[r])
             dW[r] = res.dW_s
             acc_dh = acc_dh + res.dh_s
             acc_l = acc_l + res.loss if kind == "fkl" else res.loss
@@ -100,3 +100,35 @@ def test_p2p_argument_errors():
     with pytest.raises(K.KDError) as e:
         K.p2p_wait(bad, 0)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("name,P", [("c2", 8), ("c3_jsd", 4)])
+def test_p2p_full_vocab_sampled(name, P):
+    """BASELINE config shapes (d_t 4096, d_s 2048, V = 151936; c3: T = 2, prompt/padding mask), 8192 tokens in
+    2048-token exchange chunks, P emulated ranks: the p2p result equals the rank-order sum of the shards' partials bit
+    for bit on every rank, and 48 sampled tokens match the fp64 oracle."""
+    from paper_2603_01875_b200.sharding import P2PExchange, vocab_shard_bounds, vocab_sharded_p2p_one_gpu
+    cfg = KI.CONFIGS[name]
+    N, c = 8192, 2048
+    W_t, W_s = KI.make_heads(cfg.vocab, cfg.d_t, cfg.d_s, seed=1000)
+    H_t, H_s = KI.make_hidden(N, W_t, W_s, seed=1001, head_seed=1000)
+    mask = KI.make_mask(KI.KDConfig(**{**cfg.__dict__, "n_seq": N // cfg.seq_len})) if cfg.mask != "none" else None
+    inp = KI.KDInputs(H_t, W_t, H_s, W_s, mask)
+    Ht, Hs, Wt, Ws = dev_bf16(H_t), dev_bf16(H_s), dev_bf16(W_t), dev_bf16(W_s)
+    m = None if mask is None else torch.from_numpy(mask).cuda()
+    bounds = vocab_shard_bounds(cfg.vocab, P)
+    spans = [(a, min(N, a + c)) for a in range(0, N, c)]
+    ref_loss, ref_dh, _ = _reference(Ht, Wt, Hs, Ws, m, spans, bounds, V=cfg.vocab, T=cfg.temperature, kind=cfg.kind,
+                                     beta=cfg.jsd_beta, want_dW=False)
+    exs = P2PExchange.local_group(P, cfg.d_s, max_rows=c, max_tokens=N)
+    out = vocab_sharded_p2p_one_gpu(Ht, Wt, Hs, Ws, m, exchanges=exs, T=cfg.temperature, kind=cfg.kind,
+                                    beta=cfg.jsd_beta, exchange_chunk=c)
+    torch.cuda.synchronize()
+    for r, (loss, dh, _) in enumerate(out):
+        assert torch.equal(dh, ref_dh), f"rank {r}: dh_s differs from the rank-order sum"
+        assert torch.equal(loss, ref_loss), f"rank {r}: loss differs"
+    live = np.arange(N) if mask is None else np.flatnonzero(mask)
+    rows = np.sort(np.random.default_rng(3).choice(live, 48, replace=False))
+    loss, dh, _ = oracle_run(inp, T=cfg.temperature, kind=cfg.kind, beta=cfg.jsd_beta, rows=rows)
+    assert_kd_close("loss (p2p, full V)", out[0][0].cpu().numpy()[rows], loss, LOSS_RTOL, LOSS_ATOL)
+    assert_grad_close("dh_s (p2p, full V)", out[0][1].cpu().numpy()[rows], dh)
