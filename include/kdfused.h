@@ -215,6 +215,9 @@ kd_status kd_vocab_backward(const kd_problem* p, const void* h_t, const void* W_
  *   kd_p2p_wait(done target)                  before a slot set is reused (chunk c+3 waits for
  *                                              done >= base + c + 1 from every owner) and before
  *                                              dh_out/loss_out are read (done >= base + n_chunks)
+ * dh_out / loss_out hold the step's result until the owners' combines of the NEXT step rewrite them; those cannot
+ * start before this rank's kd_vocab_backward_p2p of the next step, so a consumer enqueued on this rank's stream
+ * before its next step is safe (on another stream: order it before the next step's calls).
  * A rank may defer kd_p2p_combine(c) behind its next chunk's kernels (sharding.py does), hiding the wait, and
  * run kd_vocab_stats_p2p(c+1) before kd_vocab_backward_p2p(c) — record set (c+1) % 3 was last read by chunk c-2,
  * whose combine (which waited for every rank's backward of c-2) this rank has already run.
