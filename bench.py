@@ -172,7 +172,9 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
+                "power_w_max": max(power) if power else None,
+                "power_w_median": statistics.median(power) if power else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
 
 
 # ------------------------------------------------------------------------------------------- oracle timing
@@ -865,6 +867,11 @@ def main():
                 "clocks": clocks, "e2e": e2e,
                 "gpu_launches": int(round(launches_per_step * args.steps)), "roofline": roofline, "cpu_baseline": cpu,
                 "useful_flop_frac": useful_frac, "kernels": kernels, "nonfinite_tokens": nonfinite,
+                "energy": ({"tokens_per_joule": value / clocks["power_w_median"],
+                            "power_w_median": clocks["power_w_median"],
+                            "note": "the step runs on the B200's software power cap: throughput = power budget / "
+                                    "energy per token, so tokens per joule is the box-independent figure"}
+                           if world == 1 and isinstance(clocks, dict) and clocks.get("power_w_median") else None),
                 "timing": {"ms_per_step": "median of the K timed steps (per-step CUDA events), max over ranks",
                            "ms_per_step_mean": (vleg["ms_per_step_mean"] if vocab_head else t_tok["mean_ms"])},
                 "tokens_loss_bearing_per_gpu": n_eff, **alongside}

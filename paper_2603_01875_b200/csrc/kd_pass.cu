@@ -225,6 +225,12 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
             const CUtensorMap* ma = tch ? &tm_ht : &tm_hs;
             const CUtensorMap* mb = tch ? &tm_wt : &tm_ws;
+#ifdef KD_X_H_LAST  // experiment: the hidden chunk's tiles kept resident (evict_last), the heads unhinted
+            if (CG == 2) {
+              tma_load_2d_pair_hint(ma, &full[st], sA + st * C::kABytes, k, row, kEvictLast);
+              tma_load_2d_pair(mb, &full[st], sB + st * C::kBBytes, k, vrow);
+            } else
+#endif
             if (CG == 2 && (p.l2_hints & 1)) {
               // the hidden chunk (~50 MB) is re-read for every vocab tile: keep it; the heads stream through
               tma_load_2d_pair_hint(ma, &full[st], sA + st * C::kABytes, k, row, kEvictLast);
@@ -752,6 +758,9 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         float4* zsm = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256) + r_in_tile;
         constexpr int kChunks = BN / 32;
         const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
+#ifdef KD_X_STAGE_HINT
+        const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
+#endif
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
 #ifdef KD_EPI_TIMING
           long long tw = 0, tt = 0, ts = 0, t0 = clock64();
@@ -774,6 +783,14 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (c == c_end - 1) release(buf);
               float4* zc = (c < SCH ? zsm : zrow) + (size_t)c * 8 * kBM;
 #ifndef KD_X_NOSTAGE  // experiment builds only: no staging traffic (the student half reuses its own logits)
+#ifdef KD_X_STAGE_HINT  // experiment: the L2 half of the staging kept resident (evict_last), read back evict_first
+              if (c >= SCH) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  st_global_f4_hint(zc + j * kBM, make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]),
+                                    pol_last);
+              } else
+#endif
 #pragma unroll
               for (int j = 0; j < 8; ++j) zc[j * kBM] = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
 #else
@@ -807,7 +824,11 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (p.side_lo == 0) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
+#ifdef KD_X_STAGE_HINT
+                  const float4 v = c >= SCH ? ld_global_f4_hint(zc + j * kBM, pol_first) : zc[j * kBM];
+#else
                   const float4 v = zc[j * kBM];
+#endif
                   zt[4 * j] = v.x;
                   zt[4 * j + 1] = v.y;
                   zt[4 * j + 2] = v.z;
