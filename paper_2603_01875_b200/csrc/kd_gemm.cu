@@ -198,6 +198,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int c_beg = part * kChunks / kParts, c_end = (part + 1) * kChunks / kParts;
     const uint32_t lane_addr = (q4 * 32) << 16;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+#ifndef KD_X_NO_GEMM_SLAB_HINT
+    const uint64_t pol_last = l2_policy_evict_last();
+#endif
     uint32_t it = 0;
     for (int u = worker; u < n_units; u += n_workers) {
       int m0, n0, kb0, kb1, ks;
@@ -227,6 +230,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (!row_ok || n0 + c * 32 >= p.N) continue;
           float* o = orow + c * 32;
+#ifndef KD_X_NO_GEMM_SLAB_HINT
+          // split-K slab tiles (EPI_STORE: the dh GEMM) are stored evict_last, so a unit's promotion pieces find their
+          // tile in L2 instead of DRAM (ncu, c2 chunk: DRAM writes 603 -> 118 MB, reads 3.41 -> 2.94 GB per launch;
+          // profiles/r02_ab.md).  dW (EPI_ACCUM, 1.2 GB of tiles re-read every chunk) stays unhinted.
+          if (EPI == EPI_STORE) {
+            if (accumulate) {
+              if (empty_k) continue;
+              float4 prev[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) prev[i] = __ldcg(reinterpret_cast<const float4*>(o + 4 * i));
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                st_global_f4_hint(o + 4 * i, make_float4(prev[i].x + v[4 * i], prev[i].y + v[4 * i + 1],
+                                                         prev[i].z + v[4 * i + 2], prev[i].w + v[4 * i + 3]), pol_last);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                st_global_f4_hint(o + 4 * i, empty_k ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                     : make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]),
+                                  pol_last);
+            }
+            continue;
+          }
+#endif
           if (accumulate) {
             if (empty_k) continue;
             float4 prev[8];

@@ -225,8 +225,12 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
             const CUtensorMap* ma = tch ? &tm_ht : &tm_hs;
             const CUtensorMap* mb = tch ? &tm_wt : &tm_ws;
-#ifdef KD_X_H_LAST  // experiment: the hidden chunk's tiles kept resident (evict_last), the heads unhinted
+#if defined(KD_X_H_LAST) || defined(KD_X_H_LAST1)  // experiment: the hidden chunk's tiles evict_last (KD_X_H_LAST1: pass 1 only)
+#ifdef KD_X_H_LAST1
+            if (CG == 2 && PASS == 1) {
+#else
             if (CG == 2) {
+#endif
               tma_load_2d_pair_hint(ma, &full[st], sA + st * C::kABytes, k, row, kEvictLast);
               tma_load_2d_pair(mb, &full[st], sB + st * C::kBBytes, k, vrow);
             } else
@@ -758,7 +762,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
         float4* zsm = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256) + r_in_tile;
         constexpr int kChunks = BN / 32;
         const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
-#ifdef KD_X_STAGE_HINT
+#ifndef KD_X_NO_STAGE_HINT
         const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
 #endif
         for (int vt = ur.vt0; vt < ur.vt1; ++vt) {
@@ -783,7 +787,11 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (c == c_end - 1) release(buf);
               float4* zc = (c < SCH ? zsm : zrow) + (size_t)c * 8 * kBM;
 #ifndef KD_X_NOSTAGE  // experiment builds only: no staging traffic (the student half reuses its own logits)
-#ifdef KD_X_STAGE_HINT  // experiment: the L2 half of the staging kept resident (evict_last), read back evict_first
+#ifndef KD_X_NO_STAGE_HINT
+              // the L2 half of the staging is stored evict_last and read back evict_first: otherwise the heads and G
+              // streaming through L2 in the ~30 µs between the two half-tiles evict the dirty lines, which then cost
+              // a DRAM write-back and a DRAM re-read (ncu: pass-2 DRAM writes 1.80 -> 1.32 GB per c2 launch, reads
+              // 5.4-5.8 -> 4.95 GB; pass 2 -3.6% in a same-box A/B, profiles/r02_ab.md)
               if (c >= SCH) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -824,7 +832,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
               if (p.side_lo == 0) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-#ifdef KD_X_STAGE_HINT
+#ifndef KD_X_NO_STAGE_HINT
                   const float4 v = c >= SCH ? ld_global_f4_hint(zc + j * kBM, pol_first) : zc[j * kBM];
 #else
                   const float4 v = zc[j * kBM];
