@@ -225,6 +225,16 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             const int k = (tch ? (p.kb_t - 1 - kb) : (p.kb_s - 1 - (kb - p.kb_t))) * kBK;
             const CUtensorMap* ma = tch ? &tm_ht : &tm_hs;
             const CUtensorMap* mb = tch ? &tm_wt : &tm_ws;
+#if defined(KD_X_W_LAST) || defined(KD_X_W_LAST1)  // experiment: the heads' tiles evict_last (KD_X_W_LAST1: pass 1 only)
+#ifdef KD_X_W_LAST1
+            if (CG == 2 && PASS == 1) {
+#else
+            if (CG == 2) {
+#endif
+              tma_load_2d_pair(ma, &full[st], sA + st * C::kABytes, k, row);
+              tma_load_2d_pair_hint(mb, &full[st], sB + st * C::kBBytes, k, vrow, kEvictLast);
+            } else
+#endif
 #if defined(KD_X_H_LAST) || defined(KD_X_H_LAST1)  // experiment: the hidden chunk's tiles evict_last (KD_X_H_LAST1: pass 1 only)
 #ifdef KD_X_H_LAST1
             if (CG == 2 && PASS == 1) {
