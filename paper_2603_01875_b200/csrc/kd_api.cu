@@ -1082,6 +1082,13 @@ kd_status kd_topk_fwd_bwd(const kd_problem* p, const void* h_s, const void* W_s,
   return KD_OK;
 }
 
+// A wait of the peer exchange to enqueue after an entry point's argument checks, before its first kernel.
+struct P2PWaitArg {
+  const unsigned* ctr = nullptr;  // counters [n], one per source rank
+  int n = 0;
+  unsigned target = 0;
+};
+
 // Stats of one shard into `rec` (plane stride rec_plane >= N): kd_vocab_stats (local) and kd_vocab_stats_p2p
 // (straight into this rank's slot of the arena's record set).
 static kd_status vocab_stats_impl(const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
@@ -1133,7 +1140,7 @@ static kd_status vocab_backward_impl(const kd_problem* p, const void* h_t, const
                                      long long rec_rank_stride, int32_t n_ranks,
                                      float* loss, float* dh_local, const RowDst& dh_dst, const RowDst& floss_dst,
                                      float* dW_s, int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
-                                     void* stream, bool p2p) {
+                                     void* stream, bool p2p, const P2PWaitArg& pre = P2PWaitArg{}) {
   kd_status st = validate_unstaged(p, false);
   if (st != KD_OK) return st;
   if (p->kind != KD_FKL && p->kind != KD_RKL)
@@ -1156,6 +1163,8 @@ static kd_status vocab_backward_impl(const kd_problem* p, const void* h_t, const
     if (n_nonfinite) KD_CUDA(cudaMemsetAsync(n_nonfinite, 0, 8, c.s));
     return KD_OK;
   }
+  // the peer exchange's wait for the records (after every argument check, before the first kernel)
+  if (pre.ctr) KD_LAUNCH(K_P2P, launch_p2p_wait(pre.ctr, pre.n, pre.target, c.s));
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
   // masked rows: local outputs zeroed here; in the peer exchange the owner writes their zeros (k_p2p_combine)
   if (mask && (loss || dh_local)) KD_LAUNCH(K_ZERO, launch_zero_masked(mask, P.N, loss, dh_local, P.d_s, c.s));
@@ -1317,17 +1326,18 @@ kd_status kd_vocab_backward_p2p(const kd_problem* p, const void* h_t, const void
   const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
   const RowDst dh = p2p_dh_dst(x, L, set, p->n_tokens, false), fl = p2p_dh_dst(x, L, set, p->n_tokens, true);
   long long rec_plane = p->n_tokens, rec_rank = 5ll * p->n_tokens;
+  P2PWaitArg pre{};
   if (!recs) {  // the records all-gathered into this rank's arena by kd_vocab_stats_p2p: wait for all of them
     recs = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_recs + set * L.rset_bytes));
     rec_plane = L.rplane;
     rec_rank = 5ll * L.rplane;
-    KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrRecords)), x->world,
-                                     records_target,
-                                     static_cast<cudaStream_t>(stream)));
+    pre.ctr = reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrRecords));
+    pre.n = x->world;
+    pre.target = records_target;
   }
   if ((st = vocab_backward_impl(p, h_t, W_t, h_s, W_s, mask, recs, rec_plane, rec_rank, n_ranks,
                                 p->kind == KD_RKL ? loss : nullptr, nullptr, dh, fl, dW_s, n_nonfinite, workspace,
-                                workspace_bytes, stream, true)) != KD_OK)
+                                workspace_bytes, stream, true, pre)) != KD_OK)
     return st;
   // publish: every owner's arrival counter + 1 (one per rank per exchange chunk, also for an empty chunk)
   P2PFlags f{};
@@ -1414,7 +1424,7 @@ static kd_status vocab_fix_setup(Ctx& c, const kd_problem* p, void* workspace, s
 static kd_status vocab_partials_impl(Ctx& c, const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
                                      const void* W_s, const uint8_t* mask, const float* recs, long long rec_plane,
                                      long long rec_rank, int32_t n_ranks, float* kj, long long kj_plane,
-                                     void* workspace, size_t workspace_bytes) {
+                                     void* workspace, size_t workspace_bytes, const P2PWaitArg& pre = P2PWaitArg{}) {
   const Plan& P = c.P;
   if (P.N == 0) return KD_OK;
   if (!recs || !kj) return fail(KD_ERR_INVALID_ARG, "recs / kj is NULL");
@@ -1425,6 +1435,7 @@ static kd_status vocab_partials_impl(Ctx& c, const kd_problem* p, const void* h_
   q.want_dW = 0;
   kd_status st;
   if ((st = check_common(&q, h_t, W_t, h_s, W_s, kj, kj, nullptr, workspace, workspace_bytes, P)) != KD_OK) return st;
+  if (pre.ctr) KD_LAUNCH(K_P2P, launch_p2p_wait(pre.ctr, pre.n, pre.target, c.s));
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, nullptr)) != KD_OK) return st;
   KD_CUDA(cudaMemsetAsync(kj, 0, (size_t)2 * kj_plane * sizeof(float), c.s));
   KD_LAUNCH(K_MERGE, launch_merge(recs, rec_plane, rec_rank, n_ranks, P.Nc, 0, c.n_eff, P.kind, 0,
@@ -1449,7 +1460,8 @@ kd_status kd_vocab_partials(const kd_problem* p, const void* h_t, const void* W_
 static kd_status vocab_finish_impl(Ctx& c, const kd_problem* p, const void* h_t, const void* W_t, const void* h_s,
                                    const void* W_s, const uint8_t* mask, const float* kj_all, long long kj_plane,
                                    int32_t n_ranks, float* loss, float* dh_local, const RowDst& dh, float* dW_s,
-                                   int64_t* n_nonfinite, void* workspace, size_t workspace_bytes) {
+                                   int64_t* n_nonfinite, void* workspace, size_t workspace_bytes,
+                                   const P2PWaitArg& pre = P2PWaitArg{}) {
   const Plan& P = c.P;
   float* dW = p->want_dW ? dW_s : nullptr;
   kd_status st;
@@ -1463,6 +1475,7 @@ static kd_status vocab_finish_impl(Ctx& c, const kd_problem* p, const void* h_t,
     return KD_OK;
   }
   if (!kj_all) return fail(KD_ERR_INVALID_ARG, "kj_all is NULL");
+  if (pre.ctr) KD_LAUNCH(K_P2P, launch_p2p_wait(pre.ctr, pre.n, pre.target, c.s));
   // the prologue is deterministic in the inputs: it rebuilds the same row compaction / packed rows that
   // kd_vocab_partials used, leaving the chunk's G planes in the workspace untouched
   if ((st = prologue(c, h_t, W_t, h_s, W_s, mask, n_nonfinite)) != KD_OK) return st;
@@ -1495,14 +1508,15 @@ kd_status kd_vocab_partials_p2p(const kd_problem* p, const void* h_t, const void
   if (p->d_s != x->d_s) return fail(KD_ERR_SHAPE, "problem d_s != kd_p2p.d_s");
   const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (p->n_tokens > 0)
-    KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrRecords)), x->world,
-                                     records_target, s));
+  P2PWaitArg pre{};
+  pre.ctr = reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrRecords));
+  pre.n = x->world;
+  pre.target = records_target;
   const float* recs = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_recs + set * L.rset_bytes));
   const long long kslot = L.off_kj + set * L.kjset_bytes + (long long)x->rank * 2 * L.rplane * 4;
   float* kj = reinterpret_cast<float*>(arena_at(x, x->rank, kslot));
   if ((st = vocab_partials_impl(c, p, h_t, W_t, h_s, W_s, mask, recs, L.rplane, 5ll * L.rplane, x->world, kj,
-                                L.rplane, workspace, workspace_bytes)) != KD_OK)
+                                L.rplane, workspace, workspace_bytes, pre)) != KD_OK)
     return st;
   return p2p_allgather(x, kslot, 2, p->n_tokens, L.rplane, kCtrKJ, s);
 }
@@ -1520,13 +1534,14 @@ kd_status kd_vocab_finish_p2p(const kd_problem* p, const void* h_t, const void* 
   if (p->d_s != x->d_s) return fail(KD_ERR_SHAPE, "problem d_s != kd_p2p.d_s");
   const P2PLayout L = p2p_layout(x->world, x->max_rows, x->max_tokens, x->d_s);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (p->n_tokens > 0)
-    KD_LAUNCH(K_P2P, launch_p2p_wait(reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrKJ)), x->world,
-                                     kj_target, s));
+  P2PWaitArg pre{};
+  pre.ctr = reinterpret_cast<const unsigned*>(arena_at(x, x->rank, kCtrKJ));
+  pre.n = x->world;
+  pre.target = kj_target;
   const float* kj_all = reinterpret_cast<const float*>(arena_at(x, x->rank, L.off_kj + set * L.kjset_bytes));
   if ((st = vocab_finish_impl(c, p, h_t, W_t, h_s, W_s, mask, kj_all, L.rplane, x->world, loss, nullptr,
                               p2p_dh_dst(x, L, set, p->n_tokens, false), dW_s, n_nonfinite, workspace,
-                              workspace_bytes)) != KD_OK)
+                              workspace_bytes, pre)) != KD_OK)
     return st;
   // publish: every owner's arrival counter [rank] + 1 (also for an empty chunk)
   P2PFlags f{};

@@ -41,6 +41,8 @@ int main(void) {
          offsetof(kd_problem, temperature), offsetof(kd_problem, loss_scale), offsetof(kd_problem, want_dW),
          offsetof(kd_problem, chunk_tokens), offsetof(kd_problem, grad_precision), offsetof(kd_problem, stage_logits),
          offsetof(kd_problem, reserved));
+  printf("%zu %zu %zu %zu %zu\n", sizeof(kd_p2p), offsetof(kd_p2p, d_s), offsetof(kd_p2p, max_rows),
+         offsetof(kd_p2p, max_tokens), offsetof(kd_p2p, arena));
   return 0;
 }
 '''
@@ -53,6 +55,8 @@ int main(void) {
     P = kdfused.KDProblem
     want = [ctypes.sizeof(P), P.vocab.offset, P.temperature.offset, P.loss_scale.offset, P.want_dW.offset,
             P.chunk_tokens.offset, P.grad_precision.offset, P.stage_logits.offset, P.reserved.offset]
+    X = kdfused.KDP2P
+    want += [ctypes.sizeof(X), X.d_s.offset, X.max_rows.offset, X.max_tokens.offset, X.arena.offset]
     assert got == want
 
 
@@ -169,3 +173,37 @@ def test_product_never_imports_oracle():
                 assert "oracle" not in re.sub(r"#.*|//.*|\"\"\".*?\"\"\"", "", src, flags=re.S), f
                 # no import of the oracle package in any spelling, comments included
                 assert not re.search(r"^\s*(from|import)\s+oracle\b|import_module\(\s*[\"']oracle", src, flags=re.M), f
+
+
+def test_p2p_struct_layout_and_validation():
+    """kd_p2p: arena sizing, and host-side checks of the peer exchange reject bad views before any launch (no GPU
+    needed: they return before any CUDA call); its struct layout is in test_struct_layout_matches_header."""
+    L = kd.lib()
+    assert ctypes.sizeof(kdfused.KDP2P) == 4 * 4 + 2 * 8 + 8 * 8
+    assert L.kd_p2p_arena_bytes(0, 64, 64, 128) == 0 and L.kd_p2p_arena_bytes(9, 64, 64, 128) == 0
+    n = L.kd_p2p_arena_bytes(2, 64, 128, 128)
+    assert n > 0 and n % 256 == 0
+    # 2 ranks, R = 32: slots 3x[2][32][128] f32 + loss 3x[2][32] + records 3x[2][5][64] + (K, J) 3x[2][2][64] + outputs
+    assert n >= 256 + 3 * (2 * 32 * 128 * 4) + 3 * 256 + 3 * (2 * 5 * 64 * 4) + 3 * (2 * 2 * 64 * 4) + 128 * 128 * 4
+    dh, ls = ctypes.c_void_p(), ctypes.c_void_p()
+    assert L.kd_p2p_outputs(None, ctypes.byref(dh), ctypes.byref(ls)) == 1
+    x = kdfused.make_p2p(2, 0, 128, 64, 128, [0x100000, 0x100100 + 8])  # rank 1's arena misaligned
+    assert L.kd_p2p_outputs(ctypes.byref(x), ctypes.byref(dh), ctypes.byref(ls)) == 3
+    x = kdfused.make_p2p(2, 2, 128, 64, 128, [0x100000, 0x200000])  # rank outside [0, world)
+    assert L.kd_p2p_outputs(ctypes.byref(x), ctypes.byref(dh), ctypes.byref(ls)) == 1
+    x = kdfused.make_p2p(2, 1, 128, 64, 128, [0x100000, 0x200000])
+    assert L.kd_p2p_outputs(ctypes.byref(x), ctypes.byref(dh), ctypes.byref(ls)) == 0
+    assert dh.value > 0x200000 and ls.value > dh.value  # rank 1's own arena
+    p = kd.make_problem(64, 64, 128, 1000, v_begin=0, v_end=500)
+    assert L.kd_p2p_combine(ctypes.byref(x), 3, 64, 0, None, 1, 0, None) == 1       # set outside [0, 3)
+    assert L.kd_p2p_combine(ctypes.byref(x), 0, 65, 0, None, 1, 0, None) == 2       # more rows than max_rows
+    assert L.kd_p2p_combine(ctypes.byref(x), 0, 64, 100, None, 1, 0, None) == 2     # past max_tokens
+    rc = L.kd_vocab_backward_p2p(ctypes.byref(p), *([None] * 6), 3, None, None, None, None, 0, ctypes.byref(x), 0,
+                                 0, None)
+    assert rc == 1 and b"n_ranks" in L.kd_last_error()                              # n_ranks != world
+    p_big = kd.make_problem(65, 64, 128, 1000, v_begin=0, v_end=500)
+    rc = L.kd_vocab_stats_p2p(ctypes.byref(p_big), *([None] * 5), None, 0, ctypes.byref(x), 0, None)
+    assert rc == 2                                                                  # n_tokens > max_rows
+    pj = kd.make_problem(64, 64, 128, 1000, kind="fkl", v_begin=0, v_end=500)
+    rc = L.kd_vocab_partials_p2p(ctypes.byref(pj), *([None] * 5), None, 0, ctypes.byref(x), 0, 1, None)
+    assert rc == 4                                                                  # FKL is not a (K, J) kind
