@@ -78,8 +78,8 @@ typedef struct {
   float loss_scale;      /* L = loss_scale · Σ_n mask_n ℓ_n; 1/max(1,Σmask) gives SPEC's mean */
   int32_t want_dW;       /* 0: skip dL/dW_s */
   int32_t accumulate_dW; /* 1: dW_s += (gradient accumulation, P:210 GA=8); 0: dW_s = */
-  int32_t chunk_tokens;  /* token chunk Nc bounding the G scratch (0 = default: ~24 MiB of H_t|H_s rows, clamped to
-                            [1024, 8192], so the chunk stays L2-resident; rounded up to the 256-row pair tile) */
+  int32_t chunk_tokens;  /* token chunk Nc bounding the G scratch (0 = default: ~36 MiB of H_t|H_s rows, clamped to
+                            [1024, 4096], so the chunk stays L2-resident; rounded up to the 256-row pair tile) */
   int32_t grad_precision;/* kd_grad_precision: how G reaches the backward GEMMs */
   int32_t stage_logits;  /* 0 (default): pass 2 recomputes both LM heads to form G — no logit ever reaches HBM.
                             1: the STAGED variant, kd_fused_fwd_bwd only: pass 1 also writes

@@ -540,11 +540,15 @@ static Plan make_plan(const kd_problem* p) {
   P.bn = pass_bn();
   const int bmt = kBM * P.cg;  // token rows per fused-pass work tile
   // Default chunk: the fused passes re-read the chunk's hidden rows for every vocab tile, so they must stay
-  // L2-resident next to the streaming heads: ~24 MiB of H_t|H_s per chunk (measured: c2 at 8192 tokens = 100 MB
-  // of hidden rows runs 12% slower than at 2048; profiles/r01_tuning.md).  KD_CHUNK_TOKENS overrides (experiments).
+  // L2-resident next to the streaming heads, while every chunk streams both heads once per pass from DRAM.  ~36 MiB
+  // of H_t|H_s per chunk, at most 4096 tokens: 3072 at configs 2/3/5, 4096 at config 4.  Measured with the pass-2
+  // staging L2 hints (profiles/r02_ab.md, r02b_ab7/ab8): c2 3072 vs 2048 +0.8 / +2.3% on two boxes (2560 and 3584
+  // lose: 80 / 112 dh-GEMM tiles quantise badly on 74 pair workers), c3 RKL +0.9%, c5 +1.4%; c4 4096 vs 5120 / 6144
+  // +0.8 / +0.6%.  (Round 1, without the hints, preferred 24 MiB: c2 at 8192 tokens ran 12% slower than at 2048.)
+  // KD_CHUNK_TOKENS overrides (experiments).
   static const int nc_env = env_int("KD_CHUNK_TOKENS", 0);
-  int nc_default = (int)((24ll << 20) / ((long long)(P.d_t + P.d_s) * 2));
-  nc_default = nc_default < 1024 ? 1024 : (nc_default > 8192 ? 8192 : nc_default);
+  int nc_default = (int)((36ll << 20) / ((long long)(P.d_t + P.d_s) * 2));
+  nc_default = nc_default < 1024 ? 1024 : (nc_default > 4096 ? 4096 : nc_default);
   if (nc_env > 0) nc_default = nc_env;
   int nc = p->chunk_tokens > 0 ? p->chunk_tokens : nc_default;
   const int n_pad = ((P.N + bmt - 1) / bmt) * bmt;

@@ -430,7 +430,8 @@ def make_p2p(world: int, rank: int, d_s: int, max_rows: int, max_tokens: int, ar
 
 
 def p2p_outputs(x: KDP2P, device, n_tokens: int, d_s: int):
-    """(dh_out [n_tokens, d_s], loss_out [n_tokens]) views of this rank's arena (valid until the next step)."""
+    """(dh_out [n_tokens, d_s], loss_out [n_tokens]) views of this rank's arena: valid until the next step on it, and
+    only while the arena's owner (sharding.P2PExchange.own) is alive — the views do not keep it alive."""
     dh, ls = ctypes.c_void_p(), ctypes.c_void_p()
     _check(lib().kd_p2p_outputs(ctypes.byref(x), ctypes.byref(dh), ctypes.byref(ls)))
     dev = torch.device(device)

@@ -111,8 +111,9 @@ def test_handoff_handle_size_matches_header():
 
 
 def test_default_chunk_keeps_hidden_rows_l2_resident():
-    # default chunk = 24 MiB of H_t|H_s rows: 2048 tokens at d_t + d_s = 6144, 4096 at 3072 (kdfused.h chunk_tokens)
-    for d_t, d_s, nc in ((4096, 2048, 2048), (2048, 1024, 4096)):
+    # default chunk = 36 MiB of H_t|H_s rows, at most 4096 tokens: 3072 tokens at d_t + d_s = 6144, 4096 at 3072
+    # (kdfused.h chunk_tokens; the measurements behind the rule are in profiles/r02_ab.md)
+    for d_t, d_s, nc in ((4096, 2048, 3072), (2048, 1024, 4096)):
         dflt = kd.workspace_size(kd.make_problem(65536, d_t, d_s, 151936))
         explicit = kd.workspace_size(kd.make_problem(65536, d_t, d_s, 151936, chunk_tokens=nc))
         assert dflt == explicit
