@@ -380,13 +380,14 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     return out
 
 
-def p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW):
+def p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW, P=None, steps=None):
     """--sim-p2p P: the P-rank peer-exchange step emulated on one GPU (sharding.vocab_sharded_p2p_one_gpu): every
     rank's kernels in one stream, the peers' arenas local.  The time is the whole job's compute serialised on one GPU
     (so tokens/s ~ the single-GPU headline) plus the exchange kernels; their cost per rank is in the kernel split
     ("p2p": owner sums + counters; the peer stores ride inside reduce_dh).  Local HBM stands in for NVLink."""
     from paper_2603_01875_b200 import sharding
-    P = args.sim_p2p
+    P = P or args.sim_p2p
+    steps = steps or args.steps
     n = Ht.shape[0]
     chunk = sharding.default_exchange_chunk(n, -(-cfg.vocab // P), cfg.kind)
     exs = sharding.P2PExchange.local_group(P, cfg.d_s, max_rows=chunk, max_tokens=n, device=Ht.device)
@@ -397,14 +398,17 @@ def p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW):
                                                      kind=cfg.kind, beta=cfg.jsd_beta, want_dW=want_dW,
                                                      exchange_chunk=chunk)
 
-    t = timer.run(step, args.steps, args.warmup)
-    prof = timer.profiled(kd, step, args.steps)
+    t = timer.run(step, steps, args.warmup)
+    prof = timer.profiled(kd, step, steps)
     n_eff = int(mask.sum().item()) if mask is not None else n
     import torch
     same = all(torch.equal(res["r"][0][1], o[1]) for o in res["r"][1:])
+    del exs
+    torch.cuda.empty_cache()
     return {"ranks_emulated": P, "value": n_eff / (t["median_ms"] / 1e3), "unit": UNIT, "ms_per_step": t["median_ms"],
             "exchange_chunk_tokens": chunk, "all_ranks_same_dh": bool(same),
-            "kernels_ms_per_step": {k: v / args.steps for k, (c, v) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            "steps": steps,
+            "kernels_ms_per_step": {k: v / steps for k, (c, v) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "note": "one GPU runs all P ranks' kernels (no concurrency needed: every counter a kernel waits on was "
                     "raised by an earlier launch); the 'peer' stores go to local HBM, not NVLink"}
 
@@ -841,6 +845,14 @@ def main():
 
     if args.sim_p2p > 1 and world == 1:
         alongside["p2p_one_gpu"] = p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW)
+    elif world == 1 and not args.no_variants and not (args.topk or args.teacher_lse or args.stage):
+        # the peer-memory exchange's kernels at the full workload in every default run: two ranks emulated on this
+        # GPU, 5 timed steps (a failure here is recorded, never allowed to drop the headline line)
+        try:
+            alongside["p2p_one_gpu"] = p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW, P=2,
+                                                       steps=min(5, args.steps))
+        except Exception as e:  # noqa: BLE001
+            alongside["p2p_one_gpu"] = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     if args.handoff and world == 1:
         alongside["handoff"] = handoff_leg(args, cfg, kd, H_t, Ht, Wt, Hs, Ws, mask, kw, out, dW, n_eff, stream, local)
