@@ -700,6 +700,22 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
             return;
           }
 #endif
+#ifdef KD_X_G_FIRST  // experiment: G stores evict_first (they stream to DRAM; keep the staging / H lines)
+          if (two) {
+            const uint64_t gpol = l2_policy_evict_first();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              st_global_b16_hint(ph, (uint16_t)(hi[i] & 0xFFFFu), gpol);
+              st_global_b16_hint(pl, (uint16_t)(lo[i] & 0xFFFFu), gpol);
+              ph += p.n_rows;
+              pl += p.n_rows;
+              st_global_b16_hint(ph, (uint16_t)(hi[i] >> 16), gpol);
+              st_global_b16_hint(pl, (uint16_t)(lo[i] >> 16), gpol);
+              ph += p.n_rows;
+              pl += p.n_rows;
+            }
+          } else
+#endif
           if (two) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
