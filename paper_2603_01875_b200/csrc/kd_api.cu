@@ -751,6 +751,12 @@ static void attach_die(Ctx& c) {
     c.P.die_map = m->dev;
 }
 
+// RKL's pass 1: decoupled with the teacher half-tile staged (default) or the coupled form (KD_RKL_P1_COUPLED=1, A/B).
+static bool rkl_p1_coupled() {
+  static const bool v = env_int("KD_RKL_P1_COUPLED", 0) != 0;
+  return v;
+}
+
 // One fused-pass launch (the die-aware placement counters are zeroed first).
 static kd_status run_pass(Ctx& c, int pass, int kind, bool coupled, const PassParams& pp) {
   if (pp.die_map) KD_CUDA(cudaMemsetAsync(pp.sched, 0, 16, c.s));
@@ -915,11 +921,12 @@ static kd_status fused_impl(const kd_problem* p, const void* h_t, const void* W_
   for (int ch = 0; ch < P.n_chunks; ++ch) {
     const int row0 = ch * P.Nc;
     PassParams pp = pass_params(c, row0);
-    // decoupled pass 1 (independent teacher / student LSEs) for FKL/JSD/TVD; RKL needs its loss in pass 2
+    // decoupled pass 1 (independent teacher / student LSEs) for FKL/JSD/TVD; RKL needs its loss (the cross term U,
+    // both logits per element) in pass 2: decoupled with the teacher half staged (default) or coupled
     const bool coupled = P.kind == KD_RKL;
     if (lse_t) pp.side_lo = 1;  // student half-tiles only
     if (P.stage) pp.zst = ws_at<float>(c.ws, P.off_zst);
-    if ((st = run_pass(c, 1, P.kind, coupled, pp)) != KD_OK) return st;
+    if ((st = run_pass(c, 1, P.kind, coupled && rkl_p1_coupled(), pp)) != KD_OK) return st;
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff, P.kind, 0,
                            ws_at<float>(c.ws, P.off_fstats), loss, nullptr, (long long)P.N, c.idx, 0, c.nonfinite,
                            coupled ? 1 : 0, c.s, lse_t));
@@ -1121,7 +1128,7 @@ static kd_status vocab_stats_impl(const kd_problem* p, const void* h_t, const vo
     // before pass 2.  FKL (loss partials from pass 2, summed over the shards) needs the two LSEs only: the
     // decoupled pass 1, as the fused path
     const bool coupled = P.kind == KD_RKL;
-    if ((st = run_pass(c, 1, P.kind, coupled, pp)) != KD_OK) return st;
+    if ((st = run_pass(c, 1, P.kind, coupled && rkl_p1_coupled(), pp)) != KD_OK) return st;
     KD_LAUNCH(K_MERGE, launch_merge(pp.part, pp.part_plane, P.Nc, P.n_split * epi_parts(1, P.kind), P.Nc, row0, c.n_eff,
                            P.kind, 1, nullptr, nullptr, rec, rec_plane, c.idx, 0, c.nonfinite, 0, c.s));
   }

@@ -109,11 +109,14 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
     kd_pass_kernel(const __grid_constant__ CUtensorMap tm_ht, const __grid_constant__ CUtensorMap tm_wt,
                    const __grid_constant__ CUtensorMap tm_hs, const __grid_constant__ CUtensorMap tm_ws,
                    const PassParams p) {
-  constexpr int SCH = (DEC && PASS == 2) ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
+  // staged decoupled form: pass 2 (all kinds) and RKL's pass 1 (its cross term U needs both logits per element)
+  constexpr bool kStaged = DEC && (PASS == 2 || KIND == KIND_RKL);
+  constexpr int SCH = kStaged ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
   using C = PassCfg<CG, BN, SCH>;
   constexpr int kStages = C::kStages;
   constexpr int kNB = DEC ? 2 : C::kNumBuf;  // accumulator buffers (DEC: one half-tile side per buffer)
-  static_assert(!DEC || PASS == 2 || KIND == KIND_FKL || KIND == KIND_TOPK, "decoupled pass 1 uses the FKL role order");
+  static_assert(!DEC || PASS == 2 || KIND == KIND_FKL || KIND == KIND_TOPK || KIND == KIND_RKL,
+                "decoupled pass 1: FKL role order (one side per half-tile), or RKL with the teacher half staged");
   static_assert(KIND != KIND_TOPK || (PASS == 1 && DEC), "top-k selection is a one-sided decoupled pass 1");
   constexpr int kBMt = kBM * CG;  // token rows per work tile
   extern __shared__ uint8_t smem_raw[];
@@ -468,7 +471,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           }
         }
       }
-    } else if constexpr (DEC && PASS == 1) {
+    } else if constexpr (DEC && PASS == 1 && KIND != KIND_RKL) {
       constexpr int kChunks = BN / 32;
       const int c_beg = part * kChunks / EP, c_end = (part + 1) * kChunks / EP;
       for (int u = u_first; u < u_end; u += u_step) {
@@ -776,8 +779,56 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           kahan_add(Jacc, cJ, jj[0] + jj[1]);
         }
       };
-      if constexpr (DEC && PASS == 2) {
-        // decoupled pass 2: the teacher half-tile's raw fp32 logits are parked in this CTA's private staging
+      // pass 1 (coupled / staged RKL), one 32-column chunk of the tile: both sides' online records and the cross term
+      auto p1chunk = [&](float (&zt)[32], float (&zs)[32], int v0, int nvalid) {
+            if (p.zst && v0 < p.g_ld) {  // staged variant: raw logits of both heads (before the role swap / masking)
+              stage_store(p.zst, zt, v0, p.n_rows, r_local);
+              stage_store(p.zst + (size_t)p.g_ld * p.n_rows, zs, v0, p.n_rows, r_local);
+            }
+            if (nvalid <= 0) return;
+            float* zp = (KIND == KIND_RKL) ? zs : zt;
+            float* zq = (KIND == KIND_RKL) ? zt : zs;
+            if (nvalid < 32) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (i >= nvalid) { zp[i] = -1e30f; zq[i] = -1e30f; }
+            }
+            float cp = zp[0], cq = zq[0];
+#pragma unroll
+            for (int i = 1; i < 32; ++i) { cp = fmaxf(cp, zp[i]); cq = fmaxf(cq, zq[i]); }
+            const float nMp = fmaxf(Mp, cp * alpha), nMq = fmaxf(Mq, cq * alpha);
+            if (Sp == 0.f) {
+              Mp = nMp; Mq = nMq;
+            } else if (nMp > Mp || nMq > Mq) {  // rare: accurate exp2f, compensations rescaled alongside
+              const float dp = nMp - Mp, dq = nMq - Mq;
+              const float fp = exp2f(-dp), fq = exp2f(-dq);
+              U = __fmul_rn(fp, __fsub_rn(__fsub_rn(U, cU), __fmul_rn(__fsub_rn(dp, dq), __fsub_rn(Sp, cSp))));
+              cU = 0.f;
+              Sp = __fmul_rn(fp, __fsub_rn(Sp, cSp));
+              cSp = 0.f;
+              Sq = __fmul_rn(fq, __fsub_rn(Sq, cSq));
+              cSq = 0.f;
+              Mp = nMp; Mq = nMq;
+            }
+            // packed (p, q) lanes: one FFMA2 / FADD2 per element; every KD_EXP_EMU_STRIDE-th element's two exp2
+            // are evaluated on the FMA pipe (exp2_pair) to unload MUFU
+            const float2 a2 = make_float2(alpha, alpha), nm2 = make_float2(-Mp, -Mq);
+            float2 s2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float uu[4] = {0.f, 0.f, 0.f, 0.f};
+            kd_unroll32([&](auto I) {
+              constexpr int i = decltype(I)::value;
+              const float2 x = ffma2(make_float2(zp[i], zq[i]), a2, nm2);
+              const float2 e = exp2_pair<i>(x);
+              s2[i & 3] = fadd2(s2[i & 3], e);
+              uu[i & 3] = fmaf(e.x, x.x - x.y, uu[i & 3]);
+            });
+            const float2 s01 = fadd2(s2[0], s2[1]), s23 = fadd2(s2[2], s2[3]);
+            kahan_add(Sp, cSp, s01.x + s23.x);
+            kahan_add(Sq, cSq, s01.y + s23.y);
+            kahan_add(U, cU, (uu[0] + uu[1]) + (uu[2] + uu[3]));
+      };
+      if constexpr (kStaged) {
+        // decoupled pass 2 (and RKL's pass 1): the teacher half-tile's raw fp32 logits are parked in this CTA's private staging
         // buffer (BN x 128 fp32, L2-resident), freeing its accumulator at once; the student half-tile's epilogue
         // reads them back — same thread, same addresses, so program order suffices — and runs the gradient math
         // while the next vocab tile's teacher MMAs proceed.
@@ -880,7 +931,8 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
 #endif
               if (c == c_end - 1) release(buf);
               const int v0 = vt * BN + c * 32;
-              p2chunk(zt, zs, v0, min(32, p.V_r - v0));
+              if constexpr (PASS == 1) p1chunk(zt, zs, v0, min(32, p.V_r - v0));
+              else p2chunk(zt, zs, v0, min(32, p.V_r - v0));
               if (c >= SCH && (p.l2_hints & 2)) {
                 // the staged lines are dead: drop them from L2 without a write-back (the warp's 4 KB of the chunk)
                 __syncwarp();
@@ -936,51 +988,7 @@ __global__ void __launch_bounds__(pass_threads(EP), 1)
           const int v0 = vbase + c * 32;
           const int nvalid = min(32, p.V_r - v0);  // columns of this chunk inside [0, V_r)
           if (PASS == 1) {
-            if (p.zst && v0 < p.g_ld) {  // staged variant: raw logits of both heads (before the role swap / masking)
-              stage_store(p.zst, zt, v0, p.n_rows, r_local);
-              stage_store(p.zst + (size_t)p.g_ld * p.n_rows, zs, v0, p.n_rows, r_local);
-            }
-            if (nvalid <= 0) continue;
-            float* zp = (KIND == KIND_RKL) ? zs : zt;
-            float* zq = (KIND == KIND_RKL) ? zt : zs;
-            if (nvalid < 32) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i >= nvalid) { zp[i] = -1e30f; zq[i] = -1e30f; }
-            }
-            float cp = zp[0], cq = zq[0];
-#pragma unroll
-            for (int i = 1; i < 32; ++i) { cp = fmaxf(cp, zp[i]); cq = fmaxf(cq, zq[i]); }
-            const float nMp = fmaxf(Mp, cp * alpha), nMq = fmaxf(Mq, cq * alpha);
-            if (Sp == 0.f) {
-              Mp = nMp; Mq = nMq;
-            } else if (nMp > Mp || nMq > Mq) {  // rare: accurate exp2f, compensations rescaled alongside
-              const float dp = nMp - Mp, dq = nMq - Mq;
-              const float fp = exp2f(-dp), fq = exp2f(-dq);
-              U = __fmul_rn(fp, __fsub_rn(__fsub_rn(U, cU), __fmul_rn(__fsub_rn(dp, dq), __fsub_rn(Sp, cSp))));
-              cU = 0.f;
-              Sp = __fmul_rn(fp, __fsub_rn(Sp, cSp));
-              cSp = 0.f;
-              Sq = __fmul_rn(fq, __fsub_rn(Sq, cSq));
-              cSq = 0.f;
-              Mp = nMp; Mq = nMq;
-            }
-            // packed (p, q) lanes: one FFMA2 / FADD2 per element; every KD_EXP_EMU_STRIDE-th element's two exp2
-            // are evaluated on the FMA pipe (exp2_pair) to unload MUFU
-            const float2 a2 = make_float2(alpha, alpha), nm2 = make_float2(-Mp, -Mq);
-            float2 s2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            float uu[4] = {0.f, 0.f, 0.f, 0.f};
-            kd_unroll32([&](auto I) {
-              constexpr int i = decltype(I)::value;
-              const float2 x = ffma2(make_float2(zp[i], zq[i]), a2, nm2);
-              const float2 e = exp2_pair<i>(x);
-              s2[i & 3] = fadd2(s2[i & 3], e);
-              uu[i & 3] = fmaf(e.x, x.x - x.y, uu[i & 3]);
-            });
-            const float2 s01 = fadd2(s2[0], s2[1]), s23 = fadd2(s2[2], s2[3]);
-            kahan_add(Sp, cSp, s01.x + s23.x);
-            kahan_add(Sq, cSq, s01.y + s23.y);
-            kahan_add(U, cU, (uu[0] + uu[1]) + (uu[2] + uu[3]));
+            p1chunk(zt, zs, v0, nvalid);
           } else {
             p2chunk(zt, zs, v0, nvalid);
           }
@@ -1050,7 +1058,7 @@ static cudaError_t launch_pass_t(const CUtensorMap* maps, const PassParams& p, i
     if (p.die_map != nullptr) return launch_pass_t<PASS, KIND, CG, BN, DEC, true>(maps, p, grid, stream);
   }
   auto kern = kd_pass_kernel<PASS, KIND, CG, BN, DEC, DIE>;
-  constexpr int SCH = (DEC && PASS == 2) ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
+  constexpr int SCH = (DEC && (PASS == 2 || KIND == KIND_RKL)) ? (KD_P2_SMEM_STAGE < BN / 32 ? KD_P2_SMEM_STAGE : BN / 32) : 0;
   const int smem = PassCfg<CG, BN, SCH>::kSmem;
   // the shared-memory opt-in once per (instantiation, device): a driver call on every launch was measurable host
   // time for the per-chunk callers
@@ -1084,7 +1092,9 @@ static cudaError_t launch_pass_cg(int pass, int kind, bool coupled, const CUtens
   if (pass == 1) {
     // pass 1 only distinguishes which side is "primary" (RKL swaps the roles) and coupled vs decoupled sides
     if (kind == KIND_TOPK) return launch_pass_t<1, KIND_TOPK, CG, BN, true>(maps, p, grid, stream);
-    if (kind == KIND_RKL) return launch_pass_t<1, KIND_RKL, CG, BN>(maps, p, grid, stream);
+    if (kind == KIND_RKL)  // coupled (both accumulators of a tile live) or decoupled with the teacher half staged
+      return coupled ? launch_pass_t<1, KIND_RKL, CG, BN>(maps, p, grid, stream)
+                     : launch_pass_t<1, KIND_RKL, CG, BN, true>(maps, p, grid, stream);
     return coupled ? launch_pass_t<1, KIND_FKL, CG, BN>(maps, p, grid, stream)
                    : launch_pass_t<1, KIND_FKL, CG, BN, true>(maps, p, grid, stream);
   }
