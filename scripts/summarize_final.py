@@ -73,7 +73,7 @@ def main(d):
     rb = (R["dram__bytes_read.sum"] + R["dram__bytes_write.sum"]) / R["gpu__time_duration.sum"]  # GB/ms = TB/s
     md = f"""# Round 2 (final build) — `ncu --set full` of the default path's kernels
 
-Command (`scripts/gpu/r02b_final3.sh`): `ncu --set full --clock-control none --import-source on -k
+Command (`scripts/gpu/r02b_final5.sh`): `ncu --set full --clock-control none --import-source on -k
 regex:"kd_pass_kernel|kd_gemm_kernel|k_reduce_dh" --launch-skip 4 -c 4 python bench.py --tokens 6144 --steps 1
 --warmup 1 ...` — the SECOND 3072-token chunk (the default chunk) at config-2 shapes (d_t 4096, d_s 2048, V 151936,
 FKL): pass 1, pass 2, dh GEMM, dh reduction.  Raw page exported with `ncu -i … --page raw --csv` (report not
