@@ -336,7 +336,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
               want_dW=want_dW, accumulate_dW=False, group=group, dh_reduce="scatter" if own_tokens else "all")
     p2p = args.exchange == "p2p" and world > 1 and not sim and not own_tokens
     if p2p:  # arenas allocated and peer-mapped once (CUDA IPC), outside the timing
-        chunk_p2p = sharding.default_exchange_chunk(n_all, v1 - v0, cfg.kind)
+        chunk_p2p = sharding.default_exchange_chunk(n_all, v1 - v0, cfg.kind, cfg.d_t, cfg.d_s)
         kw["exchange"] = sharding.P2PExchange.create(group, cfg.d_s, max_rows=chunk_p2p, max_tokens=n_all, device=dev)
     res = {}
 
@@ -347,7 +347,7 @@ def vocab_sharded_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, world, rank, dev, wan
     prof = timer.profiled(kd, step, args.steps)
     ms = t["median_ms"]
     r = res["r"]
-    chunk = sharding.default_exchange_chunk(n_all, v1 - v0, cfg.kind)
+    chunk = sharding.default_exchange_chunk(n_all, v1 - v0, cfg.kind, cfg.d_t, cfg.d_s)
     rec_bytes = 20 * n_all * pv
     kj_bytes = 8 * n_all * pv if cfg.kind in ("jsd", "tvd") else 0
     dh_bytes = 4 * n_all * cfg.d_s
@@ -389,7 +389,7 @@ def p2p_one_gpu_leg(args, cfg, kd, Wt, Ws, Ht, Hs, mask, timer, want_dW, P=None,
     P = P or args.sim_p2p
     steps = steps or args.steps
     n = Ht.shape[0]
-    chunk = sharding.default_exchange_chunk(n, -(-cfg.vocab // P), cfg.kind)
+    chunk = sharding.default_exchange_chunk(n, -(-cfg.vocab // P), cfg.kind, cfg.d_t, cfg.d_s)
     exs = sharding.P2PExchange.local_group(P, cfg.d_s, max_rows=chunk, max_tokens=n, device=Ht.device)
     res = {}
 

@@ -137,7 +137,15 @@ def _all_reduce_async(t: torch.Tensor, group=None):
     return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group, async_op=True)
 
 
-def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str) -> int:
+def library_chunk(d_t: int, d_s: int) -> int:
+    """The library's default token chunk (kd_api.cu make_plan: ~36 MiB of H_t|H_s rows in [1024, 4096], rounded up to
+    the 256-row pair tile) — mirrored here so FKL/RKL exchange chunks hold whole library chunks."""
+    nc = (36 << 20) // (2 * (d_t + d_s))
+    nc = min(4096, max(1024, nc))
+    return -(-nc // 256) * 256
+
+
+def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str, d_t: int = 0, d_s: int = 0) -> int:
     """Tokens per pipelined exchange chunk of the vocab-sharded step.
 
     Each chunk's pass 1 runs while the previous chunk's records are all-gathered, and each chunk's partial-dh
@@ -154,6 +162,12 @@ def default_exchange_chunk(n_tokens: int, v_rows: int, kind: str) -> int:
         cap = max(4096, min(8192, int(5e9 / (12 * max(1, v_rows))) // 256 * 256))
     if n_tokens <= cap:
         return max(1, n_tokens)
+    # FKL/RKL with the widths given: whole library chunks per exchange chunk (c2: 3 x 3072 = 9216 instead of 8192 =
+    # 3072 + 3072 + 2048; simulated P = 8 rank step 17.38 -> 17.09 ms, profiles/r02_ab.md)
+    if kind not in ("jsd", "tvd") and d_t > 0 and d_s > 0:
+        lc = library_chunk(d_t, d_s)
+        per = -(-cap // lc)                       # library chunks per exchange chunk
+        return min(n_tokens, per * lc)
     # balance the chunks: a ragged tail of a few hundred tokens fills a fraction of a wave of output tiles (c3 JSD at
     # P = 2: 5376-token chunks left a 512-token tail, per-rank efficiency 0.86)
     n_chunks = -(-n_tokens // cap)
@@ -329,7 +343,8 @@ def vocab_sharded_fwd_bwd(h_t, W_t_shard, h_s, W_s_shard, mask=None, *, vocab: i
         finish_fn = finish_fn or kdfused.vocab_finish
     N = h_t.shape[0]
     d_s = W_s_shard.shape[1]
-    chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, W_s_shard.shape[0], kind)
+    chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, W_s_shard.shape[0], kind,
+                                                                             W_t_shard.shape[1], d_s)
     if fix and chunk_tokens > 0:
         chunk = min(chunk, chunk_tokens)  # the JSD/TVD pair runs one library chunk per call
     spans = [(a, min(N, a + chunk)) for a in range(0, N, chunk)]
@@ -456,7 +471,7 @@ def vocab_sharded_p2p_one_gpu(h_t, W_t, h_s, W_s, mask=None, *, exchanges, T=1.0
     N = h_t.shape[0]
     d_s = W_s.shape[1]
     fix = kind in ("jsd", "tvd")
-    chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, -(-V // P), kind)
+    chunk = exchange_chunk if exchange_chunk > 0 else default_exchange_chunk(N, -(-V // P), kind, W_t.shape[1], d_s)
     spans = [(a, min(N, a + chunk)) for a in range(0, N, chunk)]
     base = exchanges[0].chunks
     dW = [None] * P
