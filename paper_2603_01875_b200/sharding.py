@@ -215,8 +215,13 @@ class P2PExchange:
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         own = cls._alloc(world, d_s, max_rows, max_tokens, dev)
         torch.cuda.synchronize(dev)
+        shape = (d_s, max_rows, max_tokens, own.numel())
         handles = [None] * world
-        dist.all_gather_object(handles, kdfused.handoff_export(own), group=group)
+        dist.all_gather_object(handles, (shape, kdfused.handoff_export(own)), group=group)
+        if any(sh != shape for sh, _ in handles):  # every rank's kernels address the peers' arenas with ITS layout
+            raise ValueError(f"P2PExchange.create: ranks disagree on (d_s, max_rows, max_tokens, arena bytes): "
+                             f"{[sh for sh, _ in handles]}")
+        handles = [h for _, h in handles]
         ptrs, mapped = [], []
         for j, h in enumerate(handles):
             if j == rank:
